@@ -1,0 +1,40 @@
+"""Shared test fixtures.  GPU tests are marked ``@pytest.mark.gpu``."""
+
+from __future__ import annotations
+
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+REPO = Path(__file__).resolve().parents[1]
+GOLDEN = REPO / "tests" / "golden"
+if str(REPO) not in sys.path:
+    sys.path.insert(0, str(REPO))
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and the built library")
+    config.addinivalue_line("markers", "slow: long-running case")
+
+
+def golden_names():
+    idx = json.loads((GOLDEN / "golden_index.json").read_text())
+    return [m["name"] for m in idx]
+
+
+def golden_meta(name):
+    idx = json.loads((GOLDEN / "golden_index.json").read_text())
+    return next(m for m in idx if m["name"] == name)
+
+
+def load_golden(name):
+    with np.load(GOLDEN / f"{name}.npz") as z:
+        return {k: z[k] for k in z.files}
+
+
+@pytest.fixture
+def rng():
+    return np.random.default_rng(20240817)

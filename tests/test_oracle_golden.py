@@ -1,0 +1,74 @@
+"""Pin the numpy oracle against the reference's own outputs (golden vectors).
+
+The golden files were produced by running the real reference
+(``tests/golden/make_golden.py``); the oracle restates the same numpy
+primitives in the same order, so agreement is asserted BITWISE.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import golden_meta, golden_names, load_golden
+from oracle import mdp_oracle as orc
+
+NAMES = golden_names()
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_spmv_greedy_gather_apply_bitwise(name):
+    g = load_golden(name)
+    rp, col, val, cost, gam = g["row_ptr"], g["col"], g["val"], g["cost"], float(g["gamma"])
+    mx = bool(g["maximize"])
+    np.testing.assert_array_equal(orc.spmv(rp, col, val, g["spmv_x"]), g["spmv_y"])
+    # greedy_policy is called with the instance mode (bellman.py:52)
+    pi, applied = orc.greedy(rp, col, val, cost, gam, g["greedy_v"], maximize=mx)
+    np.testing.assert_array_equal(pi, g["greedy_policy"])
+    np.testing.assert_array_equal(applied, g["greedy_applied"])
+    rpp, cp, vp, gp = orc.gather_policy(rp, col, val, cost, g["greedy_policy"])
+    np.testing.assert_array_equal(rpp, g["gather_row_ptr"])
+    np.testing.assert_array_equal(cp, g["gather_col"])
+    np.testing.assert_array_equal(vp, g["gather_val"])
+    np.testing.assert_array_equal(gp, g["gather_cost"])
+    np.testing.assert_array_equal(orc.apply_J(rpp, cp, vp, gam, g["spmv_x"]), g["apply_y"])
+
+
+@pytest.mark.parametrize("name", NAMES)
+@pytest.mark.parametrize("kind", ["gmres", "richardson"])
+def test_inner_solve_bitwise(name, kind):
+    g = load_golden(name)
+    meta = golden_meta(name)[f"inner_{kind}"]
+    theta, rep = orc.inner_solve(g["gather_row_ptr"], g["gather_col"], g["gather_val"],
+                                 float(g["gamma"]), g["gather_cost"], g["greedy_v"],
+                                 float(g[f"inner_{kind}_target"]), 200, kind)
+    np.testing.assert_array_equal(theta, g[f"inner_{kind}_theta"])
+    assert rep.iterations == meta["iterations"]
+    assert rep.converged == meta["converged"]
+    assert rep.final_linear_residual_2norm == meta["final"]
+
+
+def _solve_cases():
+    out = []
+    for name in NAMES:
+        for kind, s in golden_meta(name)["solves"].items():
+            slow = s["inner"] > 50_000
+            marks = [pytest.mark.slow] if slow else []
+            out.append(pytest.param(name, kind, id=f"{name}-{kind}", marks=marks))
+    return out
+
+
+@pytest.mark.parametrize("name,kind", _solve_cases())
+def test_solve_bitwise(name, kind):
+    g = load_golden(name)
+    s = golden_meta(name)["solves"][kind]
+    if s["inner"] > 50_000:
+        pytest.skip("oracle replay of a non-converging 1e6-iteration run is too slow for CI")
+    res = orc.solve(g["row_ptr"], g["col"], g["val"], g["cost"], float(g["gamma"]),
+                    maximize=bool(g["maximize"]), kind=kind, tol=s["tol"])
+    assert res.status == s["status"]
+    assert res.outer_iterations == s["outer"]
+    assert res.inner_iterations_total == s["inner"]
+    np.testing.assert_array_equal(res.values, g[f"solve_{kind}_values"])
+    np.testing.assert_array_equal(res.policy, g[f"solve_{kind}_policy"])
+    np.testing.assert_array_equal(np.asarray(res.residual_history), g[f"solve_{kind}_history"])
