@@ -1,0 +1,209 @@
+/*
+ * ipi_b200.h — C ABI of the B200-native iPI hot path (libipi_b200.so).
+ *
+ * Drop-in boundary for the reference's Python API (mdpsolve / mdpsolve_frontend,
+ * /root/reference/pkg).  The reference has no FFI: its boundary is a Python
+ * API whose numeric core is numpy.  Every entry point below replaces one
+ * reference function (cited file:line, relative to /root/reference/pkg/src/mdpsolve)
+ * and is bound from Python with ctypes (paper_2507_22538_b200/_lib.py);
+ * INTEGRATION.md shows the binding a reference maintainer would add.
+ *
+ * Conventions
+ *  - All array pointers are DEVICE pointers borrowed from the caller (torch
+ *    tensors); the caller owns them and keeps them alive for the call (for
+ *    ipi_mdp_* handles: for the handle's lifetime).
+ *  - `stream` is a cudaStream_t passed as void*; every call is stream-ordered.
+ *    Calls that return host scalars synchronise that stream.
+ *  - Layout (model.py:112-131): row-stacked (n*m) x n CSR, row s*m+a;
+ *    row_ptr int64, col int32, values fp64; stage cost fp64 (n, m) row-major.
+ *  - Return codes: IPI_OK, or an error whose message ipi_last_error() returns
+ *    (thread-local).  Python maps 1 -> ValidationError (model.py:24),
+ *    2 -> DimensionError (sparse.py:22), 4 -> ResourceLimitError (sparse.py:26),
+ *    3 -> RuntimeError.
+ *  - A handle is used by one host thread at a time (SPEC: one solve owns its workers).
+ */
+#ifndef IPI_B200_H
+#define IPI_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IPI_OK 0
+#define IPI_EVALIDATION 1
+#define IPI_EDIMENSION 2
+#define IPI_ECUDA 3
+#define IPI_ERESOURCE 4
+
+#define IPI_MODE_MIN 0
+#define IPI_MODE_MAX 1
+
+/* inner solver kinds (inner.py:48-54) */
+#define IPI_KSP_RICHARDSON 0
+#define IPI_KSP_GMRES 1
+#define IPI_KSP_BICGSTAB 2
+#define IPI_KSP_TFQMR 3
+
+/* outer status (driver.py:41-44) */
+#define IPI_CONVERGED 0
+#define IPI_OUTER_CAP 1
+#define IPI_STALLED 2
+
+typedef struct ipi_mdp ipi_mdp;
+
+/* Inner-solve report (inner.py:87-95 InnerSolveReport). */
+typedef struct {
+  int32_t iterations;
+  int32_t converged;
+  int32_t breakdown;
+  int32_t pad;
+  double final_linear_residual_2norm;
+  double target_2norm; /* effective target after the floor (inner.py:189) */
+} ipi_inner_report;
+
+/* Solve options (driver.py:47-68 SolveOptions, pc = NONE). */
+typedef struct {
+  double tol;              /* -atol_pi   */
+  double alpha;            /* -alpha     */
+  int32_t max_outer;       /* -max_iter_pi  */
+  int32_t max_inner;       /* -max_iter_ksp */
+  int32_t ksp_type;        /* IPI_KSP_*  */
+  int32_t ksp_max_it;      /* -ksp_max_it, <=0 = unset */
+  double richardson_scale; /* -ksp_richardson_scale */
+  int32_t mode;            /* IPI_MODE_* */
+  int32_t pad;
+} ipi_opts;
+
+/* Solve statistics (driver.py:93-106 SolveResult minus the arrays). */
+typedef struct {
+  int32_t status;
+  int32_t outer_iterations;
+  int64_t inner_iterations_total;
+  double wall_time;
+  double time_greedy;
+  double time_assembly;
+  double time_inner;
+} ipi_stats;
+
+/* Kernel plan chosen at ipi_mdp_create: exposed for reports/tests. */
+typedef struct {
+  int64_t nnz;
+  int32_t row_len_min;
+  int32_t row_len_max;
+  double row_len_mean;
+  int32_t lanes_per_row;   /* G: lanes of a warp that share one CSR row        */
+  int32_t halo;            /* shared-memory V window half-width (states), -1 = none */
+  int32_t k1_blocks;
+  int32_t k1_threads;
+  int32_t k1_smem_bytes;
+  int32_t inner_blocks;
+  int32_t inner_threads;
+  int32_t inner_smem_bytes;
+  int32_t uniform_rows;    /* all rows have the same length: P_pi row_ptr is s*K */
+  int32_t pad;
+} ipi_plan;
+
+/* Validation summary (model.py:148-194 validate; sparse.py:56-86 check). */
+typedef struct {
+  int64_t bad_row_ptr;       /* count of row_ptr decreases (+1 if rp[0]!=0)   */
+  int64_t bad_col_range;     /* count of cols outside [0, n)                  */
+  int64_t bad_col_order;     /* count of non-increasing pairs inside a row    */
+  int64_t nonfinite_values;  /* count of non-finite transition values         */
+  int64_t first_bad_prob;    /* first entry index outside [0,1], -1 if none   */
+  double first_bad_prob_value;
+  int64_t n_bad_row_sums;    /* rows whose |sum-1| > 1e-12                    */
+  int64_t bad_rows[5];       /* first five such rows (ascending)              */
+  double bad_row_sums[5];
+  int64_t nonfinite_cost;    /* first flat index of a non-finite cost, -1 none */
+} ipi_validation;
+
+/* Structural CSR check (sparse.py:56-86 CsrMatrix.check). */
+typedef struct {
+  int64_t nnz;               /* row_ptr[rows]                                  */
+  int64_t nnz_mismatch;      /* row_ptr[rows] != length of col/val arrays       */
+  int64_t bad_row_ptr;       /* decreases in row_ptr (+1 if row_ptr[0] != 0)    */
+  int64_t bad_col_range;
+  int64_t bad_col_order;
+  int64_t nonfinite_values;
+} ipi_csr_report;
+
+const char* ipi_last_error(void);
+int ipi_device_count(void);
+/* Build information string (arch, git-free version). */
+const char* ipi_version(void);
+
+/* CsrMatrix construction check; runs only the row-pointer pass when that fails. */
+int ipi_csr_check(const int64_t* row_ptr, const int32_t* col, const double* val, int64_t rows,
+                  int64_t cols, int64_t nnz_len, ipi_csr_report* out, void* stream);
+
+/* ---- instance handle -------------------------------------------------- */
+/* Borrow an MDP that lives in HBM and plan the kernels for it.
+ * n_local states owned by this rank starting at global state `state0`
+ * (model.py:95-109 make_partition); n_global columns.  Replaces
+ * MdpInstance (model.py:112-141) as the device-side carrier. */
+int ipi_mdp_create(const int64_t* row_ptr, const int32_t* col, const double* values,
+                   const double* stage_cost, int64_t n_local, int64_t n_global, int32_t m,
+                   int64_t state0, double gamma, int32_t mode, void* stream, ipi_mdp** out);
+void ipi_mdp_destroy(ipi_mdp* h);
+int ipi_mdp_plan(const ipi_mdp* h, ipi_plan* out);
+
+/* validate (model.py:148-194, sparse.py:56-86) on device. */
+int ipi_validate(ipi_mdp* h, ipi_validation* out, void* stream);
+
+/* ---- K1: fused Bellman backup ---------------------------------------- */
+/* greedy_policy (bellman.py:44-68) + residual norm(v - applied, inf)
+ * (driver.py:136).  v_full: n_global values.  policy int32[n_local],
+ * applied f64[n_local]; g_pi / len_pi / res_inf_bits nullable.  res_inf_bits
+ * is an 8-byte device word receiving the max via integer atomicMax on the
+ * IEEE bits of |v-applied| (>= 0); the caller zeroes it. */
+int ipi_bellman(ipi_mdp* h, const double* v_full, int32_t mode, int32_t* policy, double* applied,
+                double* g_pi, int32_t* len_pi, unsigned long long* res_inf_bits, void* stream);
+
+/* ---- K2: policy compaction (sparse.py:243-269) ------------------------ */
+int ipi_policy_nnz(ipi_mdp* h, const int32_t* policy, int64_t* nnz_out, void* stream);
+int ipi_gather_policy(ipi_mdp* h, const int32_t* policy, int64_t* rp_pi, int32_t* col_pi,
+                      double* val_pi, double* g_pi, void* stream);
+
+/* ---- K3: SpMV family (sparse.py:189-215, 294-295) --------------------- */
+/* y = A x for a general CSR (rows x cols). */
+int ipi_spmv(const int64_t* row_ptr, const int32_t* col, const double* val, int64_t rows,
+             int64_t cols, const double* x, double* y, void* stream);
+/* PolicyOperator.apply: y = x - gamma*(P x); with b != NULL: y = b - (x - gamma*(P x)). */
+int ipi_apply_J(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi, int64_t n,
+                double gamma, const double* x, const double* b, double* y, void* stream);
+
+/* ---- K4: policy evaluation (inner.py:163-292) ------------------------- */
+/* Solve (I - gamma P_pi) x = b from x (in/out) to the floored 2-norm target
+ * or max_it iterations, one persistent cooperative kernel per call. */
+int ipi_inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi, int64_t n,
+                    double gamma, const double* b, double* x, double target_2norm,
+                    int32_t max_it, int32_t kind, double richardson_scale,
+                    ipi_inner_report* report, void* stream);
+
+/* ---- outer iPI loop (driver.py:109-209) ------------------------------- */
+/* v (device, n) holds V0 on entry and the final V on exit; policy (device,
+ * int32 n) the greedy policy of the final V; history (host) receives
+ * residual_history (capacity hist_cap >= max_outer + 1). */
+int ipi_solve(ipi_mdp* h, const ipi_opts* opts, double* v, int32_t* policy, double* history,
+              int32_t hist_cap, ipi_stats* stats, void* stream);
+
+/* ---- device generators for the BASELINE configs ----------------------- */
+/* C2/C5 locality random rows [row0, row0+rows) of an (n*m) x n instance. */
+int ipi_gen_locality(int64_t n, int32_t m, int32_t K, int64_t window, uint64_t seed,
+                     int64_t state0, int64_t n_states, int64_t* row_ptr, int32_t* col,
+                     double* val, double* cost, void* stream);
+/* C3 pendulum (N x N grid, n_actions torques) for states [state0, state0+n_states). */
+int ipi_gen_pendulum(int32_t N, int32_t n_actions, int64_t state0, int64_t n_states,
+                     int64_t* row_ptr, int32_t* col, double* val, double* cost, void* stream);
+/* C4 SIS convolution rows: two-pass.  Pass 1 (col == NULL): row lengths into
+ * row_ptr[1..] (caller scans).  Pass 2: fill col/val/cost. */
+int ipi_gen_sis(int32_t population, int32_t pass, int64_t* row_ptr, int32_t* col, double* val,
+                double* cost, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* IPI_B200_H */

@@ -1,0 +1,677 @@
+// capi.cu — extern "C" boundary (include/ipi_b200.h), planning, validation and
+// the native outer iPI loop (driver.py:109-209).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "handle.cuh"
+
+namespace ipi {
+
+static thread_local std::string g_err;
+
+void set_error(const std::string& msg) { g_err = msg; }
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int pick_lanes_per_row(double mean_len) {
+  // ~4+ elements per lane: 4 independent loads in flight per row
+  if (mean_len <= 6.0) return 1;
+  if (mean_len <= 12.0) return 2;
+  if (mean_len <= 24.0) return 4;
+  if (mean_len <= 56.0) return 8;
+  if (mean_len <= 112.0) return 16;
+  return 32;
+}
+
+int k1_set_smem(int lanes, int smem);  // bellman.cu
+
+// ---------------------------------------------------------------------------
+// planning kernels
+// ---------------------------------------------------------------------------
+__global__ void row_stats_kernel(const int64_t* rp, int64_t rows, unsigned long long* out) {
+  // out[0] = min len, out[1] = max len (atomicMin/Max on u64)
+  unsigned long long mn = ~0ull, mx = 0;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long l = (unsigned long long)(rp[r + 1] - rp[r]);
+    mn = l < mn ? l : mn;
+    mx = l > mx ? l : mx;
+  }
+  for (int off = 16; off; off >>= 1) {
+    unsigned long long a = __shfl_xor_sync(kFull, mn, off), b = __shfl_xor_sync(kFull, mx, off);
+    mn = a < mn ? a : mn;
+    mx = b > mx ? b : mx;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(out, mn);
+    atomicMax(out + 1, mx);
+  }
+}
+
+// log2 histogram of |col - state| (locality profile, 40 buckets)
+__global__ void locality_hist_kernel(const int64_t* rp, const int32_t* col, int64_t rows, int m,
+                                     int64_t state0, unsigned long long* hist) {
+  __shared__ unsigned long long sh[40];
+  for (int i = threadIdx.x; i < 40; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = wg; r < rows; r += nw) {
+    const int64_t s = state0 + r / m;
+    const int64_t p0 = rp[r], p1 = rp[r + 1];
+    for (int64_t p = p0 + lane; p < p1; p += 32) {
+      int64_t d = (int64_t)col[p] - s;
+      d = d < 0 ? -d : d;
+      const int b = d == 0 ? 0 : 64 - __clzll((unsigned long long)d);  // d in [2^(b-1), 2^b)
+      atomicAdd(&sh[b < 39 ? b : 39], 1ull);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 40; i += blockDim.x)
+    if (sh[i]) atomicAdd(&hist[i], sh[i]);
+}
+
+// nnz-balanced state boundaries: bounds[c] = first state s with rp[s*m] >= c*nnz/nb
+__global__ void bounds_kernel(const int64_t* rp, int64_t n, int m, int nb, int64_t* bounds) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c > nb) return;
+  if (c == 0) {
+    bounds[0] = 0;
+    return;
+  }
+  if (c == nb) {
+    bounds[nb] = n;
+    return;
+  }
+  const int64_t nnz = rp[n * (int64_t)m];
+  const int64_t key = (nnz * (int64_t)c) / nb;
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (rp[mid * (int64_t)m] < key) lo = mid + 1; else hi = mid;
+  }
+  bounds[c] = lo;
+}
+
+// ---------------------------------------------------------------------------
+// validation (model.py:148-194 + sparse.py:56-86)
+// ---------------------------------------------------------------------------
+struct VAcc {
+  unsigned long long bad_rp, bad_range, bad_order, nonfinite, first_bad_prob, n_bad_sum,
+      first_bad_sum_row, nonfinite_cost;
+};
+
+__global__ void validate_rowptr_kernel(const int64_t* rp, int64_t rows, VAcc* acc) {
+  unsigned long long bad = 0;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows;
+       r += (int64_t)gridDim.x * blockDim.x)
+    bad += rp[r + 1] < rp[r];
+  if (blockIdx.x == 0 && threadIdx.x == 0) bad += rp[0] != 0;
+  for (int off = 16; off; off >>= 1) bad += __shfl_xor_sync(kFull, bad, off);
+  if ((threadIdx.x & 31) == 0 && bad) atomicAdd(&acc->bad_rp, bad);
+}
+
+// warp per row: column range/order, finiteness, [0,1], row sums.
+// `after` restricts the bad-sum search to rows > after (used to list the first five).
+__global__ void validate_rows_kernel(const int64_t* rp, const int32_t* col, const double* val,
+                                     int64_t rows, int64_t ncols, long long after, VAcc* acc,
+                                     int structural_only) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long br = 0, bo = 0, nf = 0;
+  for (int64_t r = wg; r < rows; r += nw) {
+    const int64_t p0 = rp[r], p1 = rp[r + 1];
+    double sum = 0.0;
+    for (int64_t p = p0 + lane; p < p1; p += 32) {
+      const int c = col[p];
+      br += (c < 0 || (int64_t)c >= ncols);
+      if (p > p0) bo += col[p - 1] >= c;
+      const double v = val[p];
+      if (!isfinite(v)) nf += 1;
+      if (!structural_only && (v < 0.0 || v > 1.0))
+        atomicMin(&acc->first_bad_prob, (unsigned long long)p);
+      sum = add_rn(sum, v);
+    }
+    if (!structural_only && (long long)r > after) {
+      sum = warp_sum(sum);
+      if (lane == 0 && fabs(sum - 1.0) > 1e-12) {
+        atomicAdd(&acc->n_bad_sum, 1ull);
+        atomicMin(&acc->first_bad_sum_row, (unsigned long long)r);
+      }
+    }
+  }
+  for (int off = 16; off; off >>= 1) {
+    br += __shfl_xor_sync(kFull, br, off);
+    bo += __shfl_xor_sync(kFull, bo, off);
+    nf += __shfl_xor_sync(kFull, nf, off);
+  }
+  if (lane == 0) {
+    if (br) atomicAdd(&acc->bad_range, br);
+    if (bo) atomicAdd(&acc->bad_order, bo);
+    if (nf) atomicAdd(&acc->nonfinite, nf);
+  }
+}
+
+__global__ void row_sum_kernel(const int64_t* rp, const double* val, int64_t r, double* out) {
+  // same summation layout as validate_rows_kernel for one row
+  const int lane = threadIdx.x;
+  double sum = 0.0;
+  for (int64_t p = rp[r] + lane; p < rp[r + 1]; p += 32) sum = add_rn(sum, val[p]);
+  sum = warp_sum(sum);
+  if (lane == 0) *out = sum;
+}
+
+__global__ void cost_finite_kernel(const double* cost, int64_t len, VAcc* acc) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (!isfinite(cost[i])) atomicMin(&acc->nonfinite_cost, (unsigned long long)i);
+}
+
+static int grid_for(int64_t work, int threads, int sms) {
+  int64_t b = (work + threads - 1) / threads;
+  b = std::min<int64_t>(b, (int64_t)sms * 32);
+  return (int)std::max<int64_t>(b, 1);
+}
+
+static int ensure_scratch(ipi_mdp* h) {
+  if (h->pi) return IPI_OK;
+  const int64_t n = std::max<int64_t>(h->n_local, 1);
+  IPI_CUDA_TRY(cudaMalloc(&h->pi, sizeof(int32_t) * n));
+  IPI_CUDA_TRY(cudaMalloc(&h->applied, sizeof(double) * n));
+  IPI_CUDA_TRY(cudaMalloc(&h->gpi, sizeof(double) * n));
+  IPI_CUDA_TRY(cudaMalloc(&h->lenpi, sizeof(int32_t) * n));
+  IPI_CUDA_TRY(cudaMalloc(&h->res_bits, sizeof(unsigned long long) * 2));
+  IPI_CUDA_TRY(cudaMalloc(&h->xbuf, sizeof(double) * n));
+  IPI_CUDA_TRY(cudaMalloc(&h->d_report, sizeof(ipi_inner_report)));
+  const int64_t cap = std::max<int64_t>((int64_t)h->plan.row_len_max * h->n_local, 1);
+  IPI_CUDA_TRY(cudaMalloc(&h->rp_pi, sizeof(int64_t) * (n + 1)));
+  IPI_CUDA_TRY(cudaMalloc(&h->col_pi, sizeof(int32_t) * cap));
+  IPI_CUDA_TRY(cudaMalloc(&h->val_pi, sizeof(double) * cap));
+  h->cap_pi = cap;
+  return IPI_OK;
+}
+
+}  // namespace ipi
+
+using namespace ipi;
+
+extern "C" {
+
+const char* ipi_last_error(void) { return g_err.c_str(); }
+
+const char* ipi_version(void) { return "ipi_b200 0.1 (sm_100a, fp64 CSR, persistent GMRES)"; }
+
+int ipi_device_count(void) {
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) return 0;
+  return c;
+}
+
+int ipi_mdp_create(const int64_t* row_ptr, const int32_t* col, const double* values,
+                   const double* stage_cost, int64_t n_local, int64_t n_global, int32_t m,
+                   int64_t state0, double gamma, int32_t mode, void* stream, ipi_mdp** out) {
+  if (!out) return fail(IPI_EVALIDATION, "null output handle");
+  *out = nullptr;
+  if (m < 1) return fail(IPI_EVALIDATION, "action count must be >= 1, got " + std::to_string(m));
+  if (n_local < 0 || n_global < 1 || state0 < 0 || state0 + n_local > n_global)
+    return fail(IPI_EDIMENSION, "inconsistent shard geometry");
+  if (n_global > INT32_MAX) return fail(IPI_EDIMENSION, "state count exceeds int32 column range");
+  cudaStream_t st = (cudaStream_t)stream;
+  ipi_mdp* h = new ipi_mdp();
+  h->rp = row_ptr;
+  h->col = col;
+  h->val = values;
+  h->cost = stage_cost;
+  h->n_local = n_local;
+  h->n_global = n_global;
+  h->state0 = state0;
+  h->m = m;
+  h->gamma = gamma;
+  h->mode = mode;
+  cudaGetDevice(&h->device);
+  cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device);
+  auto bail = [&](int code) {
+    ipi_mdp_destroy(h);
+    return code;
+  };
+  if (cudaMallocHost(&h->host_pinned, 4096) != cudaSuccess)
+    return bail(fail(IPI_ECUDA, "cudaMallocHost failed"));
+  const int64_t rows = n_local * (int64_t)m;
+  // ---- row statistics + locality histogram --------------------------------
+  unsigned long long* d_tmp = nullptr;
+  if (cudaMalloc(&d_tmp, sizeof(unsigned long long) * 48) != cudaSuccess)
+    return bail(fail(IPI_ECUDA, "cudaMalloc failed"));
+  unsigned long long init[48];
+  std::memset(init, 0, sizeof(init));
+  init[0] = ~0ull;
+  cudaMemcpyAsync(d_tmp, init, sizeof(init), cudaMemcpyHostToDevice, st);
+  int64_t nnz = 0;
+  if (rows > 0) {
+    row_stats_kernel<<<grid_for(rows, 256, h->num_sms), 256, 0, st>>>(row_ptr, rows, d_tmp);
+    locality_hist_kernel<<<h->num_sms * 8, 256, 0, st>>>(row_ptr, col, rows, m, state0, d_tmp + 8);
+  }
+  unsigned long long hst[48];
+  cudaMemcpyAsync(hst, d_tmp, sizeof(hst), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(&nnz, row_ptr + rows, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  cudaFree(d_tmp);
+  if (e != cudaSuccess) return bail(fail(IPI_ECUDA, std::string("planning: ") + cudaGetErrorString(e)));
+  ipi_plan& p = h->plan;
+  p.nnz = nnz;
+  p.row_len_min = rows > 0 ? (int32_t)hst[0] : 0;
+  p.row_len_max = rows > 0 ? (int32_t)hst[1] : 0;
+  p.row_len_mean = rows > 0 ? (double)nnz / (double)rows : 0.0;
+  p.uniform_rows = rows > 0 && p.row_len_min == p.row_len_max;
+  p.lanes_per_row = pick_lanes_per_row(p.row_len_mean);
+  p.k1_threads = kK1Threads;
+  p.inner_threads = kInnerThreads;
+  // ---- shared-memory V window (halo) choice ---------------------------------
+  // coverage(k) = fraction of nnz with |col - s| < 2^k.  Pick the largest k
+  // whose window (own slice + 2*2^k, clipped to n_global) fits 100 KB (two
+  // 512-thread CTAs per SM); use it only if it covers >= 50% of the gathers,
+  // then shrink to the smallest k within 1% of that coverage.
+  const int ctas_win = 2;
+  const int nb_win = h->num_sms * ctas_win;
+  const int64_t own = (n_local + nb_win - 1) / std::max(nb_win, 1);
+  const int64_t cap_doubles = 100 * 1024 / 8;
+  double cum[41];
+  cum[0] = 0.0;
+  for (int b = 0; b < 40; ++b) cum[b + 1] = cum[b] + (double)hst[8 + b];
+  auto coverage = [&](int k) {  // d < 2^k  <=> bucket <= k
+    const int b = std::min(k, 39);
+    return nnz > 0 ? cum[b + 1] / (double)nnz : 1.0;
+  };
+  int kfit = -1;
+  for (int k = 0; k <= 31; ++k) {
+    const int64_t halo = 1ll << k;
+    const int64_t wlen = std::min<int64_t>(n_global, own + 2 * halo);
+    if (wlen <= cap_doubles) kfit = k;
+  }
+  p.halo = -1;
+  if (kfit >= 0 && rows > 0) {
+    const double best = coverage(kfit);
+    if (best >= 0.5) {
+      int k = kfit;
+      while (k > 0 && coverage(k - 1) >= best - 0.01) --k;
+      p.halo = (int32_t)std::min<int64_t>(1ll << k, n_global);
+    }
+  }
+  // ---- K1 grid -------------------------------------------------------------
+  int k1_blocks;
+  if (p.halo >= 0) {
+    k1_blocks = nb_win;
+    const int64_t wlen = std::min<int64_t>(n_global, own + 2 * (int64_t)p.halo);
+    p.k1_smem_bytes = (int32_t)(wlen * 8 + 1024);
+    int rc = k1_set_smem(p.lanes_per_row, p.k1_smem_bytes);
+    if (rc) return bail(rc);
+  } else {
+    k1_blocks = h->num_sms * 4;
+    p.k1_smem_bytes = 0;
+  }
+  // enough states per CTA: at least one per warp
+  const int64_t max_blocks = std::max<int64_t>(1, (n_local + 15) / 16);
+  k1_blocks = (int)std::min<int64_t>(k1_blocks, max_blocks);
+  p.k1_blocks = k1_blocks;
+  if (cudaMalloc(&h->k1_bounds, sizeof(int64_t) * (k1_blocks + 1)) != cudaSuccess)
+    return bail(fail(IPI_ECUDA, "cudaMalloc bounds"));
+  bounds_kernel<<<(k1_blocks + 1 + 127) / 128, 128, 0, st>>>(row_ptr, n_local, m, k1_blocks,
+                                                            h->k1_bounds);
+  if (p.halo >= 0) {
+    // every K1 window must fit: check the realised nnz-balanced bounds
+    std::vector<int64_t> hb(k1_blocks + 1);
+    cudaMemcpyAsync(hb.data(), h->k1_bounds, sizeof(int64_t) * (k1_blocks + 1),
+                    cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) return bail(fail(IPI_ECUDA, "bounds sync"));
+    int64_t worst = 0;
+    for (int c = 0; c < k1_blocks; ++c) worst = std::max<int64_t>(worst, hb[c + 1] - hb[c]);
+    const int64_t wlen = std::min<int64_t>(n_global, worst + 2 * (int64_t)p.halo);
+    if (wlen * 8 + 1024 > 200 * 1024) {
+      p.halo = -1;  // unbalanced slices: plain L1 gathers
+      p.k1_smem_bytes = 0;
+    } else if (wlen * 8 + 1024 > p.k1_smem_bytes) {
+      p.k1_smem_bytes = (int32_t)(wlen * 8 + 1024);
+      int rc = k1_set_smem(p.lanes_per_row, p.k1_smem_bytes);
+      if (rc) return bail(rc);
+    }
+  }
+  p.inner_blocks = 0;
+  p.inner_smem_bytes = 0;
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return bail(fail(IPI_ECUDA, std::string("planning kernels: ") + cudaGetErrorString(e)));
+  *out = h;
+  return IPI_OK;
+}
+
+void ipi_mdp_destroy(ipi_mdp* h) {
+  if (!h) return;
+  cudaFree(h->k1_bounds);
+  cudaFree(h->pi);
+  cudaFree(h->applied);
+  cudaFree(h->gpi);
+  cudaFree(h->lenpi);
+  cudaFree(h->res_bits);
+  cudaFree(h->rp_pi);
+  cudaFree(h->col_pi);
+  cudaFree(h->val_pi);
+  cudaFree(h->xbuf);
+  cudaFree(h->scan_tmp);
+  cudaFree(h->d_report);
+  if (h->host_pinned) cudaFreeHost(h->host_pinned);
+  delete h;
+}
+
+int ipi_mdp_plan(const ipi_mdp* h, ipi_plan* out) {
+  if (!h || !out) return fail(IPI_EVALIDATION, "null handle");
+  *out = h->plan;
+  return IPI_OK;
+}
+
+static int csr_check_impl(const int64_t* rp, const int32_t* col, const double* val, int64_t rows,
+                          int64_t cols, int64_t nnz_len, ipi_csr_report* out, bool probs,
+                          const double* cost, int64_t cost_len, VAcc* res, cudaStream_t st) {
+  std::memset(out, 0, sizeof(*out));
+  VAcc init;
+  std::memset(&init, 0, sizeof(init));
+  init.first_bad_prob = ~0ull;
+  init.first_bad_sum_row = ~0ull;
+  init.nonfinite_cost = ~0ull;
+  VAcc* d = nullptr;
+  IPI_CUDA_TRY(cudaMalloc(&d, sizeof(VAcc)));
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaMemcpyAsync(d, &init, sizeof(VAcc), cudaMemcpyHostToDevice, st);
+  if (rows > 0) validate_rowptr_kernel<<<grid_for(rows, 256, sms), 256, 0, st>>>(rp, rows, d);
+  if (cost && cost_len > 0) cost_finite_kernel<<<grid_for(cost_len, 256, sms), 256, 0, st>>>(cost, cost_len, d);
+  int64_t last = 0;
+  cudaMemcpyAsync(&last, rp + rows, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(res, d, sizeof(VAcc), cudaMemcpyDeviceToHost, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    cudaFree(d);
+    return fail(IPI_ECUDA, std::string("csr check: ") + cudaGetErrorString(e));
+  }
+  out->bad_row_ptr = (int64_t)res->bad_rp;
+  out->nnz = last;
+  out->nnz_mismatch = (last != nnz_len);
+  if (out->bad_row_ptr == 0 && !out->nnz_mismatch && rows > 0 && last > 0) {
+    validate_rows_kernel<<<grid_for(rows * 32, 256, sms), 256, 0, st>>>(rp, col, val, rows, cols,
+                                                                          probs ? -1 : (long long)rows, d, probs ? 0 : 1);
+    cudaMemcpyAsync(res, d, sizeof(VAcc), cudaMemcpyDeviceToHost, st);
+    e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+      cudaFree(d);
+      return fail(IPI_ECUDA, std::string("csr check: ") + cudaGetErrorString(e));
+    }
+    out->bad_col_range = (int64_t)res->bad_range;
+    out->bad_col_order = (int64_t)res->bad_order;
+    out->nonfinite_values = (int64_t)res->nonfinite;
+  }
+  cudaFree(d);
+  return IPI_OK;
+}
+
+int ipi_csr_check(const int64_t* row_ptr, const int32_t* col, const double* val, int64_t rows,
+                  int64_t cols, int64_t nnz_len, ipi_csr_report* out, void* stream) {
+  if (!out) return fail(IPI_EVALIDATION, "null report");
+  VAcc res;
+  return csr_check_impl(row_ptr, col, val, rows, cols, nnz_len, out, false, nullptr, 0, &res,
+                        (cudaStream_t)stream);
+}
+
+int ipi_validate(ipi_mdp* h, ipi_validation* out, void* stream) {
+  if (!h || !out) return fail(IPI_EVALIDATION, "null handle");
+  cudaStream_t st = (cudaStream_t)stream;
+  std::memset(out, 0, sizeof(*out));
+  out->first_bad_prob = -1;
+  out->nonfinite_cost = -1;
+  for (int i = 0; i < 5; ++i) out->bad_rows[i] = -1;
+  const int64_t rows = h->n_local * (int64_t)h->m;
+  ipi_csr_report cr;
+  VAcc r;
+  int rc = csr_check_impl(h->rp, h->col, h->val, rows, h->n_global, h->plan.nnz, &cr, true,
+                          h->cost, rows, &r, st);
+  if (rc) return rc;
+  out->bad_row_ptr = cr.bad_row_ptr + (cr.nnz_mismatch ? 1 : 0);
+  out->bad_col_range = cr.bad_col_range;
+  out->bad_col_order = cr.bad_col_order;
+  out->nonfinite_values = cr.nonfinite_values;
+  out->nonfinite_cost = r.nonfinite_cost == ~0ull ? -1 : (int64_t)r.nonfinite_cost;
+  if (out->bad_row_ptr) return IPI_OK;
+  out->first_bad_prob = r.first_bad_prob == ~0ull ? -1 : (int64_t)r.first_bad_prob;
+  if (r.first_bad_prob != ~0ull) {
+    IPI_CUDA_TRY(cudaMemcpy(&out->first_bad_prob_value, h->val + r.first_bad_prob, sizeof(double),
+                            cudaMemcpyDeviceToHost));
+  }
+  out->n_bad_row_sums = (int64_t)r.n_bad_sum;
+  if (r.n_bad_sum > 0) {
+    VAcc* d = nullptr;
+    double* dsum = nullptr;
+    IPI_CUDA_TRY(cudaMalloc(&d, sizeof(VAcc)));
+    IPI_CUDA_TRY(cudaMalloc(&dsum, sizeof(double)));
+    VAcc init;
+    std::memset(&init, 0, sizeof(init));
+    init.first_bad_prob = ~0ull;
+    init.first_bad_sum_row = ~0ull;
+    init.nonfinite_cost = ~0ull;
+    unsigned long long row = r.first_bad_sum_row;
+    for (int k = 0; k < 5 && row != ~0ull; ++k) {
+      out->bad_rows[k] = (int64_t)row;
+      row_sum_kernel<<<1, 32, 0, st>>>(h->rp, h->val, (int64_t)row, dsum);
+      cudaMemcpyAsync(&out->bad_row_sums[k], dsum, sizeof(double), cudaMemcpyDeviceToHost, st);
+      if (k == 4) break;
+      cudaMemcpyAsync(d, &init, sizeof(VAcc), cudaMemcpyHostToDevice, st);
+      validate_rows_kernel<<<grid_for(rows * 32, 256, h->num_sms), 256, 0, st>>>(
+          h->rp, h->col, h->val, rows, h->n_global, (long long)row, d, 0);
+      VAcc r2;
+      cudaMemcpyAsync(&r2, d, sizeof(VAcc), cudaMemcpyDeviceToHost, st);
+      if (cudaStreamSynchronize(st) != cudaSuccess) break;
+      row = r2.first_bad_sum_row;
+    }
+    cudaStreamSynchronize(st);
+    cudaFree(d);
+    cudaFree(dsum);
+  }
+  IPI_CUDA_TRY(cudaGetLastError());
+  return IPI_OK;
+}
+
+int ipi_bellman(ipi_mdp* h, const double* v_full, int32_t mode, int32_t* policy, double* applied,
+                double* g_pi, int32_t* len_pi, unsigned long long* res_inf_bits, void* stream) {
+  if (!h) return fail(IPI_EVALIDATION, "null handle");
+  return launch_bellman(h, v_full, mode, policy, applied, g_pi, len_pi, res_inf_bits,
+                        (cudaStream_t)stream);
+}
+
+int ipi_policy_nnz(ipi_mdp* h, const int32_t* policy, int64_t* nnz_out, void* stream) {
+  if (!h || !nnz_out) return fail(IPI_EVALIDATION, "null argument");
+  return policy_nnz(h, policy, nnz_out, (cudaStream_t)stream);
+}
+
+int ipi_gather_policy(ipi_mdp* h, const int32_t* policy, int64_t* rp_pi, int32_t* col_pi,
+                      double* val_pi, double* g_pi, void* stream) {
+  if (!h) return fail(IPI_EVALIDATION, "null handle");
+  return gather_policy(h, policy, nullptr, rp_pi, col_pi, val_pi, g_pi, nullptr,
+                       (cudaStream_t)stream);
+}
+
+int ipi_spmv(const int64_t* row_ptr, const int32_t* col, const double* val, int64_t rows,
+             int64_t cols, const double* x, double* y, void* stream) {
+  (void)cols;
+  if (rows < 0) return fail(IPI_EDIMENSION, "negative row count");
+  if (rows == 0) return IPI_OK;
+  int64_t nnz = 0;
+  IPI_CUDA_TRY(cudaMemcpyAsync(&nnz, row_ptr + rows, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                               (cudaStream_t)stream));
+  IPI_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+  return launch_spmv(row_ptr, col, val, rows, x, nullptr, 0.0, 0, y,
+                     pick_lanes_per_row((double)nnz / (double)rows), (cudaStream_t)stream);
+}
+
+int ipi_apply_J(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi, int64_t n,
+                double gamma, const double* x, const double* b, double* y, void* stream) {
+  if (n <= 0) return IPI_OK;
+  int64_t nnz = 0;
+  IPI_CUDA_TRY(cudaMemcpyAsync(&nnz, rp_pi + n, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                               (cudaStream_t)stream));
+  IPI_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+  return launch_spmv(rp_pi, col_pi, val_pi, n, x, b, gamma, b ? 2 : 1, y,
+                     pick_lanes_per_row((double)nnz / (double)n), (cudaStream_t)stream);
+}
+
+int ipi_inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi, int64_t n,
+                    double gamma, const double* b, double* x, double target_2norm,
+                    int32_t max_it, int32_t kind, double richardson_scale,
+                    ipi_inner_report* report, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n <= 0) return fail(IPI_EDIMENSION, "empty system");
+  int64_t nnz = 0;
+  IPI_CUDA_TRY(cudaMemcpyAsync(&nnz, rp_pi + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  IPI_CUDA_TRY(cudaStreamSynchronize(st));
+  ipi_inner_report* d_rep = nullptr;
+  IPI_CUDA_TRY(cudaMalloc(&d_rep, sizeof(ipi_inner_report)));
+  int rc = inner_solve(rp_pi, col_pi, val_pi, n, gamma, b, x, target_2norm, max_it, kind,
+                       richardson_scale, pick_lanes_per_row((double)nnz / (double)n), -1, d_rep, st);
+  if (rc == IPI_OK && report) {
+    cudaError_t e = cudaMemcpyAsync(report, d_rep, sizeof(*report), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = fail(IPI_ECUDA, std::string("inner solve: ") + cudaGetErrorString(e));
+  }
+  cudaFree(d_rep);
+  return rc;
+}
+
+// driver.py:109-209 — the outer loop, natively.  One host sync per outer
+// iteration (the residual scalar that drives the stopping tests).
+int ipi_solve(ipi_mdp* h, const ipi_opts* o, double* v, int32_t* policy, double* history,
+              int32_t hist_cap, ipi_stats* stats, void* stream) {
+  if (!h || !o || !v || !stats) return fail(IPI_EVALIDATION, "null argument");
+  if (h->state0 != 0 || h->n_local != h->n_global)
+    return fail(IPI_EVALIDATION, "ipi_solve drives a whole instance; sharded runs use the rank driver");
+  if (!(o->tol > 0.0)) return fail(IPI_EVALIDATION, "tolerance must be > 0");
+  if (!(o->alpha > 0.0 && o->alpha < 1.0)) return fail(IPI_EVALIDATION, "alpha must lie in (0, 1)");
+  if (o->max_outer < 1 || o->max_inner < 1) return fail(IPI_EVALIDATION, "iteration caps must be >= 1");
+  if (hist_cap < 1) return fail(IPI_EVALIDATION, "history capacity must be >= 1");
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = ensure_scratch(h);
+  if (rc) return rc;
+  const int64_t n = h->n_local;
+  const auto t_start = std::chrono::steady_clock::now();
+  std::vector<cudaEvent_t> ev;
+  auto new_event = [&]() {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    ev.push_back(e);
+    return e;
+  };
+  struct Phase {
+    cudaEvent_t a, b;
+    int kind;  // 0 greedy, 1 assembly, 2 inner
+  };
+  std::vector<Phase> phases;
+  double* host = reinterpret_cast<double*>(h->host_pinned);
+  ipi_inner_report* hrep = reinterpret_cast<ipi_inner_report*>(host + 8);
+  std::vector<double> hist;
+  int64_t inner_total = 0;
+  int stall = 0;
+  int k = 0;
+  int status = IPI_CONVERGED;
+  double* vcur = v;
+  double* vnext = h->xbuf;
+  bool pending_report = false;
+  while (true) {
+    Phase pg{new_event(), new_event(), 0};
+    cudaEventRecord(pg.a, st);
+    IPI_CUDA_TRY(cudaMemsetAsync(h->res_bits, 0, sizeof(unsigned long long), st));
+    rc = launch_bellman(h, vcur, o->mode, h->pi, h->applied, h->gpi, nullptr, h->res_bits, st);
+    if (rc) return rc;
+    cudaEventRecord(pg.b, st);
+    phases.push_back(pg);
+    IPI_CUDA_TRY(cudaMemcpyAsync(host, h->res_bits, sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (pending_report)
+      IPI_CUDA_TRY(cudaMemcpyAsync(hrep, h->d_report, sizeof(ipi_inner_report), cudaMemcpyDeviceToHost, st));
+    IPI_CUDA_TRY(cudaStreamSynchronize(st));
+    if (pending_report) {
+      inner_total += hrep->iterations;
+      pending_report = false;
+    }
+    const double res = host[0];
+    hist.push_back(res);
+    if (res <= o->tol) {
+      status = IPI_CONVERGED;
+      break;
+    }
+    if (k >= o->max_outer) {
+      status = IPI_OUTER_CAP;
+      break;
+    }
+    if (k > 0 && res >= hist[k - 1]) {
+      if (++stall >= 50) {  // driver.py:38,146-153
+        status = IPI_STALLED;
+        break;
+      }
+    } else {
+      stall = 0;
+    }
+    Phase pa{new_event(), new_event(), 1};
+    cudaEventRecord(pa.a, st);
+    rc = gather_policy(h, h->pi, nullptr, h->rp_pi, h->col_pi, h->val_pi, nullptr, nullptr, st);
+    if (rc) return rc;
+    cudaEventRecord(pa.b, st);
+    phases.push_back(pa);
+    double target;
+    int cap;
+    if (o->ksp_max_it > 0) {
+      target = 0.0;
+      cap = o->ksp_max_it;
+    } else {
+      target = o->alpha * res;
+      cap = o->max_inner;
+    }
+    Phase pi_{new_event(), new_event(), 2};
+    cudaEventRecord(pi_.a, st);
+    IPI_CUDA_TRY(cudaMemcpyAsync(vnext, vcur, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    rc = inner_solve(h->rp_pi, h->col_pi, h->val_pi, n, h->gamma, h->gpi, vnext, target, cap,
+                     o->ksp_type, o->richardson_scale, h->plan.lanes_per_row, h->plan.halo,
+                     h->d_report, st);
+    if (rc) return rc;
+    cudaEventRecord(pi_.b, st);
+    phases.push_back(pi_);
+    pending_report = true;
+    std::swap(vcur, vnext);
+    ++k;
+  }
+  if (vcur != v) IPI_CUDA_TRY(cudaMemcpyAsync(v, vcur, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  if (policy) IPI_CUDA_TRY(cudaMemcpyAsync(policy, h->pi, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, st));
+  IPI_CUDA_TRY(cudaStreamSynchronize(st));
+  const auto t_end = std::chrono::steady_clock::now();
+  double tg = 0, ta = 0, ti = 0;
+  for (auto& ph : phases) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ph.a, ph.b);
+    (ph.kind == 0 ? tg : ph.kind == 1 ? ta : ti) += ms * 1e-3;
+  }
+  for (auto e : ev) cudaEventDestroy(e);
+  const int nh = std::min<int>((int)hist.size(), hist_cap);
+  if (history) std::memcpy(history, hist.data(), sizeof(double) * nh);
+  stats->status = status;
+  stats->outer_iterations = k;
+  stats->inner_iterations_total = inner_total;
+  stats->wall_time = std::chrono::duration<double>(t_end - t_start).count();
+  stats->time_greedy = tg;
+  stats->time_assembly = ta;
+  stats->time_inner = ti;
+  return IPI_OK;
+}
+
+}  // extern "C"

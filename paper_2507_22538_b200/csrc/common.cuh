@@ -1,0 +1,127 @@
+// common.cuh — shared device helpers for the sm_100a iPI kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <string>
+
+#include "../../include/ipi_b200.h"
+
+namespace ipi {
+
+constexpr int kWarp = 32;
+constexpr unsigned kFull = 0xffffffffu;
+
+// ---------------------------------------------------------------------------
+// error plumbing (thread-local message, returned codes)
+// ---------------------------------------------------------------------------
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+
+#define IPI_CUDA_TRY(expr)                                                        \
+  do {                                                                            \
+    cudaError_t _e = (expr);                                                      \
+    if (_e != cudaSuccess) {                                                      \
+      return ::ipi::fail(IPI_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+    }                                                                             \
+  } while (0)
+
+#define IPI_LAUNCH_CHECK()                                                        \
+  do {                                                                            \
+    cudaError_t _e = cudaGetLastError();                                          \
+    if (_e != cudaSuccess) {                                                      \
+      return ::ipi::fail(IPI_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(_e)); \
+    }                                                                             \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// loads.  CSR streams are read once per pass: bypass L1 (keep it for the
+// gathered V) and mark them evict-first in L2 so V stays L2-resident.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+__device__ __forceinline__ double ld_stream(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+               : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int ld_stream(const int* p, uint64_t pol) {
+  int v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;"
+               : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ long long ld_stream(const long long* p, uint64_t pol) {
+  long long v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s64 %0, [%1], %2;"
+               : "=l"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int64_t ld_stream_i64(const int64_t* p, uint64_t pol) {
+  return (int64_t)ld_stream(reinterpret_cast<const long long*>(p), pol);
+}
+
+// Exact two-step rounding as numpy does it (no FMA contraction):
+// prod = a*b rounded, then sum rounded.
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+
+// ---------------------------------------------------------------------------
+// warp / group reductions (fixed xor trees -> deterministic)
+// ---------------------------------------------------------------------------
+template <int G>
+__device__ __forceinline__ double group_sum(double v) {
+#pragma unroll
+  for (int off = G / 2; off > 0; off >>= 1) v = add_rn(v, __shfl_xor_sync(kFull, v, off));
+  return v;
+}
+
+__device__ __forceinline__ double warp_sum(double v) { return group_sum<32>(v); }
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v = fmax(v, __shfl_xor_sync(kFull, v, off));
+  return v;
+}
+
+// Argmin/argmax merge with first-index tie break (bellman.py:59-60):
+// prefer strictly better q, on equal q the smaller action.
+__device__ __forceinline__ bool better(double q, int a, double bq, int ba, bool maximize) {
+  if (maximize) return q > bq || (q == bq && a < ba);
+  return q < bq || (q == bq && a < ba);
+}
+
+// Block reduction of one double per thread: warp trees then warp 0 sums the
+// per-warp values in warp order.  Result valid in thread 0 only.
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0) {
+    const int nw = blockDim.x >> 5;
+    for (int w = 0; w < nw; ++w) t = add_rn(t, red[w]);
+  }
+  return t;
+}
+
+__device__ __forceinline__ int64_t lower_bound_i64(const int64_t* a, int64_t n, int64_t key) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (a[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+}  // namespace ipi

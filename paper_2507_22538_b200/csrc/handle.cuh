@@ -1,0 +1,72 @@
+// handle.cuh — the ipi_mdp handle and cross-file launcher declarations.
+#pragma once
+
+#include "common.cuh"
+
+struct ipi_mdp {
+  // borrowed instance arrays (device)
+  const int64_t* rp = nullptr;
+  const int32_t* col = nullptr;
+  const double* val = nullptr;
+  const double* cost = nullptr;
+  int64_t n_local = 0, n_global = 0, state0 = 0;
+  int32_t m = 0;
+  double gamma = 0.0;
+  int32_t mode = IPI_MODE_MIN;
+
+  ipi_plan plan{};
+  int num_sms = 0;
+  int device = 0;
+  int64_t* k1_bounds = nullptr;  // k1_blocks + 1 local state boundaries (device)
+
+  // owned scratch (device), allocated on first use
+  int32_t* pi = nullptr;
+  double* applied = nullptr;
+  double* gpi = nullptr;
+  int32_t* lenpi = nullptr;
+  unsigned long long* res_bits = nullptr;
+  int64_t* rp_pi = nullptr;
+  int32_t* col_pi = nullptr;
+  double* val_pi = nullptr;
+  int64_t cap_pi = 0;
+  double* xbuf = nullptr;
+  int64_t* scan_tmp = nullptr;
+  int64_t scan_tmp_len = 0;
+  ipi_inner_report* d_report = nullptr;
+  void* host_pinned = nullptr;  // small pinned staging area
+};
+
+namespace ipi {
+
+constexpr int kK1Threads = 512;
+constexpr int kInnerThreads = 512;
+constexpr int kGmresRestart = 30;  // inner.py:40
+
+int pick_lanes_per_row(double mean_len);
+
+// bellman.cu
+int launch_bellman(ipi_mdp* h, const double* v_full, int32_t mode, int32_t* policy,
+                   double* applied, double* g_pi, int32_t* len_pi,
+                   unsigned long long* res_bits, cudaStream_t st);
+
+// policy.cu
+int gather_policy(ipi_mdp* h, const int32_t* policy, const int32_t* len_pi, int64_t* rp_pi,
+                  int32_t* col_pi, double* val_pi, double* g_pi, int64_t* nnz_out,
+                  cudaStream_t st);
+int policy_nnz(ipi_mdp* h, const int32_t* policy, int64_t* nnz_out, cudaStream_t st);
+
+// spmv.cu
+int launch_spmv(const int64_t* rp, const int32_t* col, const double* val, int64_t rows,
+                const double* x, const double* b, double gamma, int epi, double* y,
+                int lanes, cudaStream_t st);
+
+// krylov.cu
+int inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi, int64_t n,
+                double gamma, const double* b, double* x, double target, int32_t max_it,
+                int32_t kind, double scale, int lanes, int halo, ipi_inner_report* d_report,
+                cudaStream_t st);
+
+// device scratch arena for the inner solver (per device, grown on demand)
+double* krylov_workspace(int64_t n, int64_t doubles_needed);
+
+}  // namespace ipi

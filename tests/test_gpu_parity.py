@@ -1,0 +1,183 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden
+vectors and the oracle on identical inputs.
+
+Tolerances (north star): final V within 1e-8 relative; Bellman residual <=
+atol; greedy policy bit-identical except where the oracle's best/second-best
+Q gap < 1e-10.  Integer/index work (policy gather) is asserted bit-exact.
+Floating-point kernels differ from numpy only by summation order, so SpMV /
+greedy values are asserted to 1e-13 relative.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import golden_meta, golden_names, load_golden
+from oracle import mdp_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2507_22538_b200 as ipi  # noqa: E402
+
+NAMES = golden_names()
+V_RTOL = 1e-8
+TIE_GAP = 1e-10
+
+
+def instance(g, mode=None):
+    n, m = g["cost"].shape
+    csr = ipi.CsrMatrix(n * m, n, g["row_ptr"], g["col"], g["val"])
+    if mode is None:
+        mode = ipi.Mode.MAX if bool(g["maximize"]) else ipi.Mode.MIN
+    return ipi.MdpInstance(n=n, m=m, gamma=float(g["gamma"]), stage_cost=g["cost"],
+                           transitions=csr, mode=mode)
+
+
+def assert_policy_parity(pi_gpu, pi_ref, gap):
+    diff = np.flatnonzero(np.asarray(pi_gpu) != np.asarray(pi_ref))
+    assert np.all(gap[diff] < TIE_GAP), f"policy differs at non-tied states {diff[:10]}"
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_spmv_matches_reference(name):
+    g = load_golden(name)
+    mdp = instance(g)
+    y = ipi.spmv(mdp.transitions, g["spmv_x"])
+    scale = np.abs(g["val"]).max() * np.abs(g["spmv_x"]).max() * 64
+    np.testing.assert_allclose(y, g["spmv_y"], rtol=1e-13, atol=1e-15 * scale)
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_greedy_matches_reference(name):
+    g = load_golden(name)
+    mdp = instance(g)
+    res = ipi.greedy_policy(mdp, g["greedy_v"])
+    assert res.policy.dtype == np.int64
+    gap = orc.q_gap(g["row_ptr"], g["col"], g["val"], g["cost"], float(g["gamma"]),
+                    g["greedy_v"], bool(g["maximize"]))
+    assert_policy_parity(res.policy, g["greedy_policy"], gap)
+    scale = max(1.0, np.abs(g["greedy_applied"]).max())
+    np.testing.assert_allclose(res.applied, g["greedy_applied"], rtol=1e-13, atol=1e-14 * scale)
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_gather_and_apply_match_reference(name):
+    g = load_golden(name)
+    mdp = instance(g)
+    p_pi = ipi.gather_policy_matrix(mdp, g["greedy_policy"])
+    rp, col, val = p_pi.numpy()
+    np.testing.assert_array_equal(rp, g["gather_row_ptr"])       # bit-exact
+    np.testing.assert_array_equal(col, g["gather_col"])
+    np.testing.assert_array_equal(val, g["gather_val"])
+    np.testing.assert_array_equal(ipi.gather_policy_cost(mdp, g["greedy_policy"]), g["gather_cost"])
+    op = ipi.PolicyOperator(p_pi, float(g["gamma"]))
+    y = op.apply(g["spmv_x"])
+    np.testing.assert_allclose(y, g["apply_y"], rtol=1e-13, atol=1e-14 * np.abs(g["spmv_x"]).max())
+
+
+@pytest.mark.parametrize("name", NAMES)
+@pytest.mark.parametrize("kind", ["gmres", "richardson"])
+def test_inner_solve_matches_reference(name, kind):
+    g = load_golden(name)
+    meta = golden_meta(name)[f"inner_{kind}"]
+    mdp = instance(g)
+    p_pi = ipi.gather_policy_matrix(mdp, g["greedy_policy"])
+    op = ipi.PolicyOperator(p_pi, float(g["gamma"]))
+    theta, rep = ipi.inner_solve(op, g["gather_cost"], g["greedy_v"],
+                                 float(g[f"inner_{kind}_target"]), 200,
+                                 kind=ipi.InnerSolver.from_name(kind))
+    assert rep.target_2norm == pytest.approx(meta["eff"], rel=1e-12)
+    assert rep.converged == meta["converged"]
+    if meta["converged"]:
+        assert rep.final_linear_residual_2norm <= rep.target_2norm
+        # both iterates satisfy ||b - A x||_2 <= eff  =>  |x - x'| <= 2 eff / (1 - gamma)
+        bound = 2.0 * meta["eff"] / (1.0 - float(g["gamma"])) * 1.0001 + 1e-12
+        assert np.max(np.abs(theta - g[f"inner_{kind}_theta"])) <= bound
+        assert abs(rep.iterations - meta["iterations"]) <= max(3, 0.15 * meta["iterations"])
+    else:
+        assert rep.iterations == meta["iterations"]
+        np.testing.assert_allclose(theta, g[f"inner_{kind}_theta"], rtol=1e-6,
+                                   atol=1e-6 * np.abs(g[f"inner_{kind}_theta"]).max())
+
+
+def _solve_cases():
+    out = []
+    for name in NAMES:
+        for kind, s in golden_meta(name)["solves"].items():
+            if kind not in ("gmres", "richardson") or s["inner"] > 50_000:
+                continue
+            out.append(pytest.param(name, kind, id=f"{name}-{kind}"))
+    return out
+
+
+@pytest.mark.parametrize("name,kind", _solve_cases())
+def test_solve_matches_reference(name, kind):
+    g = load_golden(name)
+    s = golden_meta(name)["solves"][kind]
+    mdp = instance(g)
+    res = ipi.solve(mdp, ipi.SolveOptions(inner=ipi.InnerSolver.from_name(kind), tol=s["tol"]))
+    ref_v = g[f"solve_{kind}_values"]
+    assert res.status.value == s["status"]
+    assert res.outer_iterations == s["outer"]
+    assert len(res.residual_history) == len(g[f"solve_{kind}_history"])
+    scale = max(1.0, np.abs(ref_v).max())
+    np.testing.assert_allclose(res.values, ref_v, rtol=V_RTOL, atol=V_RTOL * scale)
+    gap = orc.q_gap(g["row_ptr"], g["col"], g["val"], g["cost"], float(g["gamma"]), ref_v,
+                    bool(g["maximize"]))
+    assert_policy_parity(res.policy, g[f"solve_{kind}_policy"], gap)
+    hist, ref_h = np.asarray(res.residual_history), g[f"solve_{kind}_history"]
+    # Intermediate iterates are only pinned to the inner tolerance (alpha = 1e-4 forcing):
+    # rounding-order differences move them within it, so history entries far above the
+    # noise floor agree to alpha-level relative error (C1/C4 show <= 4e-9 in practice);
+    # the tail only needs <= tol.  Final V is asserted at 1e-8 above.
+    big = ref_h > 1e-10
+    np.testing.assert_allclose(hist[big], ref_h[big], rtol=1e-4, atol=1e-13 * scale)
+    assert hist[-1] <= s["tol"]
+    # independent certificate: recompute the Bellman residual of the returned V
+    _, applied = orc.greedy(g["row_ptr"], g["col"], g["val"], g["cost"], float(g["gamma"]),
+                            res.values, bool(g["maximize"]))
+    assert np.max(np.abs(res.values - applied)) <= s["tol"] * 1.0001
+
+
+def test_solve_bitwise_rerun():
+    g = load_golden("cfg2_locality_n256")
+    mdp = instance(g)
+    a = ipi.solve(mdp)
+    b = ipi.solve(mdp)
+    np.testing.assert_array_equal(a.values, b.values)
+    np.testing.assert_array_equal(a.policy, b.policy)
+    assert a.residual_history == b.residual_history
+    assert a.inner_iterations_total == b.inner_iterations_total
+
+
+def test_toy_fixed_point_and_warm_start():
+    g = load_golden("ref_toy")
+    mdp = instance(g)
+    res = ipi.solve(mdp)
+    np.testing.assert_allclose(res.values, [2.0], atol=1e-8)
+    assert res.status is ipi.SolveStatus.CONVERGED
+    warm = ipi.solve(mdp, ipi.SolveOptions(v0=res.values))
+    assert warm.outer_iterations == 0
+
+
+def test_dense_optimum_matches_brute_force():
+    from conftest import GOLDEN
+    g = load_golden("ref_dense5x3")
+    opt = np.load(GOLDEN / "ref_dense5x3_optimum.npy")
+    res = ipi.solve(instance(g), ipi.SolveOptions(tol=1e-9))
+    np.testing.assert_allclose(res.values, opt, atol=1e-6)
+
+
+def test_max_mode_equals_negated_min():
+    g = load_golden("ref_fixture_random")
+    n, m = g["cost"].shape
+    csr = ipi.CsrMatrix(n * m, n, g["row_ptr"], g["col"], g["val"])
+    rmax = ipi.solve(ipi.MdpInstance(n, m, float(g["gamma"]), g["cost"], csr, ipi.Mode.MAX))
+    rmin = ipi.solve(ipi.MdpInstance(n, m, float(g["gamma"]), -g["cost"], csr, ipi.Mode.MIN))
+    np.testing.assert_allclose(rmax.values, -rmin.values, rtol=1e-9, atol=1e-9)
+    np.testing.assert_array_equal(rmax.policy, rmin.policy)
