@@ -1,0 +1,414 @@
+"""Benchmark: Bellman backups/s of the fused K1 kernel on BASELINE config 2.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1)
+
+Workload (BASELINE.json configs[1], the metric's config): C2 random-locality
+MDP, nS = 1,048,576, nA = 32, 64 nnz per (s,a) row (2^31 nnz, 25.8 GB of
+fp64 values + int32 indices), gamma 0.999, generated on the device from the
+seed by the Philox recipe (generators.py).  A *step* is one pass of the hot
+path over the whole instance: the value-vector exchange (NCCL all-gather of
+the V blocks when N > 1) followed by one fused Bellman backup (SpMV + cost +
+gamma + per-state argmin + residual max) over every (s, a) row.  The matrix
+(25.8 GB) is 200x the 126 MB L2, so no flush is needed between steps.
+
+``value`` = n*m / (max-over-ranks device time per step) [(s,a)-backups/s].
+``e2e`` runs the same step through the public API ``greedy_policy(mdp, v)``
+with V in pinned host memory and the policy/TV copied back every step.
+``roofline`` uses the algorithmic bytes of one K1 launch (see
+DESIGN.md) over the K1 launch time measured here with CUDA events.
+``cpu_baseline`` times the CPU oracle (numpy restatement of greedy_policy,
+bellman.py:44-68) on a bounded sample of the same instance (rank 0, N = 1).
+``ipi`` reports iPI time-to-tolerance (GMRES, alpha 1e-4, atol 1e-8) on the
+same instance from V0 = 0 (N = 1 only).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+WORKLOAD = 2  # BASELINE.json configs[1]
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--scale", type=int, default=1, help="divide n by this (debug only)")
+    ap.add_argument("--no-ipi", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ----------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, flag in zip(names, parts[4:8]):
+                if flag.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    p = REPO / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic():
+    p = REPO / "profiles" / "k1_c2_ncu.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get("dram_bytes_per_launch"), d
+    return None, None
+
+
+def k1_bytes(n: int, m: int, nnz: int) -> int:
+    """Algorithmic bytes of one K1 launch:
+    values+indices, row pointers (int64), stage costs, V (once), outputs
+    (applied f64 + policy i32)."""
+    rows = n * m
+    return nnz * 12 + (rows + 1) * 8 + rows * 8 + n * 8 + n * 12
+
+
+# ----------------------------------------------------------------------------
+def build_shard(ctx, args, torch):
+    from paper_2507_22538_b200 import devgen
+    from paper_2507_22538_b200.generators import CONFIGS
+    from paper_2507_22538_b200.parallel import MdpShard
+    from paper_2507_22538_b200.sparse import CsrMatrix
+    spec = CONFIGS[WORKLOAD]
+    n = spec.n // args.scale
+    lo, hi = ctx.block
+    rp, col, val, cost = devgen.locality(n, spec.m, spec.K, spec.window, args.seed, lo, hi - lo)
+    csr = CsrMatrix((hi - lo) * spec.m, n, rp, col, val)
+    shard = MdpShard(n, spec.m, spec.gamma, lo, cost, csr)
+    return spec, n, shard
+
+
+def cpu_baseline_sample(shard, spec, n, torch, target_s=12.0):
+    """numpy oracle greedy on a prefix of the instance's states (rank 0)."""
+    from oracle import mdp_oracle as orc
+    t = shard.transitions
+    S = min(shard.n_local, max(1024, shard.n_local // 8))
+    rows = S * spec.m
+    nnz = int(t.row_ptr[rows])
+    rp = t.row_ptr[: rows + 1].cpu().numpy()
+    col = t.col_idx[:nnz].cpu().numpy()
+    val = t.values[:nnz].cpu().numpy()
+    cost = shard.stage_cost[:S].cpu().numpy()
+    rng = np.random.default_rng(1)
+    v = rng.random(n)
+    times = []
+    t_start = time.perf_counter()
+    while True:
+        t0 = time.perf_counter()
+        orc.greedy(rp, col, val, cost, spec.gamma, v)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_start > target_s or len(times) >= 5:
+            break
+    best = min(times)
+    return {"value": rows / best, "unit": "(s,a)-backups/s", "cores": 1, "kind": "port",
+            "sample": f"first {S} of {n} states ({rows} rows, {nnz} nnz) of the same C2 instance; "
+                      f"numpy oracle greedy (oracle/mdp_oracle.py, restating bellman.py:44-68), "
+                      f"best of {len(times)} reps, single thread",
+            "nnz_per_s": nnz / best, "seconds": best}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle port on the host cores, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import torch
+    from oracle import mdp_oracle as orc
+    from paper_2507_22538_b200.generators import CONFIGS
+    spec = CONFIGS[WORKLOAD]
+    n = spec.n // args.scale
+    # bounded sample of the same instance: the first S states' rows, built by
+    # the host restatement of the device recipe (identical integer stream)
+    S = max(64, min(2048, n // 512))
+    from paper_2507_22538_b200.generators import locality_row_host
+    rows = S * spec.m
+    col = np.empty(rows * spec.K, np.int32)
+    val = np.empty(rows * spec.K)
+    cost = np.empty((S, spec.m))
+    for s in range(S):
+        for a in range(spec.m):
+            r = s * spec.m + a
+            c, v_, g = locality_row_host(s, a, n, spec.m, spec.K, spec.window, args.seed)
+            col[r * spec.K:(r + 1) * spec.K] = c
+            val[r * spec.K:(r + 1) * spec.K] = v_
+            cost[s, a] = g
+    rp = np.arange(rows + 1, dtype=np.int64) * spec.K
+    v = np.random.default_rng(1).random(n)
+    reps = max(1, int(200_000_000 // max(rows * spec.K, 1)))  # ~1 s of numpy per step
+    for _ in range(args.warmup):
+        orc.greedy(rp, col, val, cost, spec.gamma, v)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        for _ in range(reps):
+            orc.greedy(rp, col, val, cost, spec.gamma, v)
+    dt = (time.perf_counter() - t0) / args.steps
+    value = rows * reps / dt
+    line = {
+        "impl": "reference", "metric": "bellman_backups_per_s", "value": value,
+        "unit": "(s,a)-backups/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": CONFIGS[WORKLOAD].name, "n_states": n, "n_actions": spec.m,
+                   "nnz_per_row": spec.K, "gamma": spec.gamma, "sample_states": S,
+                   "sample_rows": rows, "reps_per_step": reps},
+        "cpu_baseline": {"value": value, "unit": "(s,a)-backups/s", "cores": 1, "kind": "port",
+                         "sample": f"first {S} states of C2 x {reps} reps per step; numpy oracle "
+                                   f"greedy (restates bellman.py:44-68), single thread"},
+        "e2e": {"value": value, "unit": "(s,a)-backups/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "cpu_cores_available": os.cpu_count(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2507_22538_b200 as ipi
+    from paper_2507_22538_b200.parallel import RankContext, allgather_blocks
+    from paper_2507_22538_b200.generators import CONFIGS
+    spec0 = CONFIGS[WORKLOAD]
+    ctx = RankContext.from_env(spec0.n // args.scale)
+    t_gen = time.perf_counter()
+    spec, n, shard = build_shard(ctx, args, torch)
+    torch.cuda.synchronize()
+    t_gen = time.perf_counter() - t_gen
+    plan = shard.plan()
+    lo, hi = ctx.block
+    dev = torch.device("cuda", local)
+    rng = torch.Generator(device="cpu").manual_seed(1)
+    v_full = torch.rand(n, generator=rng, dtype=torch.float64).to(dev)
+    v_local = v_full[lo:hi].clone()
+    st = torch.cuda.current_stream()
+
+    def step():
+        allgather_blocks(v_local, v_full, ctx.partition)
+        shard.bellman(v_full)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    k1_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+             for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        time.sleep(0.3)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t_begin = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_begin.record(st)
+        for i in range(args.steps):
+            ev[i][0].record(st)
+            allgather_blocks(v_local, v_full, ctx.partition)
+            k1_ev[i][0].record(st)
+            shard.bellman(v_full)
+            k1_ev[i][1].record(st)
+            ev[i][1].record(st)
+        t_end.record(st)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    total_ms = t_begin.elapsed_time(t_end)
+    k1_ms = [a.elapsed_time(b) for a, b in k1_ev]
+    ms_t = torch.tensor([total_ms / args.steps, statistics.mean(k1_ms)], device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_step, ms_k1 = float(ms_t[0]), float(ms_t[1])
+    value = n * spec.m / (ms_step * 1e-3)
+
+    # ---- e2e through the public API with pinned host buffers ---------------
+    h2d = (hi - lo) * 8
+    d2h = (hi - lo) * (4 + 8)
+    v_host = torch.empty(hi - lo, dtype=torch.float64, pin_memory=True)
+    v_host.copy_(v_local)
+    e2e_mdp = None
+    if world == 1:
+        e2e_mdp = ipi.MdpInstance(n=n, m=spec.m, gamma=spec.gamma, stage_cost=shard.stage_cost,
+                                  transitions=shard.transitions)
+        e2e_mdp._handle = shard.handle()  # same device plan; no second planning pass
+
+        def e2e_step():
+            return ipi.greedy_policy(e2e_mdp, v_host)
+    else:
+        pol_h = torch.empty(hi - lo, dtype=torch.int32, pin_memory=True)
+        app_h = torch.empty(hi - lo, dtype=torch.float64, pin_memory=True)
+
+        def e2e_step():
+            v_local.copy_(v_host, non_blocking=True)
+            allgather_blocks(v_local, v_full, ctx.partition)
+            pol, app, _ = shard.bellman(v_full)
+            pol_h.copy_(pol, non_blocking=True)
+            app_h.copy_(app, non_blocking=True)
+            st.synchronize()
+
+    for _ in range(max(args.warmup, 3)):
+        e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        e2e_step()
+    torch.cuda.synchronize()
+    e2e_s = torch.tensor([(time.perf_counter() - t0) / args.steps], device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    e2e_value = n * spec.m / float(e2e_s[0])
+    if e2e_mdp is not None:
+        e2e_mdp._handle = None  # owned by the shard
+
+    # ---- roofline --------------------------------------------------------------
+    nnz = plan["nnz"]
+    alg = k1_bytes(hi - lo, spec.m, nnz) + (n - (hi - lo)) * 0  # V counted once (n*8 inside)
+    alg = nnz * 12 + ((hi - lo) * spec.m + 1) * 8 + (hi - lo) * spec.m * 8 + n * 8 + (hi - lo) * 12
+    peak, peak_src = peaks()
+    achieved = alg / (ms_k1 * 1e-3) / 1e9
+    traffic, traffic_meta = ncu_traffic()
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": traffic, "kernel": "k1_bellman",
+            "algorithmic_bytes_per_launch": alg, "k1_ms": ms_k1, "peak_source": peak_src,
+            "frac_of_8tbs_spec": achieved / 8000.0}
+
+    out = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            cpu = cpu_baseline_sample(shard, spec, n, torch)
+        ipi_rep = None
+        if world == 1 and not args.no_ipi:
+            mdp = ipi.MdpInstance(n=n, m=spec.m, gamma=spec.gamma, stage_cost=shard.stage_cost,
+                                  transitions=shard.transitions)
+            mdp._handle = shard.handle()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            res = ipi.solve(mdp, ipi.SolveOptions(alpha=spec.alpha, tol=spec.atol))
+            t_solve = time.perf_counter() - t0
+            mdp._handle = None
+            ipi_rep = {"time_to_tol_s": res.wall_time, "time_incl_validate_s": t_solve,
+                       "status": res.status.value, "outer": res.outer_iterations,
+                       "inner": res.inner_iterations_total,
+                       "final_residual": res.residual_history[-1],
+                       "time_greedy_s": res.time_greedy, "time_assembly_s": res.time_assembly,
+                       "time_inner_s": res.time_inner,
+                       "residual_history": res.residual_history}
+        out = {
+            "metric": "bellman_backups_per_s", "value": value, "unit": "(s,a)-backups/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (device Philox generator, seed %d)" % args.seed,
+            "config": {"workload": spec.name, "n_states": n, "n_actions": spec.m,
+                       "nnz_per_row": spec.K, "nnz": int(nnz) * (world if world > 1 else 1),
+                       "gamma": spec.gamma, "window": spec.window,
+                       "parallelism": f"rowblock{world}",
+                       "l2": "inputs 25.8 GB >> 126 MB L2: no flush needed",
+                       "step": "V all-gather (N>1) + fused Bellman backup over all rows"},
+            "nnz_per_s": nnz * world / (ms_step * 1e-3),
+            "state_backups_per_s": n / (ms_step * 1e-3),
+            "e2e": {"value": e2e_value, "unit": "(s,a)-backups/s", "h2d_bytes_per_step": h2d * world,
+                    "d2h_bytes_per_step": d2h * world,
+                    "path": "greedy_policy(mdp, pinned host V) -> pinned host policy/TV"},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "gpu_launches": args.steps,
+            "clocks": clk.summary(),
+            "plan": plan,
+            "ipi": ipi_rep,
+            "gen_seconds": t_gen,
+        }
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if out is not None:
+        print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

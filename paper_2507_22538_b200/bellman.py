@@ -61,7 +61,26 @@ def greedy_device(mdp: MdpInstance, v: torch.Tensor, mode: Mode, *, with_residua
 
 
 def greedy_policy(mdp: MdpInstance, v, mode: Mode | None = None, workers=None) -> GreedyResult:
-    """Greedy policy for cost vector ``v``; ties pick the smallest action."""
+    """Greedy policy for cost vector ``v``; ties pick the smallest action.
+
+    Output placement follows the input: numpy in -> numpy out (int64 policy,
+    like bellman.py:54); CUDA tensor in -> CUDA tensors out; CPU tensor in
+    (e.g. pinned host memory) -> one H2D copy of V, one K1 launch, and D2H
+    copies of the results into pinned host tensors."""
+    host_torch = isinstance(v, torch.Tensor) and v.device.type == "cpu"
+    if host_torch:
+        if tuple(v.shape) != (mdp.n,):
+            raise ValidationError(f"cost vector length {tuple(v.shape)} does not match n = {mdp.n}")
+        vt = v.to(mdp.stage_cost.device, torch.float64, non_blocking=True)
+        if not bool(torch.isfinite(vt).all()):
+            raise ValidationError("cost vector has non-finite entries")
+        pi, applied, _ = greedy_device(mdp, vt, mode or mdp.mode)
+        pol_h = torch.empty(mdp.n, dtype=torch.int32, pin_memory=True)
+        app_h = torch.empty(mdp.n, dtype=torch.float64, pin_memory=True)
+        pol_h.copy_(pi, non_blocking=True)
+        app_h.copy_(applied, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return GreedyResult(policy=pol_h, applied=app_h)
     vt, was_np = _check_cost_vector(mdp, v)
     mode = mode or mdp.mode
     pi, applied, _ = greedy_device(mdp, vt, mode)
