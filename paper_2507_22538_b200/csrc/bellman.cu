@@ -150,6 +150,190 @@ __global__ void __launch_bounds__(kK1Threads) k1_bellman(K1Args a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Uniform-row fast path (every row has the same even length K; rows start at
+// r*K so value pairs are 16-byte aligned).  Each lane owns P value pairs per
+// row (16-byte ld.v2.f64 + 8-byte ld.v2.s32); the warp's (state, row-step)
+// batches are flattened into one stream and software-pipelined: batch b+1's
+// loads are issued before batch b's gathers/shuffles, so every warp keeps two
+// batches of CSR bytes in flight (Little's law: ~52 KB/SM at 6.4 TB/s).
+// ---------------------------------------------------------------------------
+template <int P>
+struct Batch {
+  double2 v[P];
+  int2 c[P];
+};
+
+template <int G, int P, bool WIN>
+__global__ void __launch_bounds__(kK1Threads) k1_bellman_uniform(K1Args a, int K) {
+  extern __shared__ double win[];
+  __shared__ double red[32];
+  const int64_t s_lo = a.bounds[blockIdx.x], s_hi = a.bounds[blockIdx.x + 1];
+  int64_t w_lo = 0, w_len = 0;
+  if (WIN) {
+    int64_t lo = a.state0 + s_lo - a.halo;
+    int64_t hi = a.state0 + s_hi + a.halo;
+    lo = lo < 0 ? 0 : lo;
+    hi = hi > a.n_global ? a.n_global : hi;
+    w_lo = lo;
+    w_len = hi > lo ? hi - lo : 0;
+    for (int64_t i = threadIdx.x; i < w_len; i += blockDim.x) win[i] = __ldg(a.v + lo + i);
+    __syncthreads();
+  }
+  const uint64_t pol = policy_evict_first();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  constexpr int GPW = 32 / G;
+  const int grp = lane / G, gl = lane % G;
+  const bool mx = a.maximize != 0;
+  const int m = a.m;
+  const int nit = (m + GPW - 1) / GPW;
+  const int pairs = K >> 1;
+  double res = 0.0;
+
+  auto gather = [&](int c) -> double {
+    if (WIN) {
+      const uint64_t off = (uint64_t)((int64_t)c - w_lo);
+      if (off < (uint64_t)w_len) return win[off];
+    }
+    return __ldg(a.v + c);
+  };
+  auto load = [&](int64_t s, int it, Batch<P>& b) {
+    const int act = it * GPW + grp;
+    const int64_t base = (s * (int64_t)m + act) * (int64_t)K;
+#pragma unroll
+    for (int t = 0; t < P; ++t) {
+      const int j = gl + G * t;
+      if (act < m && j < pairs) {
+        b.v[t] = ld_stream_v2(a.val + base + 2 * j, pol);
+        b.c[t] = ld_stream_v2(a.col + base + 2 * j, pol);
+      } else {
+        b.v[t] = make_double2(0.0, 0.0);
+        b.c[t] = make_int2(-1, -1);
+      }
+    }
+  };
+
+  int64_t s = s_lo + warp;
+  if (s < s_hi) {
+    int it = 0;
+    Batch<P> cur, nxt;
+    load(s, 0, cur);
+    double bq = mx ? -INFINITY : INFINITY;
+    int ba = INT_MAX;
+    while (true) {
+      int it_n = it + 1;
+      int64_t s_n = s;
+      if (it_n == nit) {
+        it_n = 0;
+        s_n = s + nwarps;
+      }
+      const bool has_next = s_n < s_hi;
+      if (has_next) load(s_n, it_n, nxt);
+      // gathers + row sum for the current batch
+      double acc = 0.0;
+#pragma unroll
+      for (int t = 0; t < P; ++t) {
+        if (cur.c[t].x >= 0) {
+          const double x0 = gather(cur.c[t].x), x1 = gather(cur.c[t].y);
+          acc = add_rn(acc, mul_rn(cur.v[t].x, x0));
+          acc = add_rn(acc, mul_rn(cur.v[t].y, x1));
+        }
+      }
+      acc = group_sum<G>(acc);
+      const int act = it * GPW + grp;
+      const int64_t row0 = s * (int64_t)m;
+      if (act < m) {
+        const double q = add_rn(__ldg(a.cost + row0 + act), mul_rn(a.gamma, acc));
+        if (better(q, act, bq, ba, mx)) {
+          bq = q;
+          ba = act;
+        }
+      }
+      if (it == nit - 1) {
+#pragma unroll
+        for (int off = 16; off >= G; off >>= 1) {
+          const double oq = __shfl_xor_sync(kFull, bq, off);
+          const int oa = __shfl_xor_sync(kFull, ba, off);
+          if (better(oq, oa, bq, ba, mx)) {
+            bq = oq;
+            ba = oa;
+          }
+        }
+        if (ba == INT_MAX) ba = 0;
+        if (lane == 0) {
+          a.policy[s] = ba;
+          a.applied[s] = bq;
+          if (a.gpi) a.gpi[s] = __ldg(a.cost + row0 + ba);
+          if (a.lenpi) a.lenpi[s] = K;
+          const double vs = WIN ? gather((int)(a.state0 + s)) : __ldg(a.v + a.state0 + s);
+          res = fmax(res, fabs(sub_rn(vs, bq)));
+        }
+        bq = mx ? -INFINITY : INFINITY;
+        ba = INT_MAX;
+      }
+      if (!has_next) break;
+      cur = nxt;
+      s = s_n;
+      it = it_n;
+    }
+  }
+  if (a.res_bits) {
+    res = warp_max(res);
+    if (lane == 0) red[warp] = res;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < nwarps; ++w) t = fmax(t, red[w]);
+      atomicMax(a.res_bits, (unsigned long long)__double_as_longlong(t));
+    }
+  }
+}
+
+// (G, P) for the uniform path: pairs = K/2 <= P*G, P = 2 (or 4 for very long rows)
+bool uniform_shape(int K, int* G, int* P) {
+  if (K <= 0 || (K & 1)) return false;
+  const int pairs = K / 2;
+  const int gs[6] = {1, 2, 4, 8, 16, 32};
+  for (int g : gs)
+    if (pairs <= 2 * g) {
+      *G = g;
+      *P = 2;
+      return true;
+    }
+  if (pairs <= 128) {
+    *G = 32;
+    *P = 4;
+    return true;
+  }
+  return false;
+}
+
+template <int G, int P>
+static void launch_u(const K1Args& a, int K, bool win, int blocks, int smem, cudaStream_t st) {
+  if (win)
+    k1_bellman_uniform<G, P, true><<<blocks, kK1Threads, smem, st>>>(a, K);
+  else
+    k1_bellman_uniform<G, P, false><<<blocks, kK1Threads, 0, st>>>(a, K);
+}
+
+template <int G, int P>
+static cudaError_t set_smem_attr_u(int smem) {
+  return cudaFuncSetAttribute(k1_bellman_uniform<G, P, true>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+}
+
+static cudaError_t uniform_smem(int G, int P, int smem) {
+  if (P == 4) return set_smem_attr_u<32, 4>(smem);
+  switch (G) {
+    case 1: return set_smem_attr_u<1, 2>(smem);
+    case 2: return set_smem_attr_u<2, 2>(smem);
+    case 4: return set_smem_attr_u<4, 2>(smem);
+    case 8: return set_smem_attr_u<8, 2>(smem);
+    case 16: return set_smem_attr_u<16, 2>(smem);
+    default: return set_smem_attr_u<32, 2>(smem);
+  }
+}
+
 template <int G>
 static void launch_g(const K1Args& a, bool win, int blocks, int smem, cudaStream_t st) {
   if (win)
@@ -175,7 +359,47 @@ int k1_set_smem(int lanes, int smem) {
     default: e = set_smem_attr<32>(smem); break;
   }
   if (e != cudaSuccess) return fail(IPI_ECUDA, std::string("k1 smem attr: ") + cudaGetErrorString(e));
+  for (int K = 2; K <= 256; K *= 2) {  // make every uniform instance launchable too
+    int G, P;
+    if (uniform_shape(K, &G, &P)) {
+      e = uniform_smem(G, P, smem);
+      if (e != cudaSuccess) return fail(IPI_ECUDA, std::string("k1 smem attr: ") + cudaGetErrorString(e));
+    }
+  }
   return IPI_OK;
+}
+
+// Resident CTAs per SM of the K1 variant the plan selects.
+int k1_occupancy(int lanes, int uniform_K, bool win, int smem) {
+  int G = 0, P = 0, nb = 0;
+  const void* fn = nullptr;
+  if (uniform_K > 0 && uniform_shape(uniform_K, &G, &P)) {
+#define U_FN(GG, PP) (win ? (const void*)k1_bellman_uniform<GG, PP, true> : (const void*)k1_bellman_uniform<GG, PP, false>)
+    if (P == 4) fn = U_FN(32, 4);
+    else switch (G) {
+      case 1: fn = U_FN(1, 2); break;
+      case 2: fn = U_FN(2, 2); break;
+      case 4: fn = U_FN(4, 2); break;
+      case 8: fn = U_FN(8, 2); break;
+      case 16: fn = U_FN(16, 2); break;
+      default: fn = U_FN(32, 2); break;
+    }
+#undef U_FN
+  } else {
+#define G_FN(GG) (win ? (const void*)k1_bellman<GG, true> : (const void*)k1_bellman<GG, false>)
+    switch (lanes) {
+      case 1: fn = G_FN(1); break;
+      case 2: fn = G_FN(2); break;
+      case 4: fn = G_FN(4); break;
+      case 8: fn = G_FN(8); break;
+      case 16: fn = G_FN(16); break;
+      default: fn = G_FN(32); break;
+    }
+#undef G_FN
+  }
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kK1Threads, win ? smem : 0) != cudaSuccess)
+    return 1;
+  return nb < 1 ? 1 : nb;
 }
 
 int launch_bellman(ipi_mdp* h, const double* v_full, int32_t mode, int32_t* policy,
@@ -202,6 +426,24 @@ int launch_bellman(ipi_mdp* h, const double* v_full, int32_t mode, int32_t* poli
   a.res_bits = res_bits;
   const bool win = h->plan.halo >= 0;
   const int blocks = h->plan.k1_blocks, smem = h->plan.k1_smem_bytes;
+  int G = 0, P = 0;
+  if (h->plan.uniform_rows && uniform_shape(h->plan.row_len_max, &G, &P)) {
+    const int K = h->plan.row_len_max;
+    if (P == 4) {
+      launch_u<32, 4>(a, K, win, blocks, smem, st);
+    } else {
+      switch (G) {
+        case 1: launch_u<1, 2>(a, K, win, blocks, smem, st); break;
+        case 2: launch_u<2, 2>(a, K, win, blocks, smem, st); break;
+        case 4: launch_u<4, 2>(a, K, win, blocks, smem, st); break;
+        case 8: launch_u<8, 2>(a, K, win, blocks, smem, st); break;
+        case 16: launch_u<16, 2>(a, K, win, blocks, smem, st); break;
+        default: launch_u<32, 2>(a, K, win, blocks, smem, st); break;
+      }
+    }
+    IPI_LAUNCH_CHECK();
+    return IPI_OK;
+  }
   switch (h->plan.lanes_per_row) {
     case 1: launch_g<1>(a, win, blocks, smem, st); break;
     case 2: launch_g<2>(a, win, blocks, smem, st); break;

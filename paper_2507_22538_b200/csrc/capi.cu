@@ -32,6 +32,7 @@ int pick_lanes_per_row(double mean_len) {
 }
 
 int k1_set_smem(int lanes, int smem);  // bellman.cu
+int k1_occupancy(int lanes, int uniform_K, bool win, int smem);
 
 // ---------------------------------------------------------------------------
 // planning kernels
@@ -315,8 +316,9 @@ int ipi_mdp_create(const int64_t* row_ptr, const int32_t* col, const double* val
     int rc = k1_set_smem(p.lanes_per_row, p.k1_smem_bytes);
     if (rc) return bail(rc);
   } else {
-    k1_blocks = h->num_sms * 4;
     p.k1_smem_bytes = 0;
+    k1_blocks = h->num_sms * k1_occupancy(p.lanes_per_row, p.uniform_rows ? p.row_len_max : 0,
+                                          false, 0);
   }
   // enough states per CTA: at least one per warp
   const int64_t max_blocks = std::max<int64_t>(1, (n_local + 15) / 16);

@@ -68,6 +68,19 @@ __device__ __forceinline__ int64_t ld_stream_i64(const int64_t* p, uint64_t pol)
   return (int64_t)ld_stream(reinterpret_cast<const long long*>(p), pol);
 }
 
+__device__ __forceinline__ double2 ld_stream_v2(const double* p, uint64_t pol) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+               : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int2 ld_stream_v2(const int* p, uint64_t pol) {
+  int2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.s32 {%0, %1}, [%2], %3;"
+               : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol));
+  return v;
+}
+
 // Exact two-step rounding as numpy does it (no FMA contraction):
 // prod = a*b rounded, then sum rounded.
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }

@@ -131,12 +131,17 @@ def test_solve_matches_reference(name, kind):
                     bool(g["maximize"]))
     assert_policy_parity(res.policy, g[f"solve_{kind}_policy"], gap)
     hist, ref_h = np.asarray(res.residual_history), g[f"solve_{kind}_history"]
-    # Intermediate iterates are only pinned to the inner tolerance (alpha = 1e-4 forcing):
-    # rounding-order differences move them within it, so history entries far above the
-    # noise floor agree to alpha-level relative error (C1/C4 show <= 4e-9 in practice);
-    # the tail only needs <= tol.  Final V is asserted at 1e-8 above.
+    # Intermediate iterates are only pinned to the inner tolerance: the inner solve stops at
+    # ||r||_2 <= alpha * res_{k-1}, so rounding-order differences may move V_k (and hence
+    # res_k) by about alpha * res_{k-1}.  Entries far above the noise floor must agree to
+    # 1e-6 relative plus that one-alpha-step slack; the tail only needs <= tol.  The final
+    # V is asserted at 1e-8 above.
+    alpha = 1e-4
+    slack = np.concatenate(([0.0], alpha * ref_h[:-1]))
     big = ref_h > 1e-10
-    np.testing.assert_allclose(hist[big], ref_h[big], rtol=1e-4, atol=1e-13 * scale)
+    err = np.abs(hist - ref_h)
+    allowed = 1e-6 * ref_h + slack + 1e-13 * scale
+    assert np.all(err[big] <= allowed[big]), (hist, ref_h)
     assert hist[-1] <= s["tol"]
     # independent certificate: recompute the Bellman residual of the returned V
     _, applied = orc.greedy(g["row_ptr"], g["col"], g["val"], g["cost"], float(g["gamma"]),
