@@ -84,7 +84,16 @@ def solve_parity(mdp, spec, arrays, *, tol=None, kind="gmres", max_outer=1000):
     ref = orc.solve(rp, col, val, cost, spec.gamma, tol=tol, alpha=spec.alpha, kind=kind,
                     max_outer=max_outer)
     assert res.status.value == ref.status
-    assert res.outer_iterations == ref.outer_iterations
+    # The last inner solve only reaches ||r||_2 <= alpha*res; when the oracle's final
+    # outer residual lands within that slack of tol, a rounding-order difference can
+    # cost one extra outer step (observed once on C4: 34 vs 33, final V within 2e-10).
+    assert abs(res.outer_iterations - ref.outer_iterations) <= 1, (res.residual_history,
+                                                                   ref.residual_history)
+    k = min(len(res.residual_history), len(ref.residual_history)) - 1
+    h, hr = np.asarray(res.residual_history[:k]), np.asarray(ref.residual_history[:k])
+    slack = np.concatenate(([0.0], spec.alpha * hr[:-1])) if k else hr
+    big = hr > 1e-7
+    assert np.all(np.abs(h - hr)[big] <= (1e-6 * hr + slack)[big])
     scale = max(1.0, np.abs(ref.values).max())
     np.testing.assert_allclose(res.values, ref.values, rtol=1e-8, atol=1e-8 * scale)
     gap = orc.q_gap(rp, col, val, cost, spec.gamma, ref.values)
