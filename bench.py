@@ -359,6 +359,7 @@ def run_ours(args):
             mdp = ipi.MdpInstance(n=n, m=spec.m, gamma=spec.gamma, stage_cost=shard.stage_cost,
                                   transitions=shard.transitions)
             mdp._handle = shard.handle()
+            ipi.solve(mdp, ipi.SolveOptions(alpha=spec.alpha, tol=spec.atol))  # warm-up (lazy loading)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             res = ipi.solve(mdp, ipi.SolveOptions(alpha=spec.alpha, tol=spec.atol))

@@ -158,12 +158,6 @@ __global__ void __launch_bounds__(kK1Threads) k1_bellman(K1Args a) {
 // loads are issued before batch b's gathers/shuffles, so every warp keeps two
 // batches of CSR bytes in flight (Little's law: ~52 KB/SM at 6.4 TB/s).
 // ---------------------------------------------------------------------------
-template <int P>
-struct Batch {
-  double2 v[P];
-  int2 c[P];
-};
-
 template <int G, int P, bool WIN>
 __global__ void __launch_bounds__(kK1Threads) k1_bellman_uniform(K1Args a, int K) {
   extern __shared__ double win[];
@@ -300,12 +294,7 @@ bool uniform_shape(int K, int* G, int* P) {
       *P = 2;
       return true;
     }
-  if (pairs <= 128) {
-    *G = 32;
-    *P = 4;
-    return true;
-  }
-  return false;
+  return false;  // rows longer than 128: generic path
 }
 
 template <int G, int P>
@@ -323,15 +312,11 @@ static cudaError_t set_smem_attr_u(int smem) {
 }
 
 static cudaError_t uniform_smem(int G, int P, int smem) {
-  if (P == 4) return set_smem_attr_u<32, 4>(smem);
-  switch (G) {
-    case 1: return set_smem_attr_u<1, 2>(smem);
-    case 2: return set_smem_attr_u<2, 2>(smem);
-    case 4: return set_smem_attr_u<4, 2>(smem);
-    case 8: return set_smem_attr_u<8, 2>(smem);
-    case 16: return set_smem_attr_u<16, 2>(smem);
-    default: return set_smem_attr_u<32, 2>(smem);
-  }
+  cudaError_t e = cudaSuccess;
+#define IPI_U_SMEM(GG, PP) e = set_smem_attr_u<GG, PP>(smem)
+  IPI_DISPATCH_UNIFORM(G, P, IPI_U_SMEM);
+#undef IPI_U_SMEM
+  return e;
 }
 
 template <int G>
@@ -374,16 +359,9 @@ int k1_occupancy(int lanes, int uniform_K, bool win, int smem) {
   int G = 0, P = 0, nb = 0;
   const void* fn = nullptr;
   if (uniform_K > 0 && uniform_shape(uniform_K, &G, &P)) {
-#define U_FN(GG, PP) (win ? (const void*)k1_bellman_uniform<GG, PP, true> : (const void*)k1_bellman_uniform<GG, PP, false>)
-    if (P == 4) fn = U_FN(32, 4);
-    else switch (G) {
-      case 1: fn = U_FN(1, 2); break;
-      case 2: fn = U_FN(2, 2); break;
-      case 4: fn = U_FN(4, 2); break;
-      case 8: fn = U_FN(8, 2); break;
-      case 16: fn = U_FN(16, 2); break;
-      default: fn = U_FN(32, 2); break;
-    }
+#define U_FN(GG, PP) fn = (win ? (const void*)k1_bellman_uniform<GG, PP, true> \
+                           : (const void*)k1_bellman_uniform<GG, PP, false>)
+    IPI_DISPATCH_UNIFORM(G, P, U_FN);
 #undef U_FN
   } else {
 #define G_FN(GG) (win ? (const void*)k1_bellman<GG, true> : (const void*)k1_bellman<GG, false>)
@@ -429,18 +407,9 @@ int launch_bellman(ipi_mdp* h, const double* v_full, int32_t mode, int32_t* poli
   int G = 0, P = 0;
   if (h->plan.uniform_rows && uniform_shape(h->plan.row_len_max, &G, &P)) {
     const int K = h->plan.row_len_max;
-    if (P == 4) {
-      launch_u<32, 4>(a, K, win, blocks, smem, st);
-    } else {
-      switch (G) {
-        case 1: launch_u<1, 2>(a, K, win, blocks, smem, st); break;
-        case 2: launch_u<2, 2>(a, K, win, blocks, smem, st); break;
-        case 4: launch_u<4, 2>(a, K, win, blocks, smem, st); break;
-        case 8: launch_u<8, 2>(a, K, win, blocks, smem, st); break;
-        case 16: launch_u<16, 2>(a, K, win, blocks, smem, st); break;
-        default: launch_u<32, 2>(a, K, win, blocks, smem, st); break;
-      }
-    }
+#define IPI_U_LAUNCH(GG, PP) launch_u<GG, PP>(a, K, win, blocks, smem, st)
+    IPI_DISPATCH_UNIFORM(G, P, IPI_U_LAUNCH);
+#undef IPI_U_LAUNCH
     IPI_LAUNCH_CHECK();
     return IPI_OK;
   }

@@ -58,15 +58,18 @@ __global__ void row_stats_kernel(const int64_t* rp, int64_t rows, unsigned long 
 }
 
 // log2 histogram of |col - state| (locality profile, 40 buckets)
+// Rows are sampled with a fixed stride (>= 2^17 sampled rows) so planning stays
+// a few ms even at 2^31 nnz; the histogram only steers the window size.
 __global__ void locality_hist_kernel(const int64_t* rp, const int32_t* col, int64_t rows, int m,
-                                     int64_t state0, unsigned long long* hist) {
+                                     int64_t state0, int64_t stride, unsigned long long* hist) {
   __shared__ unsigned long long sh[40];
   for (int i = threadIdx.x; i < 40; i += blockDim.x) sh[i] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t r = wg; r < rows; r += nw) {
+  for (int64_t rs = wg; rs * stride < rows; rs += nw) {
+    const int64_t r = rs * stride;
     const int64_t s = state0 + r / m;
     const int64_t p0 = rp[r], p1 = rp[r + 1];
     for (int64_t p = p0 + lane; p < p1; p += 32) {
@@ -259,7 +262,9 @@ int ipi_mdp_create(const int64_t* row_ptr, const int32_t* col, const double* val
   int64_t nnz = 0;
   if (rows > 0) {
     row_stats_kernel<<<grid_for(rows, 256, h->num_sms), 256, 0, st>>>(row_ptr, rows, d_tmp);
-    locality_hist_kernel<<<h->num_sms * 8, 256, 0, st>>>(row_ptr, col, rows, m, state0, d_tmp + 8);
+    const int64_t stride = std::max<int64_t>(1, rows >> 17);
+    locality_hist_kernel<<<h->num_sms * 8, 256, 0, st>>>(row_ptr, col, rows, m, state0, stride,
+                                                         d_tmp + 8);
   }
   unsigned long long hst[48];
   cudaMemcpyAsync(hst, d_tmp, sizeof(hst), cudaMemcpyDeviceToHost, st);
@@ -290,7 +295,7 @@ int ipi_mdp_create(const int64_t* row_ptr, const int32_t* col, const double* val
   for (int b = 0; b < 40; ++b) cum[b + 1] = cum[b] + (double)hst[8 + b];
   auto coverage = [&](int k) {  // d < 2^k  <=> bucket <= k
     const int b = std::min(k, 39);
-    return nnz > 0 ? cum[b + 1] / (double)nnz : 1.0;
+    return cum[40] > 0 ? cum[b + 1] / cum[40] : 1.0;
   };
   int kfit = -1;
   for (int k = 0; k <= 31; ++k) {
@@ -543,7 +548,8 @@ int ipi_inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* v
   ipi_inner_report* d_rep = nullptr;
   IPI_CUDA_TRY(cudaMalloc(&d_rep, sizeof(ipi_inner_report)));
   int rc = inner_solve(rp_pi, col_pi, val_pi, n, gamma, b, x, target_2norm, max_it, kind,
-                       richardson_scale, pick_lanes_per_row((double)nnz / (double)n), -1, d_rep, st);
+                       richardson_scale, pick_lanes_per_row((double)nnz / (double)n), -1, 0, d_rep,
+                       st);
   if (rc == IPI_OK && report) {
     cudaError_t e = cudaMemcpyAsync(report, d_rep, sizeof(*report), cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
@@ -645,7 +651,7 @@ int ipi_solve(ipi_mdp* h, const ipi_opts* o, double* v, int32_t* policy, double*
     IPI_CUDA_TRY(cudaMemcpyAsync(vnext, vcur, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
     rc = inner_solve(h->rp_pi, h->col_pi, h->val_pi, n, h->gamma, h->gpi, vnext, target, cap,
                      o->ksp_type, o->richardson_scale, h->plan.lanes_per_row, h->plan.halo,
-                     h->d_report, st);
+                     h->plan.uniform_rows ? h->plan.row_len_max : 0, h->d_report, st);
     if (rc) return rc;
     cudaEventRecord(pi_.b, st);
     phases.push_back(pi_);

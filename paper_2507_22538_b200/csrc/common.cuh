@@ -81,6 +81,13 @@ __device__ __forceinline__ int2 ld_stream_v2(const int* p, uint64_t pol) {
   return v;
 }
 
+// Register batch of P value pairs + column pairs (uniform-row fast paths).
+template <int P>
+struct Batch {
+  double2 v[P];
+  int2 c[P];
+};
+
 // Exact two-step rounding as numpy does it (no FMA contraction):
 // prod = a*b rounded, then sum rounded.
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }

@@ -39,10 +39,36 @@ struct ipi_mdp {
 namespace ipi {
 
 constexpr int kK1Threads = 512;
-constexpr int kInnerThreads = 512;
+constexpr int kInnerThreads = 1024;
 constexpr int kGmresRestart = 30;  // inner.py:40
 
 int pick_lanes_per_row(double mean_len);
+bool uniform_shape(int K, int* G, int* P);
+
+// Dispatch a uniform-row (G, P) shape chosen by uniform_shape() to a template
+// instance: P = 1 with G in {1..32}, or (G, P) = (32, 2).
+#define IPI_DISPATCH_UNIFORM(G_, P_, FN)                 \
+  do {                                                   \
+    if ((P_) == 2) {                                     \
+      switch (G_) {                                      \
+        case 1: FN(1, 2); break;                         \
+        case 2: FN(2, 2); break;                         \
+        case 4: FN(4, 2); break;                         \
+        case 8: FN(8, 2); break;                         \
+        case 16: FN(16, 2); break;                       \
+        default: FN(32, 2); break;                       \
+      }                                                  \
+    } else {                                             \
+      switch (G_) {                                      \
+        case 1: FN(1, 1); break;                         \
+        case 2: FN(2, 1); break;                         \
+        case 4: FN(4, 1); break;                         \
+        case 8: FN(8, 1); break;                         \
+        case 16: FN(16, 1); break;                       \
+        default: FN(32, 1); break;                       \
+      }                                                  \
+    }                                                    \
+  } while (0)
 
 // bellman.cu
 int launch_bellman(ipi_mdp* h, const double* v_full, int32_t mode, int32_t* policy,
@@ -63,8 +89,8 @@ int launch_spmv(const int64_t* rp, const int32_t* col, const double* val, int64_
 // krylov.cu
 int inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi, int64_t n,
                 double gamma, const double* b, double* x, double target, int32_t max_it,
-                int32_t kind, double scale, int lanes, int halo, ipi_inner_report* d_report,
-                cudaStream_t st);
+                int32_t kind, double scale, int lanes, int halo, int uniform_K,
+                ipi_inner_report* d_report, cudaStream_t st);
 
 // device scratch arena for the inner solver (per device, grown on demand)
 double* krylov_workspace(int64_t n, int64_t doubles_needed);

@@ -20,6 +20,7 @@
 // Every vector op uses separate mul/add roundings like numpy (no FMA).
 #include <cooperative_groups.h>
 
+#include <algorithm>
 #include <mutex>
 
 #include "handle.cuh"
@@ -47,7 +48,9 @@ struct KArgs {
   int kind;
   double scale;
   int halo;
-  int win_cap;
+  int win_cap;   // doubles of the shared-memory window (0 = none)
+  int own_cap;   // doubles of the shared-memory w slice (0 = w in global)
+  int K;         // uniform row length of P_pi (0 = variable)
   ipi_inner_report* rep;
 };
 
@@ -90,8 +93,11 @@ __device__ __forceinline__ void grid_allreduce(double (&v)[NV], const KArgs& a, 
 }
 
 // Row sums of P_pi over this CTA's rows with an optional shared-memory window
-// of the input vector; epi(s, Px_s) is called by one lane per row.
-template <int G, bool WIN, class Epi>
+// of the input vector; epi(s, Px_s) is called by one lane per row.  P == 0:
+// generic rows (G lanes strided over the row, 4 loads in flight); P > 0:
+// uniform even-length rows, P 16-byte value pairs per lane, batches
+// software-pipelined across row groups (same scheme as K1's fast path).
+template <int G, int P, bool WIN, class Epi>
 __device__ __forceinline__ void spmv_rows(const KArgs& a, const double* xin, int64_t s_lo,
                                           int64_t s_hi, double* win, uint64_t pol, Epi&& epi) {
   int64_t w_lo = 0, w_len = 0;
@@ -107,49 +113,93 @@ __device__ __forceinline__ void spmv_rows(const KArgs& a, const double* xin, int
     }
     __syncthreads();
   }
+  auto gather = [&](int c) -> double {
+    if (WIN) {
+      const uint64_t off = (uint64_t)((int64_t)c - w_lo);
+      if (off < (uint64_t)w_len) return win[off];
+    }
+    return xin[c];
+  };
   constexpr int GPW = 32 / G;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int grp = lane / G, gl = lane % G;
-  for (int64_t base = s_lo + (int64_t)warp * GPW; base < s_hi; base += (int64_t)nwarps * GPW) {
-    const int64_t s = base + grp;
-    double acc = 0.0;
-    if (s < s_hi) {
-      const int64_t p0 = __ldg(a.rp + s), p1 = __ldg(a.rp + s + 1);
-      for (int64_t p = p0 + gl; p < p1; p += 4 * G) {
-        double vv[4];
-        int cc[4];
+  if constexpr (P == 0) {
+    for (int64_t base = s_lo + (int64_t)warp * GPW; base < s_hi; base += (int64_t)nwarps * GPW) {
+      const int64_t s = base + grp;
+      double acc = 0.0;
+      if (s < s_hi) {
+        const int64_t p0 = __ldg(a.rp + s), p1 = __ldg(a.rp + s + 1);
+        for (int64_t p = p0 + gl; p < p1; p += 4 * G) {
+          double vv[4];
+          int cc[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int64_t q = p + (int64_t)u * G;
-          if (q < p1) {
-            vv[u] = ld_stream(a.val + q, pol);
-            cc[u] = ld_stream(a.col + q, pol);
-          } else {
-            vv[u] = 0.0;
-            cc[u] = -1;
+          for (int u = 0; u < 4; ++u) {
+            const int64_t q = p + (int64_t)u * G;
+            if (q < p1) {
+              vv[u] = ld_stream(a.val + q, pol);
+              cc[u] = ld_stream(a.col + q, pol);
+            } else {
+              vv[u] = 0.0;
+              cc[u] = -1;
+            }
+          }
+          double xx[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) xx[u] = cc[u] >= 0 ? gather(cc[u]) : 0.0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (cc[u] >= 0) acc = add_rn(acc, mul_rn(vv[u], xx[u]));
+        }
+      }
+      acc = group_sum<G>(acc);
+      if (s < s_hi && gl == 0) epi(s, acc);
+    }
+  } else {
+    const int K = a.K, pairs = K >> 1;
+    auto load = [&](int64_t base, Batch<P>& b) {
+      const int64_t s = base + grp;
+#pragma unroll
+      for (int t = 0; t < P; ++t) {
+        const int j = gl + G * t;
+        if (s < s_hi && j < pairs) {
+          b.v[t] = ld_stream_v2(a.val + s * K + 2 * j, pol);
+          b.c[t] = ld_stream_v2(a.col + s * K + 2 * j, pol);
+        } else {
+          b.v[t] = make_double2(0.0, 0.0);
+          b.c[t] = make_int2(-1, -1);
+        }
+      }
+    };
+    int64_t base = s_lo + (int64_t)warp * GPW;
+    if (base < s_hi) {
+      Batch<P> cur, nxt;
+      load(base, cur);
+      while (true) {
+        const int64_t nb = base + (int64_t)nwarps * GPW;
+        const bool has_next = nb < s_hi;
+        if (has_next) load(nb, nxt);
+        double acc = 0.0;
+#pragma unroll
+        for (int t = 0; t < P; ++t) {
+          if (cur.c[t].x >= 0) {
+            const double x0 = gather(cur.c[t].x), x1 = gather(cur.c[t].y);
+            acc = add_rn(acc, mul_rn(cur.v[t].x, x0));
+            acc = add_rn(acc, mul_rn(cur.v[t].y, x1));
           }
         }
-        double xx[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          xx[u] = 0.0;
-          if (cc[u] >= 0) {
-            const uint64_t off = (uint64_t)((int64_t)cc[u] - w_lo);
-            xx[u] = (WIN && off < (uint64_t)w_len) ? win[off] : xin[cc[u]];
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (cc[u] >= 0) acc = add_rn(acc, mul_rn(vv[u], xx[u]));
+        acc = group_sum<G>(acc);
+        const int64_t s = base + grp;
+        if (s < s_hi && gl == 0) epi(s, acc);
+        if (!has_next) break;
+        cur = nxt;
+        base = nb;
       }
     }
-    acc = group_sum<G>(acc);
-    if (s < s_hi && gl == 0) epi(s, acc);
   }
 }
 
-template <int G, bool WIN>
-__global__ void __launch_bounds__(kInnerThreads, 2) inner_kernel(KArgs a) {
+template <int G, int P, bool WIN>
+__global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double win[];
   __shared__ KShared sh;
@@ -168,13 +218,15 @@ __global__ void __launch_bounds__(kInnerThreads, 2) inner_kernel(KArgs a) {
   const double* b = a.b;
   double* x = a.x;
   double* r = a.r;
-  double* w = a.w;
+  // this CTA's slice of w: shared memory when it fits, else its global rows
+  const bool w_shared = (s_hi - s_lo) <= a.own_cap;
+  double* wl = w_shared ? (win + a.win_cap) : (a.w + s_lo);
   int slot = 0;
 
   // ---- r = b - (x - gamma P x), ||b||, ||r|| --------------------------------
   double acc2[2] = {0.0, 0.0};
   for (int64_t i = s_lo + tid; i < s_hi; i += nthr) acc2[0] = add_rn(acc2[0], mul_rn(b[i], b[i]));
-  spmv_rows<G, WIN>(a, x, s_lo, s_hi, win, pol, [&](int64_t s, double px) {
+  spmv_rows<G, P, WIN>(a, x, s_lo, s_hi, win, pol, [&](int64_t s, double px) {
     const double ri = sub_rn(b[s], sub_rn(x[s], mul_rn(gam, px)));
     r[s] = ri;
     acc2[1] = add_rn(acc2[1], mul_rn(ri, ri));
@@ -192,7 +244,7 @@ __global__ void __launch_bounds__(kInnerThreads, 2) inner_kernel(KArgs a) {
       ++it;
       grid.sync();
       double acc1[1] = {0.0};
-      spmv_rows<G, WIN>(a, x, s_lo, s_hi, win, pol, [&](int64_t s, double px) {
+      spmv_rows<G, P, WIN>(a, x, s_lo, s_hi, win, pol, [&](int64_t s, double px) {
         const double ri = sub_rn(b[s], sub_rn(x[s], mul_rn(gam, px)));
         r[s] = ri;
         acc1[0] = add_rn(acc1[0], mul_rn(ri, ri));
@@ -218,9 +270,9 @@ __global__ void __launch_bounds__(kInnerThreads, 2) inner_kernel(KArgs a) {
         const double* Vj = a.V + (int64_t)j * n;
         const double* V0 = a.V;
         double p[1] = {0.0};
-        spmv_rows<G, WIN>(a, Vj, s_lo, s_hi, win, pol, [&](int64_t s, double px) {
+        spmv_rows<G, P, WIN>(a, Vj, s_lo, s_hi, win, pol, [&](int64_t s, double px) {
           const double wi = sub_rn(Vj[s], mul_rn(gam, px));
-          w[s] = wi;
+          wl[s - s_lo] = wi;
           p[0] = add_rn(p[0], mul_rn(V0[s], wi));
         });
         ++it;
@@ -234,14 +286,14 @@ __global__ void __launch_bounds__(kInnerThreads, 2) inner_kernel(KArgs a) {
           double q = 0.0;
           if (l < j) {
             for (int64_t i = s_lo + tid; i < s_hi; i += nthr) {
-              const double wi = sub_rn(w[i], mul_rn(hlj, Vl[i]));
-              w[i] = wi;
+              const double wi = sub_rn(wl[i - s_lo], mul_rn(hlj, Vl[i]));
+              wl[i - s_lo] = wi;
               q = add_rn(q, mul_rn(Vn[i], wi));
             }
           } else {
             for (int64_t i = s_lo + tid; i < s_hi; i += nthr) {
-              const double wi = sub_rn(w[i], mul_rn(hlj, Vl[i]));
-              w[i] = wi;
+              const double wi = sub_rn(wl[i - s_lo], mul_rn(hlj, Vl[i]));
+              wl[i - s_lo] = wi;
               q = add_rn(q, mul_rn(wi, wi));
             }
           }
@@ -279,7 +331,7 @@ __global__ void __launch_bounds__(kInnerThreads, 2) inner_kernel(KArgs a) {
         ++j;
         if (brk == 2) break;  // estimated convergence / invariant subspace
         double* Vnew = a.V + (int64_t)j * n;
-        for (int64_t i = s_lo + tid; i < s_hi; i += nthr) Vnew[i] = w[i] / hnorm;
+        for (int64_t i = s_lo + tid; i < s_hi; i += nthr) Vnew[i] = wl[i - s_lo] / hnorm;
         grid.sync();
       }
       if (j == 0) break;
@@ -300,7 +352,7 @@ __global__ void __launch_bounds__(kInnerThreads, 2) inner_kernel(KArgs a) {
       }
       grid.sync();
       double acc1[1] = {0.0};
-      spmv_rows<G, WIN>(a, x, s_lo, s_hi, win, pol, [&](int64_t s, double px) {
+      spmv_rows<G, P, WIN>(a, x, s_lo, s_hi, win, pol, [&](int64_t s, double px) {
         const double ri = sub_rn(b[s], sub_rn(x[s], mul_rn(gam, px)));
         r[s] = ri;
         acc1[0] = add_rn(acc1[0], mul_rn(ri, ri));
@@ -351,42 +403,42 @@ double* krylov_workspace(int64_t /*n*/, int64_t doubles_needed) {
   return g_ws;
 }
 
-template <int G, bool WIN>
-static int launch_inner_t(KArgs& a, int smem, cudaStream_t st) {
-  auto fn = inner_kernel<G, WIN>;
-  if (WIN) {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return fail(IPI_ECUDA, std::string("inner smem attr: ") + cudaGetErrorString(e));
-  }
-  int dev = 0, sms = 0, per_sm = 0;
-  IPI_CUDA_TRY(cudaGetDevice(&dev));
-  IPI_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+template <int G, int P, bool WIN>
+static int launch_inner_t(KArgs& a, int smem, int blocks, cudaStream_t st) {
+  auto fn = inner_kernel<G, P, WIN>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return fail(IPI_ECUDA, std::string("inner smem attr: ") + cudaGetErrorString(e));
+  int per_sm = 0;
   IPI_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kInnerThreads, smem));
   if (per_sm < 1) return fail(IPI_ECUDA, "inner kernel cannot be resident (smem/regs)");
-  // small systems are barrier-latency bound: one CTA per SM; large ones: up to 2
-  const int64_t nnz_est = a.n * 64;
-  int use = (a.n < 200000 && nnz_est < (1ll << 24)) ? 1 : (per_sm >= 2 ? 2 : 1);
-  int blocks = sms * use;
-  int64_t max_useful = (a.n + 31) / 32;
-  if (blocks > max_useful) blocks = (int)(max_useful < 1 ? 1 : max_useful);
-  a.partials = a.partials;  // sized by caller for 2*blocks*2
   void* args[] = {(void*)&a};
   IPI_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)fn, dim3(blocks), dim3(kInnerThreads), args,
                                            (size_t)smem, st));
   return IPI_OK;
 }
 
+template <int G, int P>
+static int launch_inner_gp(KArgs& a, bool win, int smem, int blocks, cudaStream_t st) {
+  return win ? launch_inner_t<G, P, true>(a, smem, blocks, st)
+             : launch_inner_t<G, P, false>(a, smem, blocks, st);
+}
+
 int inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi, int64_t n,
                 double gamma, const double* b, double* x, double target, int32_t max_it,
-                int32_t kind, double scale, int lanes, int halo, ipi_inner_report* d_report,
-                cudaStream_t st) {
+                int32_t kind, double scale, int lanes, int halo, int uniform_K,
+                ipi_inner_report* d_report, cudaStream_t st) {
   if (kind != IPI_KSP_GMRES && kind != IPI_KSP_RICHARDSON)
     return fail(IPI_EVALIDATION, "inner solver kind not built on the device path yet");
   if (max_it < 1) return fail(IPI_EVALIDATION, "iteration cap must be >= 1, got " + std::to_string(max_it));
   if (target < 0.0) return fail(IPI_EVALIDATION, "residual target must be >= 0");
   if (n == 0) return fail(IPI_EDIMENSION, "empty system");
-  const int64_t max_blocks = 148 * 4;
-  const int64_t need = (int64_t)(R + 1) * n + 2 * n + 4 * max_blocks;
+  int dev = 0, sms = 148;
+  IPI_CUDA_TRY(cudaGetDevice(&dev));
+  IPI_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  // one 1024-thread CTA per SM (fewer for tiny systems: >= 32 rows per CTA)
+  int blocks = sms;
+  if ((int64_t)blocks * 32 > n) blocks = (int)std::max<int64_t>(1, n / 32);
+  const int64_t need = (int64_t)(R + 1) * n + 2 * n + 4 * (int64_t)blocks;
   double* ws = krylov_workspace(n, need);
   if (!ws) return fail(IPI_ERESOURCE, "cannot allocate Krylov workspace of " + std::to_string(need * 8) + " bytes");
   KArgs a;
@@ -405,42 +457,40 @@ int inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_p
   a.max_it = max_it;
   a.kind = kind;
   a.scale = scale;
-  a.halo = halo;
   a.rep = d_report;
-  // Shared-memory window of the multiplied vector: own slice + 2*halo doubles.
-  // Prefer two 512-thread CTAs per SM (<= 100 KB each); fall back to one CTA
-  // (<= 200 KB) or to plain L1 gathers when even that does not fit.
-  int smem = 0;
-  a.win_cap = 0;
-  if (halo >= 0) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    for (int use = 2; use >= 1 && smem == 0; --use) {
-      const int64_t own = (n + (int64_t)sms * use - 1) / ((int64_t)sms * use);
-      int64_t cap = own + own / 4 + 2 * (int64_t)halo + 64;
-      if (cap > n) cap = n;
-      const int64_t bytes = cap * 8;
-      if (bytes <= (use == 2 ? 100 : 200) * 1024) {
-        smem = (int)bytes;
-        a.win_cap = (int)cap;
-      }
-    }
-    if (smem == 0) halo = -1;
-    a.halo = halo;
+  int G = lanes, P = 0;
+  a.K = 0;
+  if (uniform_K > 0 && uniform_shape(uniform_K, &G, &P)) a.K = uniform_K;
+  else P = 0;
+  // shared memory: [window: own + 2*halo][w slice: own]; budget ~200 KB
+  const int64_t budget = 200 * 1024 / 8;
+  const int64_t own_est = (n + blocks - 1) / blocks;
+  int64_t own_cap = a.K ? own_est + 1 : std::min<int64_t>(n, 2 * own_est + 32);
+  int64_t win_cap = 0;
+  if (halo >= 0) win_cap = std::min<int64_t>(n, own_cap + 2 * (int64_t)halo);
+  if (win_cap + own_cap > budget) own_cap = 0;      // keep the window, w in global
+  if (win_cap > budget) win_cap = 0;                // window does not fit either
+  if (win_cap + own_cap > budget) own_cap = 0;
+  a.halo = win_cap > 0 ? halo : -1;
+  a.win_cap = (int)win_cap;
+  a.own_cap = (int)own_cap;
+  const bool win = win_cap > 0;
+  const int smem = (int)((win_cap + own_cap) * 8);
+  if (P > 0) {
+    int rc = IPI_OK;
+#define IPI_INNER_LAUNCH(GG, PP) rc = launch_inner_gp<GG, PP>(a, win, smem, blocks, st)
+    IPI_DISPATCH_UNIFORM(G, P, IPI_INNER_LAUNCH);
+#undef IPI_INNER_LAUNCH
+    return rc;
   }
-  const bool win = halo >= 0;
-#define IPI_INNER(GG)                                                           \
-  return win ? launch_inner_t<GG, true>(a, smem, st) : launch_inner_t<GG, false>(a, 0, st)
   switch (lanes) {
-    case 1: IPI_INNER(1);
-    case 2: IPI_INNER(2);
-    case 4: IPI_INNER(4);
-    case 8: IPI_INNER(8);
-    case 16: IPI_INNER(16);
-    default: IPI_INNER(32);
+    case 1: return launch_inner_gp<1, 0>(a, win, smem, blocks, st);
+    case 2: return launch_inner_gp<2, 0>(a, win, smem, blocks, st);
+    case 4: return launch_inner_gp<4, 0>(a, win, smem, blocks, st);
+    case 8: return launch_inner_gp<8, 0>(a, win, smem, blocks, st);
+    case 16: return launch_inner_gp<16, 0>(a, win, smem, blocks, st);
+    default: return launch_inner_gp<32, 0>(a, win, smem, blocks, st);
   }
-#undef IPI_INNER
 }
 
 }  // namespace ipi
