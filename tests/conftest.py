@@ -15,6 +15,17 @@ if str(REPO) not in sys.path:
     sys.path.insert(0, str(REPO))
 
 
+def _ensure_oracle_built():
+    try:
+        from oracle import build_oracle
+        build_oracle.build()
+    except Exception:  # pragma: no cover - reported by the tests that need it
+        pass
+
+
+_ensure_oracle_built()
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and the built library")
     config.addinivalue_line("markers", "slow: long-running case")

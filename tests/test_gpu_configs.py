@@ -220,3 +220,42 @@ def test_c2_full_solve_certificate(c2_full):
     assert r <= spec.atol
     # a-posteriori bound ||V - V*|| <= r / (1 - gamma) is then <= 1e-5
     assert r / (1 - spec.gamma) <= 1e-5
+
+
+# ----------------------------------------------------------------------------
+# full C2 size against the C/OpenMP oracle (bitwise-pinned Bellman backup);
+# the GPU box host has the RAM for the 26 GB instance
+# ----------------------------------------------------------------------------
+
+@pytest.mark.slow
+def test_c2_full_size_oracle_parity(c2_full):
+    import os
+    from oracle import c_oracle as co
+    mdp, spec = c2_full
+    rp, col, val = mdp.transitions.numpy()
+    cost = mdp.stage_cost.cpu().numpy()
+    nt = os.cpu_count()
+    # one Bellman backup at a seeded V
+    v = np.random.default_rng(5).random(mdp.n) * 10
+    g = ipi.greedy_policy(mdp, v)
+    pi, applied, res = co.greedy(rp, col, val, cost, spec.gamma, v, nthreads=nt)
+    np.testing.assert_allclose(g.applied, applied, rtol=1e-13, atol=1e-13)
+    diff = np.flatnonzero(g.policy != pi)
+    if diff.size:
+        pv = co.spmv(rp, col, val, v, nthreads=nt).reshape(mdp.n, mdp.m)
+        q = np.sort(cost[diff] + spec.gamma * pv[diff], axis=1)
+        assert np.all(q[:, 1] - q[:, 0] < TIE_GAP)
+    # the whole iPI solve
+    res_gpu = ipi.solve(mdp, ipi.SolveOptions(alpha=spec.alpha, tol=spec.atol))
+    ref = co.solve(rp, col, val, cost, spec.gamma, tol=spec.atol, alpha=spec.alpha, nthreads=nt)
+    assert res_gpu.status.value == ref.status == "converged"
+    assert abs(res_gpu.outer_iterations - ref.outer_iterations) <= 1
+    scale = max(1.0, np.abs(ref.values).max())
+    np.testing.assert_allclose(res_gpu.values, ref.values, rtol=1e-8, atol=1e-8 * scale)
+    diff = np.flatnonzero(res_gpu.policy != ref.policy)
+    if diff.size:
+        pv = co.spmv(rp, col, val, ref.values, nthreads=nt).reshape(mdp.n, mdp.m)
+        q = np.sort(cost[diff] + spec.gamma * pv[diff], axis=1)
+        assert np.all(q[:, 1] - q[:, 0] < TIE_GAP)
+    _, _, r = co.greedy(rp, col, val, cost, spec.gamma, res_gpu.values, nthreads=nt)
+    assert r <= spec.atol

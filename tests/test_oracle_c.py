@@ -1,0 +1,63 @@
+"""Pin the C/OpenMP oracle restatement: Bellman backup / SpMV bitwise equal to
+the reference's golden outputs (numpy reduceat pairwise order restated),
+solves to tolerance (BLAS dot order is not reproducible), generator equal to
+the Python recipe."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import golden_meta, golden_names, load_golden
+from oracle import c_oracle as co
+from paper_2507_22538_b200 import generators as gen
+
+NAMES = golden_names()
+
+
+@pytest.mark.parametrize("name", NAMES)
+@pytest.mark.parametrize("threads", [1, 4])
+def test_c_spmv_and_greedy_bitwise(name, threads):
+    g = load_golden(name)
+    y = co.spmv(g["row_ptr"], g["col"], g["val"], g["spmv_x"], nthreads=threads)
+    np.testing.assert_array_equal(y, g["spmv_y"])
+    pi, applied, res = co.greedy(g["row_ptr"], g["col"], g["val"], g["cost"], float(g["gamma"]),
+                                 g["greedy_v"], bool(g["maximize"]), nthreads=threads)
+    np.testing.assert_array_equal(pi, g["greedy_policy"])
+    np.testing.assert_array_equal(applied, g["greedy_applied"])
+    assert res == float(np.max(np.abs(g["greedy_v"] - g["greedy_applied"])))
+
+
+def _cases():
+    out = []
+    for name in NAMES:
+        for kind, s in golden_meta(name)["solves"].items():
+            if kind in ("gmres", "richardson") and s["inner"] <= 50_000:
+                out.append(pytest.param(name, kind, id=f"{name}-{kind}"))
+    return out
+
+
+@pytest.mark.parametrize("name,kind", _cases())
+def test_c_solve_matches_reference(name, kind):
+    g = load_golden(name)
+    s = golden_meta(name)["solves"][kind]
+    r = co.solve(g["row_ptr"], g["col"], g["val"], g["cost"], float(g["gamma"]),
+                 maximize=bool(g["maximize"]), kind=kind, tol=s["tol"], nthreads=2)
+    ref = g[f"solve_{kind}_values"]
+    assert r.status == s["status"]
+    assert r.outer_iterations == s["outer"]
+    np.testing.assert_allclose(r.values, ref, rtol=1e-10, atol=1e-10 * max(1, np.abs(ref).max()))
+    np.testing.assert_array_equal(r.policy, g[f"solve_{kind}_policy"])
+    if kind == "richardson":  # no dots inside: bitwise
+        np.testing.assert_array_equal(r.values, ref)
+
+
+def test_c_generator_equals_python_recipe():
+    a = gen.random_locality_host(300, 3, 16, 20, seed=4)
+    b = co.gen_locality(300, 3, 16, 20, seed=4, nthreads=3)
+    np.testing.assert_array_equal(a[0], b[0])
+    np.testing.assert_array_equal(a[1], b[1])
+    np.testing.assert_array_equal(a[3], b[3])
+    np.testing.assert_allclose(a[2], b[2], rtol=4e-16, atol=0)
+    part = co.gen_locality(300, 3, 16, 20, seed=4, state0=100, n_states=50)
+    np.testing.assert_array_equal(part[1], b[1][100 * 48:150 * 48])
