@@ -216,6 +216,87 @@ def _tighten(est, eff, rn, current):
     return min(current, est * (eff / rn) * 0.5)
 
 
+def _bicgstab(apply_a, b, theta0, eff, max_it):
+    """BiCGStab with estimate-then-verify stopping (inner.py:295-373), pc = identity."""
+    x = theta0.copy()
+    r_true = b - apply_a(x)
+    rn = norm2(r_true)
+    it = 0
+    breakdown = False
+    if rn <= eff:
+        return x, it, rn, breakdown
+    r = np.array(r_true, dtype=np.float64, copy=True)
+    rtilde = r.copy()
+    rtilde_norm = norm2(rtilde)
+    rho = dot(rtilde, r)
+    p = r.copy()
+    est = norm2(r)
+    est_target = eff
+    stale = False
+    while it < max_it:
+        if abs(rho) <= 1e-14 * rtilde_norm * est:
+            breakdown = True
+            break
+        v = apply_a(p)
+        sigma = dot(rtilde, v)
+        if abs(sigma) <= 1e-14 * rtilde_norm * norm2(v):
+            breakdown = True
+            break
+        alpha = rho / sigma
+        s = r - alpha * v
+        s_norm = norm2(s)
+        if s_norm <= est_target:
+            x = x + alpha * p
+            it += 1
+            r_true = b - apply_a(x)
+            rn = norm2(r_true)
+            stale = False
+            if rn <= eff:
+                break
+            est_target = _tighten(s_norm, eff, rn, est_target)
+            r = np.array(r_true, dtype=np.float64, copy=True)
+            rtilde = r.copy()
+            rtilde_norm = norm2(rtilde)
+            rho = dot(rtilde, r)
+            p = r.copy()
+            est = norm2(r)
+            continue
+        t = apply_a(s)
+        tt = dot(t, t)
+        if tt == 0.0:
+            breakdown = True
+            break
+        omega = dot(t, s) / tt
+        if omega == 0.0 or not math.isfinite(omega):
+            breakdown = True
+            break
+        x = x + alpha * p + omega * s
+        r = s - omega * t
+        it += 1
+        stale = True
+        est = norm2(r)
+        if est <= est_target:
+            r_true = b - apply_a(x)
+            rn = norm2(r_true)
+            stale = False
+            if rn <= eff:
+                break
+            if est == 0.0:
+                break
+            est_target = _tighten(est, eff, rn, est_target)
+        rho_new = dot(rtilde, r)
+        beta = (rho_new / rho) * (alpha / omega)
+        if not math.isfinite(beta):
+            breakdown = True
+            break
+        rho = rho_new
+        p = r + beta * (p - omega * v)
+    if stale or breakdown:
+        r_true = b - apply_a(x)
+        rn = norm2(r_true)
+    return x, it, rn, breakdown
+
+
 def _tfqmr(apply_a, b, theta0, eff, max_it):
     """Transpose-free QMR with estimate-then-verify stopping (inner.py:376-450)."""
     x = theta0.copy()
@@ -311,6 +392,8 @@ def inner_solve(rp_pi, col_pi, val_pi, gamma, b, theta0, target, max_it,
         theta, its, rn, broke = _gmres(apply_a, b, theta0, eff, max_it)
     elif kind == "tfqmr":
         theta, its, rn, broke = _tfqmr(apply_a, b, theta0, eff, max_it)
+    elif kind == "bicgstab":
+        theta, its, rn, broke = _bicgstab(apply_a, b, theta0, eff, max_it)
     else:
         raise ValueError(f"oracle has no inner solver {kind!r}")
     return theta, InnerReport(its, rn, bool(rn <= eff) and not broke, broke, eff)

@@ -384,6 +384,8 @@ int launch_bellman(ipi_mdp* h, const double* v_full, int32_t mode, int32_t* poli
                    double* applied, double* g_pi, int32_t* len_pi,
                    unsigned long long* res_bits, cudaStream_t st) {
   if (h->n_local == 0) return IPI_OK;
+  if (h->use_tma)
+    return launch_bellman_tma(h, v_full, mode, policy, applied, g_pi, len_pi, res_bits, st);
   K1Args a;
   a.rp = h->rp;
   a.col = h->col;

@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -353,6 +354,46 @@ int ipi_mdp_create(const int64_t* row_ptr, const int32_t* col, const double* val
   }
   p.inner_blocks = 0;
   p.inner_smem_bytes = 0;
+  int Gu = 0, Pu = 0;
+  p.k1_variant = (p.uniform_rows && uniform_shape(p.row_len_max, &Gu, &Pu)) ? 1 : 0;
+  // ---- TMA ring plan for uniform rows (one persistent CTA per SM) ------------
+  {
+    const char* env = getenv("IPI_K1_TMA");
+    const bool allow = !(env && env[0] == '0');
+    if (allow && p.k1_variant == 1 && n_local > 0) {
+      const int blocks = (int)std::min<int64_t>(h->num_sms, std::max<int64_t>(1, n_local / 64));
+      const int64_t per = (n_local + blocks - 1) / blocks;
+      int SC, NS, sup, wcap, stage, smem;
+      if (k1_tma_plan(per + 64, m, p.row_len_max, p.halo, n_global, &SC, &NS, &sup, &wcap, &stage,
+                      &smem)) {
+        std::vector<int64_t> hb(blocks + 1);
+        for (int c = 0; c <= blocks; ++c) {
+          int64_t b = (int64_t)((double)n_local * c / blocks);
+          b = (b / SC) * SC;
+          hb[c] = c == blocks ? n_local : std::min<int64_t>(b, n_local);
+        }
+        if (cudaMalloc(&h->tma_bounds, sizeof(int64_t) * (blocks + 1)) == cudaSuccess &&
+            cudaMemcpy(h->tma_bounds, hb.data(), sizeof(int64_t) * (blocks + 1),
+                       cudaMemcpyHostToDevice) == cudaSuccess) {
+          h->use_tma = 1;
+          h->tma_blocks = blocks;
+          h->tma_smem = smem;
+          h->tma_sc = SC;
+          h->tma_ns = NS;
+          h->tma_super = sup;
+          h->tma_wcap = wcap;
+          h->tma_stage = stage;
+          h->tma_halo = wcap > 0 ? p.halo : -1;
+          p.k1_variant = 2;
+          p.k1_tma_stages = NS;
+          p.k1_tma_chunk_states = SC;
+          p.k1_blocks = blocks;
+          p.k1_threads = (16 + 1) * 32;
+          p.k1_smem_bytes = smem;
+        }
+      }
+    }
+  }
   e = cudaGetLastError();
   if (e != cudaSuccess) return bail(fail(IPI_ECUDA, std::string("planning kernels: ") + cudaGetErrorString(e)));
   *out = h;
@@ -362,6 +403,7 @@ int ipi_mdp_create(const int64_t* row_ptr, const int32_t* col, const double* val
 void ipi_mdp_destroy(ipi_mdp* h) {
   if (!h) return;
   cudaFree(h->k1_bounds);
+  cudaFree(h->tma_bounds);
   cudaFree(h->pi);
   cudaFree(h->applied);
   cudaFree(h->gpi);
@@ -653,9 +695,23 @@ int ipi_solve(ipi_mdp* h, const ipi_opts* o, double* v, int32_t* policy, double*
                      o->ksp_type, o->richardson_scale, h->plan.lanes_per_row, h->plan.halo,
                      h->plan.uniform_rows ? h->plan.row_len_max : 0, h->d_report, st);
     if (rc) return rc;
+    if (o->ksp_type == IPI_KSP_TFQMR || o->ksp_type == IPI_KSP_BICGSTAB) {
+      // these kinds can break down: read the report now (driver.py:189-193)
+      IPI_CUDA_TRY(cudaMemcpyAsync(hrep, h->d_report, sizeof(ipi_inner_report), cudaMemcpyDeviceToHost, st));
+      IPI_CUDA_TRY(cudaStreamSynchronize(st));
+      inner_total += hrep->iterations;
+      if (hrep->breakdown) {
+        // one plain evaluation sweep from the pre-solve V: theta = g_pi + gamma * P_pi v
+        rc = launch_spmv(h->rp_pi, h->col_pi, h->val_pi, n, vcur, h->gpi, h->gamma, 3, vnext,
+                         h->plan.lanes_per_row, st);
+        if (rc) return rc;
+        inner_total += 1;
+      }
+    } else {
+      pending_report = true;
+    }
     cudaEventRecord(pi_.b, st);
     phases.push_back(pi_);
-    pending_report = true;
     std::swap(vcur, vnext);
     ++k;
   }

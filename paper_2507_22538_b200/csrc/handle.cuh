@@ -34,6 +34,12 @@ struct ipi_mdp {
   int64_t scan_tmp_len = 0;
   ipi_inner_report* d_report = nullptr;
   void* host_pinned = nullptr;  // small pinned staging area
+
+  // K1 TMA pipeline plan (bellman_tma.cu); use_tma = 0 -> register kernels
+  int use_tma = 0;
+  int64_t* tma_bounds = nullptr;
+  int tma_blocks = 0, tma_smem = 0, tma_sc = 0, tma_ns = 0, tma_super = 0, tma_wcap = 0,
+      tma_stage = 0, tma_halo = -1;
 };
 
 namespace ipi {
@@ -74,6 +80,13 @@ bool uniform_shape(int K, int* G, int* P);
 int launch_bellman(ipi_mdp* h, const double* v_full, int32_t mode, int32_t* policy,
                    double* applied, double* g_pi, int32_t* len_pi,
                    unsigned long long* res_bits, cudaStream_t st);
+
+// bellman_tma.cu
+bool k1_tma_plan(int64_t n_states_max_cta, int m, int K, int halo, int64_t n_global, int* SC,
+                 int* NS, int* super_states, int* win_cap, int* stage_bytes, int* smem_bytes);
+int launch_bellman_tma(ipi_mdp* h, const double* v_full, int32_t mode, int32_t* policy,
+                       double* applied, double* g_pi, int32_t* len_pi,
+                       unsigned long long* res_bits, cudaStream_t st);
 
 // policy.cu
 int gather_policy(ipi_mdp* h, const int32_t* policy, const int32_t* len_pi, int64_t* rp_pi,

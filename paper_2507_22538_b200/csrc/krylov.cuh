@@ -1,0 +1,656 @@
+// krylov.cuh — persistent policy-evaluation kernel shared by the krylov*.cu units.
+#pragma once
+// K4: policy evaluation (I - gamma P_pi) x = b as ONE persistent
+// cooperative kernel per inner solve (inner.py:163-292).
+//
+// Why persistent: GMRES(30) with modified Gram-Schmidt needs j+1 dependent
+// grid-wide reductions per Arnoldi step.  Launch-per-op would pay a kernel
+// launch plus a host round trip per dot (C1/C4 vectors are 80-160 KB, i.e.
+// microsecond kernels).  Here every CTA owns a contiguous, nnz-balanced slice
+// of rows/vector entries; reductions are two-level and deterministic (fixed
+// intra-CTA tree -> per-CTA partial -> every CTA sums all partials in the
+// same fixed order), so every CTA holds bit-identical scalars and runs the
+// reference's control logic (Givens, est_target tightening, caps) redundantly
+// without any broadcast.  Grid barriers are cooperative-groups grid syncs.
+//
+// Semantics mirrored exactly (inner.py line refs):
+//   eff = max(target, 1e-14*max(1,||b||))           :189
+//   Richardson: r=b-A th; stop if rn<=eff|it>=cap|!finite; th += scale*r   :216-226
+//   GMRES: restart 30, MGS, Givens, break on |g_j|<=est or hnorm==0,
+//          true residual per cycle, est_target = |g_j|*(eff/rn)*0.5       :229-283
+//   back substitution with zero-pivot -> 0                                 :286-292
+// Every vector op uses separate mul/add roundings like numpy (no FMA).
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <string>
+
+#include "handle.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace ipi {
+
+constexpr int R = kGmresRestart;
+
+struct KArgs {
+  const int64_t* rp;
+  const int32_t* col;
+  const double* val;
+  int64_t n;
+  double gamma;
+  const double* b;
+  double* x;
+  double* V;         // (R+1) * n Krylov basis
+  double* w;         // n
+  double* r;         // n
+  double* partials;  // [2 slots][grid][2]
+  double target;
+  int max_it;
+  int kind;
+  double scale;
+  int halo;
+  int win_cap;   // doubles of the shared-memory window (0 = none)
+  int own_cap;   // doubles of the shared-memory w slice (0 = w in global)
+  int K;         // uniform row length of P_pi (0 = variable)
+  ipi_inner_report* rep;
+};
+
+struct KShared {
+  double red[32];
+  double bc[4];
+  double H[(R + 1) * R];
+  double cs[R], sn[R], g[R + 1], y[R];
+  int iflag[4];
+};
+
+// Two-level deterministic all-reduce of NV doubles; result in every thread.
+template <int NV>
+__device__ __forceinline__ void grid_allreduce(double (&v)[NV], const KArgs& a, int& slot,
+                                               cg::grid_group& grid, KShared& sh) {
+  double t[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) t[k] = block_sum(v[k], sh.red);
+  const int nblk = gridDim.x;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) a.partials[((int64_t)slot * nblk + blockIdx.x) * 2 + k] = t[k];
+  }
+  grid.sync();
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      double s = 0.0;
+      for (int i = lane; i < nblk; i += 32) s = add_rn(s, a.partials[((int64_t)slot * nblk + i) * 2 + k]);
+      s = warp_sum(s);
+      if (lane == 0) sh.bc[k] = s;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v[k] = sh.bc[k];
+  slot ^= 1;
+  __syncthreads();
+}
+
+// Row sums of P_pi over this CTA's rows with an optional shared-memory window
+// of the input vector; epi(s, Px_s) is called by one lane per row.  P == 0:
+// generic rows (G lanes strided over the row, 4 loads in flight); P > 0:
+// uniform even-length rows, P 16-byte value pairs per lane, batches
+// software-pipelined across row groups (same scheme as K1's fast path).
+template <int G, int P, bool WIN, class Epi>
+__device__ __forceinline__ void spmv_rows(const KArgs& a, const double* xin, int64_t s_lo,
+                                          int64_t s_hi, double* win, uint64_t pol, Epi&& epi) {
+  int64_t w_lo = 0, w_len = 0;
+  if (WIN) {
+    int64_t lo = s_lo - a.halo, hi = s_hi + a.halo;
+    lo = lo < 0 ? 0 : lo;
+    hi = hi > a.n ? a.n : hi;
+    __syncthreads();
+    if (hi - lo <= a.win_cap) {
+      w_lo = lo;
+      w_len = hi - lo;
+      for (int64_t i = threadIdx.x; i < w_len; i += blockDim.x) win[i] = xin[lo + i];
+    }
+    __syncthreads();
+  }
+  auto gather = [&](int c) -> double {
+    if (WIN) {
+      const uint64_t off = (uint64_t)((int64_t)c - w_lo);
+      if (off < (uint64_t)w_len) return win[off];
+    }
+    return xin[c];
+  };
+  constexpr int GPW = 32 / G;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int grp = lane / G, gl = lane % G;
+  if constexpr (P == 0) {
+    for (int64_t base = s_lo + (int64_t)warp * GPW; base < s_hi; base += (int64_t)nwarps * GPW) {
+      const int64_t s = base + grp;
+      double acc = 0.0;
+      if (s < s_hi) {
+        const int64_t p0 = __ldg(a.rp + s), p1 = __ldg(a.rp + s + 1);
+        for (int64_t p = p0 + gl; p < p1; p += 4 * G) {
+          double vv[4];
+          int cc[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int64_t q = p + (int64_t)u * G;
+            if (q < p1) {
+              vv[u] = ld_stream(a.val + q, pol);
+              cc[u] = ld_stream(a.col + q, pol);
+            } else {
+              vv[u] = 0.0;
+              cc[u] = -1;
+            }
+          }
+          double xx[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) xx[u] = cc[u] >= 0 ? gather(cc[u]) : 0.0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (cc[u] >= 0) acc = add_rn(acc, mul_rn(vv[u], xx[u]));
+        }
+      }
+      acc = group_sum<G>(acc);
+      if (s < s_hi && gl == 0) epi(s, acc);
+    }
+  } else {
+    const int K = a.K, pairs = K >> 1;
+    auto load = [&](int64_t base, Batch<P>& b) {
+      const int64_t s = base + grp;
+#pragma unroll
+      for (int t = 0; t < P; ++t) {
+        const int j = gl + G * t;
+        if (s < s_hi && j < pairs) {
+          b.v[t] = ld_stream_v2(a.val + s * K + 2 * j, pol);
+          b.c[t] = ld_stream_v2(a.col + s * K + 2 * j, pol);
+        } else {
+          b.v[t] = make_double2(0.0, 0.0);
+          b.c[t] = make_int2(-1, -1);
+        }
+      }
+    };
+    int64_t base = s_lo + (int64_t)warp * GPW;
+    if (base < s_hi) {
+      Batch<P> cur, nxt;
+      load(base, cur);
+      while (true) {
+        const int64_t nb = base + (int64_t)nwarps * GPW;
+        const bool has_next = nb < s_hi;
+        if (has_next) load(nb, nxt);
+        double acc = 0.0;
+#pragma unroll
+        for (int t = 0; t < P; ++t) {
+          if (cur.c[t].x >= 0) {
+            const double x0 = gather(cur.c[t].x), x1 = gather(cur.c[t].y);
+            acc = add_rn(acc, mul_rn(cur.v[t].x, x0));
+            acc = add_rn(acc, mul_rn(cur.v[t].y, x1));
+          }
+        }
+        acc = group_sum<G>(acc);
+        const int64_t s = base + grp;
+        if (s < s_hi && gl == 0) epi(s, acc);
+        if (!has_next) break;
+        cur = nxt;
+        base = nb;
+      }
+    }
+  }
+}
+
+// KIND: 0 = GMRES + Richardson (runtime a.kind), 2 = BiCGStab, 3 = TFQMR.  Each
+// solver family is its own instantiation (and translation unit) so the hot
+// GMRES kernel does not carry the register pressure of the others.
+template <int G, int P, bool WIN, int KIND>
+__global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double win[];
+  __shared__ KShared sh;
+  const uint64_t pol = policy_evict_first();
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int nblk = gridDim.x;
+  const int64_t n = a.n;
+  const int64_t nnz = a.rp[n];
+  // nnz-balanced contiguous row slice (identical rule in every CTA)
+  const int64_t s_lo =
+      blockIdx.x == 0 ? 0 : lower_bound_i64(a.rp, n + 1, (nnz * (int64_t)blockIdx.x) / nblk);
+  const int64_t s_hi = blockIdx.x == nblk - 1
+                           ? n
+                           : lower_bound_i64(a.rp, n + 1, (nnz * (int64_t)(blockIdx.x + 1)) / nblk);
+  const double gam = a.gamma;
+  const double* b = a.b;
+  double* x = a.x;
+  double* r = a.r;
+  // this CTA's slice of w: shared memory when it fits, else its global rows
+  const bool w_shared = (s_hi - s_lo) <= a.own_cap;
+  double* wl = w_shared ? (win + a.win_cap) : (a.w + s_lo);
+  int slot = 0;
+
+  // ---- r = b - (x - gamma P x), ||b||, ||r|| --------------------------------
+  double acc2[2] = {0.0, 0.0};
+  for (int64_t i = s_lo + tid; i < s_hi; i += nthr) acc2[0] = add_rn(acc2[0], mul_rn(b[i], b[i]));
+  spmv_rows<G, P, WIN>(a, x, s_lo, s_hi, win, pol, [&](int64_t s, double px) {
+    const double ri = sub_rn(b[s], sub_rn(x[s], mul_rn(gam, px)));
+    r[s] = ri;
+    acc2[1] = add_rn(acc2[1], mul_rn(ri, ri));
+  });
+  grid_allreduce<2>(acc2, a, slot, grid, sh);
+  const double bnorm = sqrt(acc2[0]);
+  const double rr0 = acc2[1];
+  double rn = sqrt(rr0);
+  int brk = 0;
+  // true residual r = b - A x (x complete after a grid sync); returns ||r||
+  auto true_residual = [&]() -> double {
+    grid.sync();
+    double q[1] = {0.0};
+    spmv_rows<G, P, WIN>(a, x, s_lo, s_hi, win, pol, [&](int64_t s, double px) {
+      const double ri = sub_rn(b[s], sub_rn(x[s], mul_rn(gam, px)));
+      r[s] = ri;
+      q[0] = add_rn(q[0], mul_rn(ri, ri));
+    });
+    grid_allreduce<1>(q, a, slot, grid, sh);
+    return sqrt(q[0]);
+  };
+  const double eff = fmax(a.target, 1e-14 * fmax(1.0, bnorm));
+  int it = 0;
+
+  if constexpr (KIND == IPI_KSP_TFQMR) {
+    // ---- TFQMR (inner.py:376-450), pc = identity ------------------------------
+    double* r0 = a.V;
+    double* wv = a.V + n;
+    double* yv = a.V + 2 * n;
+    double* dv = a.V + 3 * n;
+    double* uv = a.V + 4 * n;
+    double* vv = a.V + 5 * n;
+    double* vt = a.V + 6 * n;
+    bool stale = false;
+    if (!(rn <= eff)) {
+      for (int64_t i = s_lo + tid; i < s_hi; i += nthr) {
+        const double ri = r[i];
+        r0[i] = ri;
+        wv[i] = ri;
+        yv[i] = ri;
+        dv[i] = 0.0;
+      }
+      grid.sync();
+      double p2[2] = {0.0, 0.0};
+      spmv_rows<G, P, WIN>(a, yv, s_lo, s_hi, win, pol, [&](int64_t s, double px) {
+        const double u = sub_rn(yv[s], mul_rn(gam, px));
+        uv[s] = u;
+        vv[s] = u;
+        p2[0] = add_rn(p2[0], mul_rn(r0[s], u));
+        p2[1] = add_rn(p2[1], mul_rn(u, u));
+      });
+      double tau = rn, thq = 0.0, eta = 0.0, rho = rr0, est_target = eff;
+      const double r0n = rn;
+      while (it < a.max_it) {
+        grid_allreduce<2>(p2, a, slot, grid, sh);
+        const double sigma = p2[0], vn = sqrt(p2[1]);
+        if (fabs(sigma) <= mul_rn(mul_rn(1e-14, r0n), vn)) { brk = 1; break; }
+        const double alpha = rho / sigma;
+        if (alpha == 0.0 || !isfinite(alpha)) { brk = 1; break; }
+        bool conv = false;
+        double pw[2] = {0.0, 0.0};
+        for (int half = 1; half <= 2; ++half) {
+          const double coef = mul_rn(mul_rn(thq, thq), eta) / alpha;
+          pw[0] = pw[1] = 0.0;
+          if (half == 1) {
+            for (int64_t i = s_lo + tid; i < s_hi; i += nthr) {
+              const double w = sub_rn(wv[i], mul_rn(alpha, uv[i]));
+              wv[i] = w;
+              dv[i] = add_rn(yv[i], mul_rn(coef, dv[i]));
+              pw[0] = add_rn(pw[0], mul_rn(w, w));
+            }
+          } else {
+            for (int64_t i = s_lo + tid; i < s_hi; i += nthr) yv[i] = sub_rn(yv[i], mul_rn(alpha, vv[i]));
+            grid.sync();
+            spmv_rows<G, P, WIN>(a, yv, s_lo, s_hi, win, pol, [&](int64_t s, double px) {
+              const double u = sub_rn(yv[s], mul_rn(gam, px));
+              uv[s] = u;
+              const double w = sub_rn(wv[s], mul_rn(alpha, u));
+              wv[s] = w;
+              dv[s] = add_rn(yv[s], mul_rn(coef, dv[s]));
+              pw[0] = add_rn(pw[0], mul_rn(w, w));
+              pw[1] = add_rn(pw[1], mul_rn(r0[s], w));
+            });
+          }
+          if (tau == 0.0) { brk = 1; break; }
+          if (half == 1) {
+            double q1[1] = {pw[0]};
+            grid_allreduce<1>(q1, a, slot, grid, sh);
+            pw[0] = q1[0];
+          } else {
+            grid_allreduce<2>(pw, a, slot, grid, sh);
+          }
+          thq = sqrt(pw[0]) / tau;
+          const double c = 1.0 / sqrt(add_rn(1.0, mul_rn(thq, thq)));
+          tau = mul_rn(mul_rn(tau, thq), c);
+          eta = mul_rn(mul_rn(c, c), alpha);
+          for (int64_t i = s_lo + tid; i < s_hi; i += nthr) x[i] = add_rn(x[i], mul_rn(eta, dv[i]));
+          stale = true;
+          const double est = mul_rn(tau, sqrt(add_rn(add_rn(mul_rn(2.0, (double)it), (double)half), 1.0)));
+          if (est <= est_target) {
+            rn = true_residual();
+            stale = false;
+            if (rn <= eff) { conv = true; break; }
+            if (est == 0.0) { brk = 1; break; }
+            est_target = fmin(est_target, mul_rn(mul_rn(est, eff / rn), 0.5));
+          }
+        }
+        ++it;
+        if (conv || brk) break;
+        const double rho_new = pw[1], wn = sqrt(pw[0]);
+        if (fabs(rho_new) <= mul_rn(mul_rn(1e-14, r0n), wn)) { brk = 1; break; }
+        const double beta = rho_new / rho;
+        rho = rho_new;
+        const double b2 = mul_rn(beta, beta);
+        for (int64_t i = s_lo + tid; i < s_hi; i += nthr) {
+          yv[i] = add_rn(wv[i], mul_rn(beta, yv[i]));
+          vt[i] = add_rn(mul_rn(beta, uv[i]), mul_rn(b2, vv[i]));
+        }
+        grid.sync();
+        p2[0] = p2[1] = 0.0;
+        spmv_rows<G, P, WIN>(a, yv, s_lo, s_hi, win, pol, [&](int64_t s, double px) {
+          const double u = sub_rn(yv[s], mul_rn(gam, px));
+          uv[s] = u;
+          const double v = add_rn(vt[s], u);
+          vv[s] = v;
+          p2[0] = add_rn(p2[0], mul_rn(r0[s], v));
+          p2[1] = add_rn(p2[1], mul_rn(v, v));
+        });
+      }
+      if (stale || brk) rn = true_residual();
+    }
+  } else if constexpr (KIND == IPI_KSP_BICGSTAB) {
+    // ---- BiCGStab (inner.py:295-373), pc = identity ---------------------------
+    double* rv = a.V;          // recurrence residual
+    double* rt = a.V + n;      // shadow residual
+    double* pv = a.V + 2 * n;
+    double* vv = a.V + 3 * n;
+    double* sv = a.V + 4 * n;
+    double* tv = a.V + 5 * n;
+    bool stale = false;
+    if (!(rn <= eff)) {
+      for (int64_t i = s_lo + tid; i < s_hi; i += nthr) {
+        const double ri = r[i];
+        rv[i] = ri;
+        rt[i] = ri;
+        pv[i] = ri;
+      }
+      double rtn = rn, rho = rr0, est = rn, est_target = eff;
+      while (it < a.max_it) {
+        if (fabs(rho) <= mul_rn(mul_rn(1e-14, rtn), est)) { brk = 1; break; }
+        grid.sync();
+        double p2[2] = {0.0, 0.0};
+        spmv_rows<G, P, WIN>(a, pv, s_lo, s_hi, win, pol, [&](int64_t s, double px) {
+          const double v = sub_rn(pv[s], mul_rn(gam, px));
+          vv[s] = v;
+          p2[0] = add_rn(p2[0], mul_rn(rt[s], v));
+          p2[1] = add_rn(p2[1], mul_rn(v, v));
+        });
+        grid_allreduce<2>(p2, a, slot, grid, sh);
+        const double sigma = p2[0];
+        if (fabs(sigma) <= mul_rn(mul_rn(1e-14, rtn), sqrt(p2[1]))) { brk = 1; break; }
+        const double alpha = rho / sigma;
+        double q1[1] = {0.0};
+        __syncthreads();
+        for (int64_t i = s_lo + tid; i < s_hi; i += nthr) {
+          const double sval = sub_rn(rv[i], mul_rn(alpha, vv[i]));
+          sv[i] = sval;
+          q1[0] = add_rn(q1[0], mul_rn(sval, sval));
+        }
+        grid_allreduce<1>(q1, a, slot, grid, sh);
+        const double s_norm = sqrt(q1[0]);
+        if (s_norm <= est_target) {
+          for (int64_t i = s_lo + tid; i < s_hi; i += nthr) x[i] = add_rn(x[i], mul_rn(alpha, pv[i]));
+          ++it;
+          grid.sync();
+          double q[1] = {0.0};
+          spmv_rows<G, P, WIN>(a, x, s_lo, s_hi, win, pol, [&](int64_t s, double px) {
+            const double ri = sub_rn(b[s], sub_rn(x[s], mul_rn(gam, px)));
+            r[s] = ri;
+            q[0] = add_rn(q[0], mul_rn(ri, ri));
+          });
+          grid_allreduce<1>(q, a, slot, grid, sh);
+          rn = sqrt(q[0]);
+          stale = false;
+          if (rn <= eff) break;
+          est_target = fmin(est_target, mul_rn(mul_rn(s_norm, eff / rn), 0.5));
+          for (int64_t i = s_lo + tid; i < s_hi; i += nthr) {
+            const double ri = r[i];
+            rv[i] = ri;
+            rt[i] = ri;
+            pv[i] = ri;
+          }
+          rtn = rn;
+          rho = q[0];
+          est = rn;
+          continue;
+        }
+        grid.sync();
+        double p3[2] = {0.0, 0.0};
+        spmv_rows<G, P, WIN>(a, sv, s_lo, s_hi, win, pol, [&](int64_t s, double px) {
+          const double t = sub_rn(sv[s], mul_rn(gam, px));
+          tv[s] = t;
+          p3[0] = add_rn(p3[0], mul_rn(t, t));
+          p3[1] = add_rn(p3[1], mul_rn(t, sv[s]));
+        });
+        grid_allreduce<2>(p3, a, slot, grid, sh);
+        const double tt = p3[0];
+        if (tt == 0.0) { brk = 1; break; }
+        const double omega = p3[1] / tt;
+        if (omega == 0.0 || !isfinite(omega)) { brk = 1; break; }
+        double p4[2] = {0.0, 0.0};
+        for (int64_t i = s_lo + tid; i < s_hi; i += nthr) {
+          x[i] = add_rn(add_rn(x[i], mul_rn(alpha, pv[i])), mul_rn(omega, sv[i]));
+          const double rnew = sub_rn(sv[i], mul_rn(omega, tv[i]));
+          rv[i] = rnew;
+          p4[0] = add_rn(p4[0], mul_rn(rnew, rnew));
+          p4[1] = add_rn(p4[1], mul_rn(rt[i], rnew));
+        }
+        ++it;
+        stale = true;
+        grid_allreduce<2>(p4, a, slot, grid, sh);
+        est = sqrt(p4[0]);
+        if (est <= est_target) {
+          rn = true_residual();
+          stale = false;
+          if (rn <= eff) break;
+          if (est == 0.0) break;
+          est_target = fmin(est_target, mul_rn(mul_rn(est, eff / rn), 0.5));
+        }
+        const double rho_new = p4[1];
+        const double beta = mul_rn(rho_new / rho, alpha / omega);
+        if (!isfinite(beta)) { brk = 1; break; }
+        rho = rho_new;
+        for (int64_t i = s_lo + tid; i < s_hi; i += nthr)
+          pv[i] = add_rn(rv[i], mul_rn(beta, sub_rn(pv[i], mul_rn(omega, vv[i]))));
+      }
+      if (stale || brk) rn = true_residual();
+    }
+  } else   if (a.kind == IPI_KSP_RICHARDSON) {
+    while (true) {
+      if (rn <= eff || it >= a.max_it || !isfinite(rn)) break;
+      for (int64_t i = s_lo + tid; i < s_hi; i += nthr) x[i] = add_rn(x[i], mul_rn(a.scale, r[i]));
+      ++it;
+      grid.sync();
+      double acc1[1] = {0.0};
+      spmv_rows<G, P, WIN>(a, x, s_lo, s_hi, win, pol, [&](int64_t s, double px) {
+        const double ri = sub_rn(b[s], sub_rn(x[s], mul_rn(gam, px)));
+        r[s] = ri;
+        acc1[0] = add_rn(acc1[0], mul_rn(ri, ri));
+      });
+      grid_allreduce<1>(acc1, a, slot, grid, sh);
+      rn = sqrt(acc1[0]);
+    }
+  } else {  // GMRES(30)
+    double est_target = eff;
+    while (rn > eff && it < a.max_it) {
+      const double beta = rn;  // ||pc(r)|| with pc = identity: same vector, same reduction
+      if (beta == 0.0 || !isfinite(beta)) break;
+      for (int64_t i = s_lo + tid; i < s_hi; i += nthr) a.V[i] = r[i] / beta;
+      if (tid == 0) {
+        for (int k = 0; k < (R + 1) * R; ++k) sh.H[k] = 0.0;
+        for (int k = 0; k < R; ++k) sh.cs[k] = sh.sn[k] = 0.0;
+        for (int k = 0; k <= R; ++k) sh.g[k] = 0.0;
+        sh.g[0] = beta;
+      }
+      int j = 0;
+      grid.sync();
+      while (j < R && it < a.max_it) {
+        const double* Vj = a.V + (int64_t)j * n;
+        const double* V0 = a.V;
+        double p[1] = {0.0};
+        spmv_rows<G, P, WIN>(a, Vj, s_lo, s_hi, win, pol, [&](int64_t s, double px) {
+          const double wi = sub_rn(Vj[s], mul_rn(gam, px));
+          wl[s - s_lo] = wi;
+          p[0] = add_rn(p[0], mul_rn(V0[s], wi));
+        });
+        ++it;
+        __syncthreads();  // w rows written by group leaders, read per-thread below
+        for (int l = 0; l <= j; ++l) {
+          grid_allreduce<1>(p, a, slot, grid, sh);
+          const double hlj = p[0];
+          if (tid == 0) sh.H[l * R + j] = hlj;
+          const double* Vl = a.V + (int64_t)l * n;
+          const double* Vn = a.V + (int64_t)(l + 1) * n;
+          double q = 0.0;
+          if (l < j) {
+            for (int64_t i = s_lo + tid; i < s_hi; i += nthr) {
+              const double wi = sub_rn(wl[i - s_lo], mul_rn(hlj, Vl[i]));
+              wl[i - s_lo] = wi;
+              q = add_rn(q, mul_rn(Vn[i], wi));
+            }
+          } else {
+            for (int64_t i = s_lo + tid; i < s_hi; i += nthr) {
+              const double wi = sub_rn(wl[i - s_lo], mul_rn(hlj, Vl[i]));
+              wl[i - s_lo] = wi;
+              q = add_rn(q, mul_rn(wi, wi));
+            }
+          }
+          p[0] = q;
+        }
+        grid_allreduce<1>(p, a, slot, grid, sh);
+        const double hnorm = sqrt(p[0]);
+        if (tid == 0) {
+          double* H = sh.H;
+          H[(j + 1) * R + j] = hnorm;
+          for (int l = 0; l < j; ++l) {
+            const double hl = H[l * R + j], hl1 = H[(l + 1) * R + j];
+            const double t = add_rn(mul_rn(sh.cs[l], hl), mul_rn(sh.sn[l], hl1));
+            H[(l + 1) * R + j] = add_rn(mul_rn(-sh.sn[l], hl), mul_rn(sh.cs[l], hl1));
+            H[l * R + j] = t;
+          }
+          const double denom = hypot(H[j * R + j], H[(j + 1) * R + j]);
+          int brk = 0;
+          if (denom == 0.0) {
+            brk = 1;
+          } else {
+            sh.cs[j] = H[j * R + j] / denom;
+            sh.sn[j] = H[(j + 1) * R + j] / denom;
+            H[j * R + j] = denom;
+            H[(j + 1) * R + j] = 0.0;
+            sh.g[j + 1] = mul_rn(-sh.sn[j], sh.g[j]);
+            sh.g[j] = mul_rn(sh.cs[j], sh.g[j]);
+            if (fabs(sh.g[j + 1]) <= est_target || hnorm == 0.0) brk = 2;
+          }
+          sh.iflag[0] = brk;
+        }
+        __syncthreads();
+        const int brk = sh.iflag[0];
+        if (brk == 1) break;  // denom == 0: j not advanced
+        ++j;
+        if (brk == 2) break;  // estimated convergence / invariant subspace
+        double* Vnew = a.V + (int64_t)j * n;
+        for (int64_t i = s_lo + tid; i < s_hi; i += nthr) Vnew[i] = wl[i - s_lo] / hnorm;
+        grid.sync();
+      }
+      if (j == 0) break;
+      if (tid == 0) {  // back substitution (inner.py:286-292)
+        for (int i = j - 1; i >= 0; --i) {
+          double dacc = 0.0;
+          for (int k = i + 1; k < j; ++k) dacc = add_rn(dacc, mul_rn(sh.H[i * R + k], sh.y[k]));
+          const double t = sub_rn(sh.g[i], dacc);
+          const double d = sh.H[i * R + i];
+          sh.y[i] = d != 0.0 ? t / d : 0.0;
+        }
+      }
+      __syncthreads();
+      for (int64_t i = s_lo + tid; i < s_hi; i += nthr) {
+        double t = 0.0;
+        for (int l = 0; l < j; ++l) t = add_rn(t, mul_rn(a.V[(int64_t)l * n + i], sh.y[l]));
+        x[i] = add_rn(x[i], t);
+      }
+      grid.sync();
+      double acc1[1] = {0.0};
+      spmv_rows<G, P, WIN>(a, x, s_lo, s_hi, win, pol, [&](int64_t s, double px) {
+        const double ri = sub_rn(b[s], sub_rn(x[s], mul_rn(gam, px)));
+        r[s] = ri;
+        acc1[0] = add_rn(acc1[0], mul_rn(ri, ri));
+      });
+      grid_allreduce<1>(acc1, a, slot, grid, sh);
+      rn = sqrt(acc1[0]);
+      const double gj = fabs(sh.g[j]);
+      if (rn > eff && gj <= est_target) {
+        if (gj == 0.0) break;
+        est_target = mul_rn(mul_rn(gj, eff / rn), 0.5);
+      }
+    }
+  }
+  if (blockIdx.x == 0 && tid == 0) {
+    a.rep->iterations = it;
+    a.rep->final_linear_residual_2norm = rn;
+    a.rep->converged = (rn <= eff && !brk) ? 1 : 0;
+    a.rep->breakdown = brk;
+    a.rep->target_2norm = eff;
+  }
+}
+
+template <int G, int P, bool WIN, int KIND>
+static int launch_inner_t(KArgs& a, int smem, int blocks, cudaStream_t st) {
+  auto fn = inner_kernel<G, P, WIN, KIND>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return fail(IPI_ECUDA, std::string("inner smem attr: ") + cudaGetErrorString(e));
+  int per_sm = 0;
+  IPI_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kInnerThreads, smem));
+  if (per_sm < 1) return fail(IPI_ECUDA, "inner kernel cannot be resident (smem/regs)");
+  void* args[] = {(void*)&a};
+  IPI_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)fn, dim3(blocks), dim3(kInnerThreads), args,
+                                           (size_t)smem, st));
+  return IPI_OK;
+}
+
+// Launch the KIND family for the planned shape (uniform (G, P) or generic lanes).
+template <int KIND>
+static int dispatch_inner(KArgs& a, int G, int P, int lanes, bool win, int smem, int blocks,
+                          cudaStream_t st) {
+  int rc = IPI_OK;
+#define IPI_INNER_LAUNCH(GG, PP)                                                    \
+  rc = win ? launch_inner_t<GG, PP, true, KIND>(a, smem, blocks, st)                \
+           : launch_inner_t<GG, PP, false, KIND>(a, smem, blocks, st)
+  if (P > 0) {
+    IPI_DISPATCH_UNIFORM(G, P, IPI_INNER_LAUNCH);
+    return rc;
+  }
+  switch (lanes) {
+    case 1: IPI_INNER_LAUNCH(1, 0); break;
+    case 2: IPI_INNER_LAUNCH(2, 0); break;
+    case 4: IPI_INNER_LAUNCH(4, 0); break;
+    case 8: IPI_INNER_LAUNCH(8, 0); break;
+    case 16: IPI_INNER_LAUNCH(16, 0); break;
+    default: IPI_INNER_LAUNCH(32, 0); break;
+  }
+#undef IPI_INNER_LAUNCH
+  return rc;
+}
+
+int dispatch_inner_gmres(KArgs& a, int G, int P, int lanes, bool win, int smem, int blocks,
+                         cudaStream_t st);
+int dispatch_inner_bicgstab(KArgs& a, int G, int P, int lanes, bool win, int smem, int blocks,
+                            cudaStream_t st);
+int dispatch_inner_tfqmr(KArgs& a, int G, int P, int lanes, bool win, int smem, int blocks,
+                         cudaStream_t st);
+
+}  // namespace ipi

@@ -3,7 +3,8 @@
 // G lanes per CSR row (G chosen from the mean row length), 32/G rows per
 // warp step, grid-stride over row groups; 4 loads in flight per lane.
 // Epilogues: 0: y = A x;  1: y = x - gamma*(A x) (PolicyOperator.apply, exact
-// two-step rounding);  2: y = b - (x - gamma*(A x)) (inner.py:220/232/276).
+// two-step rounding);  2: y = b - (x - gamma*(A x)) (inner.py:220/232/276);
+// 3: y = b + gamma*(A x) (breakdown sweep g_pi + gamma*P_pi v, driver.py:190-193).
 // Used by the Python API mirror (spmv / PolicyOperator.apply) and tests; the
 // inner solver has its own fused copy of this loop inside the persistent
 // kernel (krylov.cu).
@@ -55,6 +56,8 @@ __global__ void __launch_bounds__(256) spmv_kernel(const int64_t* __restrict__ r
     if (r < rows && gl == 0) {
       if (EPI == 0) {
         y[r] = acc;
+      } else if (EPI == 3) {
+        y[r] = add_rn(__ldg(b + r), mul_rn(gamma, acc));
       } else {
         const double ax = sub_rn(__ldg(x + r), mul_rn(gamma, acc));
         y[r] = EPI == 1 ? ax : sub_rn(__ldg(b + r), ax);
@@ -71,8 +74,10 @@ static void launch_spmv_g(const int64_t* rp, const int32_t* col, const double* v
     spmv_kernel<G, 0><<<blocks, 256, 0, st>>>(rp, col, val, rows, x, b, gamma, y);
   else if (epi == 1)
     spmv_kernel<G, 1><<<blocks, 256, 0, st>>>(rp, col, val, rows, x, b, gamma, y);
-  else
+  else if (epi == 2)
     spmv_kernel<G, 2><<<blocks, 256, 0, st>>>(rp, col, val, rows, x, b, gamma, y);
+  else
+    spmv_kernel<G, 3><<<blocks, 256, 0, st>>>(rp, col, val, rows, x, b, gamma, y);
 }
 
 int launch_spmv(const int64_t* rp, const int32_t* col, const double* val, int64_t rows,

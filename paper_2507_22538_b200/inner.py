@@ -1,8 +1,9 @@
 """Policy-evaluation Krylov solves on the device (mirrors ``mdpsolve.inner``).
 
-``inner_solve`` (inner.py:163-213) runs the whole solve — Richardson or
-restarted GMRES(30) with MGS, Givens and estimate-then-verify stopping — as
-one persistent cooperative kernel (krylov.cu).  Preconditioning is NONE on
+``inner_solve`` (inner.py:163-213) runs the whole solve — Richardson,
+restarted GMRES(30) with MGS/Givens, BiCGStab or TFQMR, each with the
+reference's estimate-then-verify stopping and breakdown reporting — as one
+persistent cooperative kernel (krylov*.cu).  Preconditioning is NONE on
 the device path (every BASELINE config uses none); the other reference
 preconditioners are listed in DESIGN.md as out of scope for this round.
 """
@@ -61,7 +62,8 @@ class Preconditioner(enum.Enum):
             raise ValueError(f"unknown preconditioner {name!r}; supported: {valid}") from None
 
 
-DEVICE_KINDS = (InnerSolver.RICHARDSON, InnerSolver.GMRES)
+DEVICE_KINDS = (InnerSolver.RICHARDSON, InnerSolver.GMRES, InnerSolver.BICGSTAB,
+                InnerSolver.TFQMR)
 
 
 @dataclass(frozen=True)

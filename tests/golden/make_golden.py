@@ -99,7 +99,7 @@ def record(name, inst, *, kinds=("gmres",), opts=None, seed=7, exact=True, tol=1
     out["gather_cost"] = ref.gather_policy_cost(inst, g.policy)
     op = ref.PolicyOperator(p_pi, inst.gamma)
     out["apply_y"] = op.apply(x)
-    for kind in ("gmres", "richardson"):
+    for kind in ("gmres", "richardson", "tfqmr", "bicgstab"):
         target = 1e-3 * float(np.max(np.abs(v - g.applied)))
         theta, rep = ref.inner_solve(op, out["gather_cost"], v, target, 200,
                                      kind=ref.InnerSolver.from_name(kind))
@@ -107,7 +107,8 @@ def record(name, inst, *, kinds=("gmres",), opts=None, seed=7, exact=True, tol=1
         out[f"inner_{kind}_target"] = np.float64(target)
         meta[f"inner_{kind}"] = {"iterations": rep.iterations,
                                  "final": rep.final_linear_residual_2norm,
-                                 "converged": rep.converged, "eff": rep.target_2norm}
+                                 "converged": rep.converged, "eff": rep.target_2norm,
+                                 "breakdown": rep.breakdown}
     for kind in kinds:
         so = ref.SolveOptions(inner=ref.InnerSolver.from_name(kind), tol=tol, **opts)
         res = ref.solve(inst, so)
@@ -138,7 +139,7 @@ def main():
     # --- reference fixtures -------------------------------------------------
     fixture = ref.gen_random(RandomParams(n=20, m=4, nnz_per_row=6, gamma=0.9, seed=123))
     metas.append(record("ref_fixture_random", fixture,
-                        kinds=("gmres", "richardson", "tfqmr")))
+                        kinds=("gmres", "richardson", "tfqmr", "bicgstab")))
     rp, col, val, cost = _arrays(fixture)
     metas.append(record("ref_fixture_random_max", _instance(rp, col, val, cost, 0.9, "max"),
                         kinds=("gmres", "richardson")))
@@ -151,7 +152,8 @@ def main():
     rows = p.reshape(15, 5)
     dense = _instance(np.arange(16, dtype=np.int64) * 5, np.tile(np.arange(5), 15),
                       rows.ravel(), gcost, 0.9)
-    metas.append(record("ref_dense5x3", dense, kinds=("gmres", "richardson", "tfqmr"), tol=1e-9))
+    metas.append(record("ref_dense5x3", dense, kinds=("gmres", "richardson", "tfqmr", "bicgstab"),
+                        tol=1e-9))
     np.save(HERE / "ref_dense5x3_optimum.npy", brute_force_optimum(dense))
     metas.append(record("ref_toy", _instance(np.array([0, 1]), np.array([0]), np.array([1.0]),
                                              np.array([[1.0]]), 0.5),
@@ -160,7 +162,7 @@ def main():
                    np.zeros((5, 3)), 0.9)
     metas.append(record("ref_zero_cost", zc, kinds=("gmres",)))
     metas.append(record("ref_sis12", ref.gen_sis(SisParams(population=12)),
-                        kinds=("gmres", "tfqmr")))
+                        kinds=("gmres", "tfqmr", "bicgstab")))
     metas.append(record("ref_pendulum9", ref.gen_pendulum(PendulumParams(grid_points=9,
                                                                          torque_points=5)),
                         kinds=("gmres", "tfqmr")))
@@ -171,14 +173,15 @@ def main():
                             kinds=("gmres", "richardson")))
     # --- scaled BASELINE-config instances (our generators, reference solve) --
     c1 = gen.random_dirichlet(100, 10, 25, seed=0)
-    metas.append(record("cfg1_dirichlet_n100", _instance(*c1, 0.99), kinds=("gmres",)))
+    metas.append(record("cfg1_dirichlet_n100", _instance(*c1, 0.99),
+                        kinds=("gmres", "richardson", "tfqmr", "bicgstab")))
     c2 = gen.random_locality_host(256, 8, 16, 16, seed=0)
     metas.append(record("cfg2_locality_n256", _instance(*c2, 0.999), kinds=("gmres",)))
     c3 = gen.pendulum_host(12, 21)
     metas.append(record("cfg3_pendulum_g12", _instance(*c3, 0.9999),
                         kinds=("gmres", "tfqmr")))
     c4 = gen.sis_host(60)
-    metas.append(record("cfg4_sis_n60", _instance(*c4, 0.9999), kinds=("gmres",)))
+    metas.append(record("cfg4_sis_n60", _instance(*c4, 0.9999), kinds=("gmres", "tfqmr", "bicgstab")))
     c2max = _instance(*c2, 0.999, "max")
     metas.append(record("cfg2_locality_n256_max", c2max, kinds=("gmres",)))
     (HERE / "golden_index.json").write_text(json.dumps(metas, indent=1) + "\n")

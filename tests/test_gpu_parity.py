@@ -81,7 +81,7 @@ def test_gather_and_apply_match_reference(name):
 
 
 @pytest.mark.parametrize("name", NAMES)
-@pytest.mark.parametrize("kind", ["gmres", "richardson"])
+@pytest.mark.parametrize("kind", ["gmres", "richardson", "tfqmr", "bicgstab"])
 def test_inner_solve_matches_reference(name, kind):
     g = load_golden(name)
     meta = golden_meta(name)[f"inner_{kind}"]
@@ -93,6 +93,7 @@ def test_inner_solve_matches_reference(name, kind):
                                  kind=ipi.InnerSolver.from_name(kind))
     assert rep.target_2norm == pytest.approx(meta["eff"], rel=1e-12)
     assert rep.converged == meta["converged"]
+    assert rep.breakdown == meta.get("breakdown", False)
     if meta["converged"]:
         assert rep.final_linear_residual_2norm <= rep.target_2norm
         # both iterates satisfy ||b - A x||_2 <= eff  =>  |x - x'| <= 2 eff / (1 - gamma)
@@ -109,7 +110,7 @@ def _solve_cases():
     out = []
     for name in NAMES:
         for kind, s in golden_meta(name)["solves"].items():
-            if kind not in ("gmres", "richardson") or s["inner"] > 50_000:
+            if s["inner"] > 50_000:
                 continue
             out.append(pytest.param(name, kind, id=f"{name}-{kind}"))
     return out
@@ -136,7 +137,9 @@ def test_solve_matches_reference(name, kind):
     # res_k) by about alpha * res_{k-1}.  Entries far above the noise floor must agree to
     # 1e-6 relative plus that one-alpha-step slack; the tail only needs <= tol.  The final
     # V is asserted at 1e-8 above.
-    alpha = 1e-4
+    # (BiCGStab/TFQMR stop on a cheap estimate and may overshoot the target by a wide
+    # margin, so their iterates are pinned an order of magnitude more loosely.)
+    alpha = 1e-4 * (10.0 if kind in ("bicgstab", "tfqmr") else 1.0)
     slack = np.concatenate(([0.0], alpha * ref_h[:-1]))
     big = ref_h > 1e-10
     err = np.abs(hist - ref_h)

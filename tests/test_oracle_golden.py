@@ -35,7 +35,7 @@ def test_spmv_greedy_gather_apply_bitwise(name):
 
 
 @pytest.mark.parametrize("name", NAMES)
-@pytest.mark.parametrize("kind", ["gmres", "richardson"])
+@pytest.mark.parametrize("kind", ["gmres", "richardson", "tfqmr", "bicgstab"])
 def test_inner_solve_bitwise(name, kind):
     g = load_golden(name)
     meta = golden_meta(name)[f"inner_{kind}"]
