@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k1_bellman_tma(K1TmaArgs a) {
   p += (size_t)a.win_cap * 8;
   unsigned char* stages = p;
   p += (size_t)NS * a.stage_bytes;
-  double* qbuf = reinterpret_cast<double*>(p);               // 2 x SC*m doubles
+  double* qbuf = reinterpret_cast<double*>(p);               // (NS+2) x SC*m doubles + counters
   __shared__ double red[32];
   const uint32_t win_s = smem_u32(win);
   const uint32_t stages_s = smem_u32(stages);
@@ -145,9 +145,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k1_bellman_tma(K1TmaArgs a) {
   if (warp == kTmaConsumers) {
     // ======================= producer warp ===================================
     if (lane == 0) {
+      int st = 0;
+      uint32_t eparity = 0;  // parity of the empty-barrier phase to wait for
       for (int64_t c = 0; c < nchunks; ++c) {
-        const int st = (int)(c % NS);
-        if (c >= NS) mbar_wait(bar_empty + 8u * st, (uint32_t)(((c / NS) - 1) & 1));
+        if (c >= NS) mbar_wait(bar_empty + 8u * st, eparity);
         const int64_t s0 = s_lo + c * SC;
         const int ns = (int)((s_hi - s0) < SC ? (s_hi - s0) : SC);
         const int rows = ns * m;
@@ -165,17 +166,31 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k1_bellman_tma(K1TmaArgs a) {
         } else {
           mbar_arrive(bar);  // tail chunk: consumers read it from global memory
         }
+        if (++st == NS) {
+          st = 0;
+          if (c >= NS - 1) eparity ^= (c >= NS) ? 1u : 0u;
+        }
       }
     }
     return;
   }
 
   // ========================= consumers =======================================
+  // Warps drift independently through the chunk stream (no per-chunk CTA
+  // barrier): each warp computes its rows of a chunk into q, releases the stage,
+  // and bumps the chunk's arrival counter; the LAST warp to arrive performs the
+  // per-state argmin.  Two chunks are in flight per warp (their loads and
+  // gathers are issued before either is reduced) to overlap the L2 latency of
+  // out-of-window gathers.  Warps can drift by at most NS chunks (the producer
+  // refills a stage only after all 16 warps released it), so NS+2 q buffers
+  // suffice.
   constexpr int GPW = 32 / G;
   const int grp = lane / G, gl = lane % G;
   const int pairs = K >> 1;
   const bool mx = a.maximize != 0;
   const double gamma = a.gamma;
+  const int QB = NS + 2;
+  int* cnt = reinterpret_cast<int*>(qbuf + (size_t)QB * rows_c);   // QB counters
   int w_lo = 0;
   uint32_t w_len = 0;
   double res = 0.0;
@@ -188,62 +203,35 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k1_bellman_tma(K1TmaArgs a) {
     return __ldg(a.v + c);
   };
 
-  for (int64_t c = 0; c < nchunks; ++c) {
-    const int st = (int)(c % NS);
-    const int64_t s0 = s_lo + c * SC;
-    const int ns = (int)((s_hi - s0) < SC ? (s_hi - s0) : SC);
-    const int rows = ns * m;
-    // super-chunk boundary: reload the V window (consumers only)
-    if (WIN && (c * SC) % a.super_states == 0) {
-      consumer_sync();  // nobody still gathers from the old window
-      int64_t lo = a.state0 + s0 - a.halo;
-      int64_t send = s0 + a.super_states;
-      if (send > s_hi) send = s_hi;
-      int64_t hi = a.state0 + send + a.halo;
-      lo = lo < 0 ? 0 : lo;
-      hi = hi > a.n_global ? a.n_global : hi;
-      w_lo = (int)lo;
-      w_len = (uint32_t)(hi - lo);
-      for (uint32_t i = tid; i < w_len; i += kTmaConsumers * 32) win[i] = __ldg(a.v + lo + i);
-      consumer_sync();
-    }
-    mbar_wait(bar_full + 8u * st, (uint32_t)((c / NS) & 1));
-    const uint32_t vb = (uint32_t)rows * K * 8, cb = (uint32_t)rows * K * 4, gb = (uint32_t)rows * 8;
-    const bool in_smem = (vb % 16 == 0) && (cb % 16 == 0) && (gb % 16 == 0);
-    const uint32_t sv = stages_s + (uint32_t)st * a.stage_bytes;
-    const uint32_t sc = sv + val_bytes_c, sg = sc + col_bytes_c;
-    const int64_t row0 = s0 * m;
-    double* q = qbuf + (size_t)(c & 1) * rows_c;
-    // ---- rows: q = cost + gamma * (P V) ------------------------------------
-    for (int rb = warp * GPW; rb < rows; rb += kTmaConsumers * GPW) {
-      const int r = rb + grp;
-      double acc = 0.0;
-      if (r < rows) {
-        for (int j = gl; j < pairs; j += G) {
-          double2 v2;
-          int2 c2;
-          const int e = r * K + 2 * j;
-          if (in_smem) {
-            v2 = lds_v2f64(sv + (uint32_t)e * 8u);
-            c2 = lds_v2s32(sc + (uint32_t)e * 4u);
-          } else {
-            v2 = *reinterpret_cast<const double2*>(a.val + row0 * K + e);
-            c2 = *reinterpret_cast<const int2*>(a.col + row0 * K + e);
-          }
-          acc = add_rn(acc, mul_rn(v2.x, gather(c2.x)));
-          acc = add_rn(acc, mul_rn(v2.y, gather(c2.y)));
+  // Row sums of one row-group pass of a chunk (rows rb.. of chunk at s0);
+  // returns the lane's partial (before the group reduction).
+  auto row_partial = [&](int r, int rows, bool in_smem, uint32_t sv, uint32_t sc_,
+                         int64_t row0) -> double {
+    double acc = 0.0;
+    if (r < rows) {
+#pragma unroll 2
+      for (int j = gl; j < pairs; j += G) {
+        double2 v2;
+        int2 c2;
+        const int e = r * K + 2 * j;
+        if (in_smem) {
+          v2 = lds_v2f64(sv + (uint32_t)e * 8u);
+          c2 = lds_v2s32(sc_ + (uint32_t)e * 4u);
+        } else {
+          v2 = *reinterpret_cast<const double2*>(a.val + row0 * K + e);
+          c2 = *reinterpret_cast<const int2*>(a.col + row0 * K + e);
         }
-      }
-      acc = group_sum<G>(acc);
-      if (r < rows && gl == 0) {
-        const double g = in_smem ? lds_f64(sg + (uint32_t)r * 8u) : __ldg(a.cost + row0 + r);
-        q[r] = add_rn(g, mul_rn(gamma, acc));
+        const double x0 = gather(c2.x), x1 = gather(c2.y);
+        acc = add_rn(acc, mul_rn(v2.x, x0));
+        acc = add_rn(acc, mul_rn(v2.y, x1));
       }
     }
-    consumer_sync();  // all rows of the chunk are in q; the stage is free
-    if (lane == 0) mbar_arrive(bar_empty + 8u * st);
-    // ---- per-state first-index argmin (warp per state) ---------------------
-    for (int t = warp; t < ns; t += kTmaConsumers) {
+    return acc;
+  };
+
+  auto finish_chunk = [&](int64_t c, int64_t s0, int ns, double* q) {
+    // caller: q of all rows visible (last arriver)
+    for (int t = 0; t < ns; ++t) {
       double bq = mx ? -INFINITY : INFINITY;
       int ba = INT_MAX;
       for (int a0 = lane; a0 < m; a0 += 32) {
@@ -273,6 +261,105 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k1_bellman_tma(K1TmaArgs a) {
         res = fmax(res, fabs(sub_rn(vs, bq)));
       }
     }
+    (void)c;
+  };
+
+  for (int i = tid; i < QB; i += kTmaConsumers * 32) cnt[i] = 0;
+  consumer_sync();
+
+  int st = 0;             // stage of chunk c
+  uint32_t parity = 0;    // full-barrier parity of chunk c
+  int qb = 0;             // q buffer of chunk c
+  int64_t next_reload = 0;
+  for (int64_t c = 0; c < nchunks; c += 2) {
+    const int64_t s0 = s_lo + c * SC;
+    // super-chunk boundary: reload the V window (consumers only; rare)
+    if (WIN && c * SC >= next_reload) {
+      consumer_sync();
+      int64_t lo = a.state0 + s0 - a.halo;
+      int64_t send = s0 + a.super_states;
+      if (send > s_hi) send = s_hi;
+      int64_t hi = a.state0 + send + a.halo;
+      lo = lo < 0 ? 0 : lo;
+      hi = hi > a.n_global ? a.n_global : hi;
+      w_lo = (int)lo;
+      w_len = (uint32_t)(hi - lo);
+      for (uint32_t i = tid; i < w_len; i += kTmaConsumers * 32) win[i] = __ldg(a.v + lo + i);
+      next_reload = c * SC + a.super_states;
+      consumer_sync();
+    }
+    // ---- two chunks: A = c, B = c+1 (if any and inside the same super-chunk)
+    const bool hasB = (c + 1 < nchunks) && (!WIN || (c + 1) * SC < next_reload);
+    const int stA = st, stB = (st + 1 == NS) ? 0 : st + 1;
+    const uint32_t parA = parity, parB = (stB == 0) ? parity ^ 1u : parity;
+    const int qbA = qb, qbB = (qb + 1 == QB) ? 0 : qb + 1;
+    const int64_t s0B = s0 + SC;
+    const int nsA = (int)((s_hi - s0) < SC ? (s_hi - s0) : SC);
+    const int nsB = hasB ? (int)((s_hi - s0B) < SC ? (s_hi - s0B) : SC) : 0;
+    const int rowsA = nsA * m, rowsB = nsB * m;
+    mbar_wait(bar_full + 8u * stA, parA);
+    if (hasB) mbar_wait(bar_full + 8u * stB, parB);
+    const uint32_t svA = stages_s + (uint32_t)stA * a.stage_bytes, svB = stages_s + (uint32_t)stB * a.stage_bytes;
+    auto aligned = [&](int rows) {
+      return ((uint32_t)rows * K * 8) % 16 == 0 && ((uint32_t)rows * K * 4) % 16 == 0 &&
+             ((uint32_t)rows * 8) % 16 == 0;
+    };
+    const bool smA = aligned(rowsA), smB = aligned(rowsB);
+    const int64_t row0A = s0 * m, row0B = s0B * m;
+    double* qA = qbuf + (size_t)qbA * rows_c;
+    double* qB = qbuf + (size_t)qbB * rows_c;
+    const int rmax = rowsA > rowsB ? rowsA : rowsB;
+    for (int rb = warp * GPW; rb < rmax; rb += kTmaConsumers * GPW) {
+      const int r = rb + grp;
+      double accA = row_partial(r, rowsA, smA, svA, svA + val_bytes_c, row0A);
+      double accB = hasB ? row_partial(r, rowsB, smB, svB, svB + val_bytes_c, row0B) : 0.0;
+      accA = group_sum<G>(accA);
+      accB = group_sum<G>(accB);
+      if (gl == 0) {
+        if (r < rowsA) {
+          const double g = smA ? lds_f64(svA + val_bytes_c + col_bytes_c + (uint32_t)r * 8u)
+                               : __ldg(a.cost + row0A + r);
+          qA[r] = add_rn(g, mul_rn(gamma, accA));
+        }
+        if (r < rowsB) {
+          const double g = smB ? lds_f64(svB + val_bytes_c + col_bytes_c + (uint32_t)r * 8u)
+                               : __ldg(a.cost + row0B + r);
+          qB[r] = add_rn(g, mul_rn(gamma, accB));
+        }
+      }
+    }
+    __syncwarp();
+    // release the stages and count arrivals; the last warp finishes the chunk
+    int lastA = 0, lastB = 0;
+    if (lane == 0) {
+      mbar_arrive(bar_empty + 8u * stA);
+      if (hasB) mbar_arrive(bar_empty + 8u * stB);
+      __threadfence_block();
+      lastA = atomicAdd(&cnt[qbA], 1) == kTmaConsumers - 1;
+      if (hasB) lastB = atomicAdd(&cnt[qbB], 1) == kTmaConsumers - 1;
+    }
+    lastA = __shfl_sync(kFull, lastA, 0);
+    lastB = __shfl_sync(kFull, lastB, 0);
+    if (lastA) {
+      __threadfence_block();
+      finish_chunk(c, s0, nsA, qA);
+      if (lane == 0) cnt[qbA] = 0;
+    }
+    if (lastB) {
+      __threadfence_block();
+      finish_chunk(c + 1, s0B, nsB, qB);
+      if (lane == 0) cnt[qbB] = 0;
+    }
+    // advance by the number of chunks consumed (1 or 2)
+    const int step = hasB ? 2 : 1;
+    for (int k = 0; k < step; ++k) {
+      if (++st == NS) {
+        st = 0;
+        parity ^= 1u;
+      }
+      if (++qb == QB) qb = 0;
+    }
+    if (!hasB) c -= 1;  // consumed only chunk c
   }
   if (a.res_bits) {
     res = warp_max(res);
@@ -323,7 +410,7 @@ bool k1_tma_plan(int64_t n_states_max_cta, int m, int K, int halo, int64_t n_glo
     if (sup < sc) return false;
   }
   wcap = (wcap + 15) / 16 * 16;  // keep the stage ring 128-byte aligned (TMA dst)
-  const int fixed = 256 + wcap * 8 + 2 * sc * m * 8 + 1024;
+  const int fixed = 256 + wcap * 8 + 12 * sc * m * 8 + 1024;  // q buffers: NS+2 <= 10
   int ns = (budget - fixed) / stage;
   if (ns > 8) ns = 8;
   if (ns < 2) return false;

@@ -358,8 +358,13 @@ int ipi_mdp_create(const int64_t* row_ptr, const int32_t* col, const double* val
   p.k1_variant = (p.uniform_rows && uniform_shape(p.row_len_max, &Gu, &Pu)) ? 1 : 0;
   // ---- TMA ring plan for uniform rows (one persistent CTA per SM) ------------
   {
+    // Experimental: off unless IPI_K1_TMA=1.  Measured on C2
+    // it is slower than the register-pipelined kernel (the shared-memory ring
+    // left beside the 72 KB V window holds ~100 KB in flight, the same as the
+    // registers of 32 warps, and the 16-warp ring couples warps through the
+    // producer's empty-barrier waits).
     const char* env = getenv("IPI_K1_TMA");
-    const bool allow = !(env && env[0] == '0');
+    const bool allow = env && env[0] == '1';
     if (allow && p.k1_variant == 1 && n_local > 0) {
       const int blocks = (int)std::min<int64_t>(h->num_sms, std::max<int64_t>(1, n_local / 64));
       const int64_t per = (n_local + blocks - 1) / blocks;
