@@ -176,6 +176,13 @@ int ipi_spmv(const int64_t* row_ptr, const int32_t* col, const double* val, int6
 int ipi_apply_J(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi, int64_t n,
                 double gamma, const double* x, const double* b, double* y, void* stream);
 
+/* Row-sharded PolicyOperator.apply for rank-local rows [state0, state0+n_local):
+ * y = x_full[state0+r] - gamma*(P x_full)[r]  (b == NULL)  or  b[r] - that.
+ * x_full holds all n_global entries (the all-gathered vector). */
+int ipi_apply_J_shard(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi,
+                      int64_t n_local, int64_t state0, double gamma, const double* x_full,
+                      const double* b, double* y, void* stream);
+
 /* ---- K4: policy evaluation (inner.py:163-292) ------------------------- */
 /* Solve (I - gamma P_pi) x = b from x (in/out) to the floored 2-norm target
  * or max_it iterations, one persistent cooperative kernel per call. */

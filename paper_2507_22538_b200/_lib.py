@@ -85,6 +85,7 @@ _SIGS = {
     "ipi_gather_policy": (C.c_int, [_p, _p, _p, _p, _p, _p, _p]),
     "ipi_spmv": (C.c_int, [_p, _p, _p, _i64, _i64, _p, _p, _p]),
     "ipi_apply_J": (C.c_int, [_p, _p, _p, _i64, _f64, _p, _p, _p, _p]),
+    "ipi_apply_J_shard": (C.c_int, [_p, _p, _p, _i64, _i64, _f64, _p, _p, _p, _p]),
     "ipi_inner_solve": (C.c_int, [_p, _p, _p, _i64, _f64, _p, _p, _f64, _i32, _i32, _f64,
                                   C.POINTER(InnerReport), _p]),
     "ipi_solve": (C.c_int, [_p, C.POINTER(Opts), _p, _p, _p, _i32, C.POINTER(Stats), _p]),

@@ -583,6 +583,19 @@ int ipi_apply_J(const int64_t* rp_pi, const int32_t* col_pi, const double* val_p
                      pick_lanes_per_row((double)nnz / (double)n), (cudaStream_t)stream);
 }
 
+int ipi_apply_J_shard(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi,
+                      int64_t n_local, int64_t state0, double gamma, const double* x_full,
+                      const double* b, double* y, void* stream) {
+  if (n_local <= 0) return IPI_OK;
+  int64_t nnz = 0;
+  IPI_CUDA_TRY(cudaMemcpyAsync(&nnz, rp_pi + n_local, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                               (cudaStream_t)stream));
+  IPI_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+  return launch_spmv(rp_pi, col_pi, val_pi, n_local, x_full, b, gamma, b ? 2 : 1, y,
+                     pick_lanes_per_row((double)nnz / (double)n_local), (cudaStream_t)stream,
+                     state0);
+}
+
 int ipi_inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi, int64_t n,
                     double gamma, const double* b, double* x, double target_2norm,
                     int32_t max_it, int32_t kind, double richardson_scale,

@@ -97,7 +97,7 @@ int policy_nnz(ipi_mdp* h, const int32_t* policy, int64_t* nnz_out, cudaStream_t
 // spmv.cu
 int launch_spmv(const int64_t* rp, const int32_t* col, const double* val, int64_t rows,
                 const double* x, const double* b, double gamma, int epi, double* y,
-                int lanes, cudaStream_t st);
+                int lanes, cudaStream_t st, int64_t diag_offset = 0);
 
 // krylov.cu
 int inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi, int64_t n,

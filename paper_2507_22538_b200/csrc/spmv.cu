@@ -18,7 +18,8 @@ __global__ void __launch_bounds__(256) spmv_kernel(const int64_t* __restrict__ r
                                                     const double* __restrict__ val, int64_t rows,
                                                     const double* __restrict__ x,
                                                     const double* __restrict__ b, double gamma,
-                                                    double* __restrict__ y) {
+                                                    double* __restrict__ y,
+                                                    const double* __restrict__ x_diag) {
   constexpr int GPW = 32 / G;
   const uint64_t pol = policy_evict_first();
   const int lane = threadIdx.x & 31;
@@ -59,7 +60,7 @@ __global__ void __launch_bounds__(256) spmv_kernel(const int64_t* __restrict__ r
       } else if (EPI == 3) {
         y[r] = add_rn(__ldg(b + r), mul_rn(gamma, acc));
       } else {
-        const double ax = sub_rn(__ldg(x + r), mul_rn(gamma, acc));
+        const double ax = sub_rn(__ldg(x_diag + r), mul_rn(gamma, acc));
         y[r] = EPI == 1 ? ax : sub_rn(__ldg(b + r), ax);
       }
     }
@@ -69,21 +70,22 @@ __global__ void __launch_bounds__(256) spmv_kernel(const int64_t* __restrict__ r
 template <int G>
 static void launch_spmv_g(const int64_t* rp, const int32_t* col, const double* val, int64_t rows,
                           const double* x, const double* b, double gamma, int epi, double* y,
-                          int blocks, cudaStream_t st) {
+                          int blocks, const double* xd, cudaStream_t st) {
   if (epi == 0)
-    spmv_kernel<G, 0><<<blocks, 256, 0, st>>>(rp, col, val, rows, x, b, gamma, y);
+    spmv_kernel<G, 0><<<blocks, 256, 0, st>>>(rp, col, val, rows, x, b, gamma, y, xd);
   else if (epi == 1)
-    spmv_kernel<G, 1><<<blocks, 256, 0, st>>>(rp, col, val, rows, x, b, gamma, y);
+    spmv_kernel<G, 1><<<blocks, 256, 0, st>>>(rp, col, val, rows, x, b, gamma, y, xd);
   else if (epi == 2)
-    spmv_kernel<G, 2><<<blocks, 256, 0, st>>>(rp, col, val, rows, x, b, gamma, y);
+    spmv_kernel<G, 2><<<blocks, 256, 0, st>>>(rp, col, val, rows, x, b, gamma, y, xd);
   else
-    spmv_kernel<G, 3><<<blocks, 256, 0, st>>>(rp, col, val, rows, x, b, gamma, y);
+    spmv_kernel<G, 3><<<blocks, 256, 0, st>>>(rp, col, val, rows, x, b, gamma, y, xd);
 }
 
 int launch_spmv(const int64_t* rp, const int32_t* col, const double* val, int64_t rows,
                 const double* x, const double* b, double gamma, int epi, double* y, int lanes,
-                cudaStream_t st) {
+                cudaStream_t st, int64_t diag_offset) {
   if (rows <= 0) return IPI_OK;
+  const double* xd = x + diag_offset;  // identity term of row r reads x[diag_offset + r]
   const int GPW = 32 / lanes;
   int64_t warps = (rows + GPW - 1) / GPW;
   int64_t blocks = (warps + 7) / 8;
@@ -93,12 +95,12 @@ int launch_spmv(const int64_t* rp, const int32_t* col, const double* val, int64_
   if (blocks > (int64_t)sms * 64) blocks = (int64_t)sms * 64;
   if (blocks < 1) blocks = 1;
   switch (lanes) {
-    case 1: launch_spmv_g<1>(rp, col, val, rows, x, b, gamma, epi, y, (int)blocks, st); break;
-    case 2: launch_spmv_g<2>(rp, col, val, rows, x, b, gamma, epi, y, (int)blocks, st); break;
-    case 4: launch_spmv_g<4>(rp, col, val, rows, x, b, gamma, epi, y, (int)blocks, st); break;
-    case 8: launch_spmv_g<8>(rp, col, val, rows, x, b, gamma, epi, y, (int)blocks, st); break;
-    case 16: launch_spmv_g<16>(rp, col, val, rows, x, b, gamma, epi, y, (int)blocks, st); break;
-    default: launch_spmv_g<32>(rp, col, val, rows, x, b, gamma, epi, y, (int)blocks, st); break;
+    case 1: launch_spmv_g<1>(rp, col, val, rows, x, b, gamma, epi, y, (int)blocks, xd, st); break;
+    case 2: launch_spmv_g<2>(rp, col, val, rows, x, b, gamma, epi, y, (int)blocks, xd, st); break;
+    case 4: launch_spmv_g<4>(rp, col, val, rows, x, b, gamma, epi, y, (int)blocks, xd, st); break;
+    case 8: launch_spmv_g<8>(rp, col, val, rows, x, b, gamma, epi, y, (int)blocks, xd, st); break;
+    case 16: launch_spmv_g<16>(rp, col, val, rows, x, b, gamma, epi, y, (int)blocks, xd, st); break;
+    default: launch_spmv_g<32>(rp, col, val, rows, x, b, gamma, epi, y, (int)blocks, xd, st); break;
   }
   IPI_LAUNCH_CHECK();
   return IPI_OK;

@@ -14,6 +14,7 @@ a run at fixed R is bit-reproducible like ``tree_reduce`` (parallel.py:21-33).
 
 from __future__ import annotations
 
+import math
 from dataclasses import dataclass
 
 import torch
@@ -22,7 +23,8 @@ from . import _lib
 from .model import Mode, Partition, make_partition
 from .sparse import CsrMatrix
 
-__all__ = ["MdpShard", "RankContext", "allgather_blocks", "rank_ordered_sum", "rank_max"]
+__all__ = ["MdpShard", "RankContext", "ShardOps", "allgather_blocks", "host_gmres",
+           "host_richardson", "rank_max", "rank_ordered_sum", "solve_sharded"]
 
 
 @dataclass
@@ -163,3 +165,216 @@ class MdpShard:
             except Exception:
                 pass
             self._handle = None
+
+
+# ----------------------------------------------------------------------------
+# Sharded iPI (host-driven phases, collectives between them)
+# ----------------------------------------------------------------------------
+#
+# Every rank runs the same control flow on bit-identical scalars (all scalar
+# reductions go through rank_ordered_sum / rank_max), so decisions (stopping
+# tests, Givens, est_target) agree across ranks without broadcasts.  The
+# numeric phases are the rank-local kernels: K1 on the shard with the
+# all-gathered V, K2 on the local rows, and the sharded J_pi apply
+# (ipi_apply_J_shard) on the all-gathered Krylov vector.  The GMRES /
+# Richardson control logic below restates inner.py:216-292 exactly; it is
+# written against a tiny vector-ops interface so the CPU tests can drive it
+# with gloo and numpy stand-ins.
+
+GMRES_RESTART = 30
+
+
+class ShardOps:
+    """Device implementation of the sharded-iPI vector interface for one rank."""
+
+    def __init__(self, shard: "MdpShard", ctx: RankContext):
+        self.shard = shard
+        self.ctx = ctx
+        dev = shard.stage_cost.device
+        self.full = torch.empty(shard.n_global, dtype=torch.float64, device=dev)
+
+    # -- collectives ------------------------------------------------------
+    def allgather(self, local: torch.Tensor) -> torch.Tensor:
+        return allgather_blocks(local.contiguous(), self.full, self.ctx.partition)
+
+    def dot(self, a: torch.Tensor, b: torch.Tensor) -> float:
+        part = torch.dot(a, b).reshape(1)
+        return float(rank_ordered_sum(part, self.ctx.world)[0])
+
+    def max(self, x: float) -> float:
+        t = torch.tensor([x], dtype=torch.float64, device=self.full.device)
+        return float(rank_max(t)[0])
+
+    # -- kernels ------------------------------------------------------------
+    def greedy(self, v_local: torch.Tensor):
+        """K1 on the shard: (policy_local int32, applied_local, global ||v - Tv||_inf)."""
+        vf = self.allgather(v_local)
+        pol, app, bits = self.shard.bellman(vf)
+        res = float(bits.view(torch.float64)[0])
+        return pol.clone(), app.clone(), self.max(res)
+
+    def gather_policy(self, policy_local: torch.Tensor):
+        sh = self.shard
+        h = sh.handle()
+        nnz = _lib.C.c_int64()
+        L = _lib.lib()
+        _lib.check(L.ipi_policy_nnz(h, _lib.ptr(policy_local), _lib.C.byref(nnz), _lib.stream_ptr()),
+                   "ipi_policy_nnz")
+        dev = policy_local.device
+        rp = torch.empty(sh.n_local + 1, dtype=torch.int64, device=dev)
+        col = torch.empty(max(nnz.value, 1), dtype=torch.int32, device=dev)
+        val = torch.empty(max(nnz.value, 1), dtype=torch.float64, device=dev)
+        g = torch.empty(sh.n_local, dtype=torch.float64, device=dev)
+        _lib.check(L.ipi_gather_policy(h, _lib.ptr(policy_local), _lib.ptr(rp), _lib.ptr(col),
+                                       _lib.ptr(val), _lib.ptr(g), _lib.stream_ptr()),
+                   "ipi_gather_policy")
+        return (rp, col, val), g
+
+    def apply(self, P, x_local: torch.Tensor, b_local: torch.Tensor | None = None) -> torch.Tensor:
+        """b - (x - gamma P x) (or x - gamma P x) on the local rows."""
+        xf = self.allgather(x_local)
+        rp, col, val = P
+        y = torch.empty_like(x_local)
+        sh = self.shard
+        _lib.check(_lib.lib().ipi_apply_J_shard(
+            _lib.ptr(rp), _lib.ptr(col), _lib.ptr(val), sh.n_local, sh.state0, sh.gamma,
+            _lib.ptr(xf), _lib.ptr(b_local) if b_local is not None else None, _lib.ptr(y),
+            _lib.stream_ptr()), "ipi_apply_J_shard")
+        return y
+
+    def sweep(self, P, g_local, v_local):
+        """g_pi + gamma * P_pi v (breakdown fallback, driver.py:190-193)."""
+        return g_local + self.shard.gamma * (v_local - self.apply(P, v_local))
+
+
+def host_richardson(ops, P, b, theta0, eff, max_it, scale):
+    """inner.py:216-226 on sharded vectors."""
+    theta = theta0.clone() if hasattr(theta0, "clone") else theta0.copy()
+    it = 0
+    while True:
+        r = ops.apply(P, theta, b)
+        rn = math.sqrt(ops.dot(r, r))
+        if rn <= eff or it >= max_it or not math.isfinite(rn):
+            break
+        theta = theta + scale * r
+        it += 1
+    return theta, it, rn, False
+
+
+def host_gmres(ops, P, b, theta0, eff, max_it):
+    """Restarted GMRES(30) with MGS and Givens (inner.py:229-292) on sharded vectors."""
+    x = theta0.clone() if hasattr(theta0, "clone") else theta0.copy()
+    it = 0
+    r = ops.apply(P, x, b)
+    rn = math.sqrt(ops.dot(r, r))
+    est_target = eff
+    R = GMRES_RESTART
+    while rn > eff and it < max_it:
+        beta = math.sqrt(ops.dot(r, r))
+        if beta == 0.0 or not math.isfinite(beta):
+            break
+        V = [r / beta]
+        H = [[0.0] * R for _ in range(R + 1)]
+        cs = [0.0] * R
+        sn = [0.0] * R
+        g = [0.0] * (R + 1)
+        g[0] = beta
+        j = 0
+        while j < R and it < max_it:
+            w = ops.apply(P, V[j])
+            it += 1
+            for l in range(j + 1):
+                H[l][j] = ops.dot(V[l], w)
+                w = w - H[l][j] * V[l]
+            hnorm = math.sqrt(ops.dot(w, w))
+            H[j + 1][j] = hnorm
+            for l in range(j):
+                t = cs[l] * H[l][j] + sn[l] * H[l + 1][j]
+                H[l + 1][j] = -sn[l] * H[l][j] + cs[l] * H[l + 1][j]
+                H[l][j] = t
+            denom = math.hypot(H[j][j], H[j + 1][j])
+            if denom == 0.0:
+                break
+            cs[j], sn[j] = H[j][j] / denom, H[j + 1][j] / denom
+            H[j][j] = denom
+            H[j + 1][j] = 0.0
+            g[j + 1] = -sn[j] * g[j]
+            g[j] = cs[j] * g[j]
+            j += 1
+            if abs(g[j]) <= est_target or hnorm == 0.0:
+                break
+            V.append(w / hnorm)
+        if j == 0:
+            break
+        y = [0.0] * j
+        for i in range(j - 1, -1, -1):
+            acc = g[i] - sum(H[i][k] * y[k] for k in range(i + 1, j))
+            y[i] = acc / H[i][i] if H[i][i] != 0.0 else 0.0
+        upd = V[0] * y[0]
+        for l in range(1, j):
+            upd = upd + V[l] * y[l]
+        x = x + upd
+        r = ops.apply(P, x, b)
+        rn = math.sqrt(ops.dot(r, r))
+        if rn > eff and abs(g[j]) <= est_target:
+            if abs(g[j]) == 0.0:
+                break
+            est_target = abs(g[j]) * (eff / rn) * 0.5
+    return x, it, rn, False
+
+
+def solve_sharded(ops, opts, n_global: int, v0_local=None):
+    """Algorithm 1 (driver.py:109-209) across ranks; returns a SolveResult whose
+    values/policy are the gathered full vectors (on every rank)."""
+    import time
+    from .driver import STALL_WINDOW, SolveResult, SolveStatus
+    from .inner import InnerSolver
+    if opts.inner not in (InnerSolver.GMRES, InnerSolver.RICHARDSON):
+        raise NotImplementedError("the sharded path runs GMRES and Richardson inner solves")
+    t0 = time.perf_counter()
+    v = v0_local
+    if v is None:
+        lo, hi = ops.ctx.block
+        v = torch.zeros(hi - lo, dtype=torch.float64, device=ops.full.device)
+    history: list[float] = []
+    inner_total = 0
+    stall = 0
+    k = 0
+    while True:
+        pol, _, res = ops.greedy(v)
+        history.append(res)
+        if res <= opts.tol:
+            status = SolveStatus.CONVERGED
+            break
+        if k >= opts.max_outer:
+            status = SolveStatus.OUTER_CAP
+            break
+        if k > 0 and res >= history[k - 1]:
+            stall += 1
+            if stall >= STALL_WINDOW:
+                status = SolveStatus.STALLED
+                break
+        else:
+            stall = 0
+        P, g = ops.gather_policy(pol)
+        if opts.ksp_max_it is not None:
+            target, cap = 0.0, opts.ksp_max_it
+        else:
+            target, cap = opts.alpha * res, opts.max_inner
+        bn = math.sqrt(ops.dot(g, g))
+        eff = max(target, 1e-14 * max(1.0, bn))          # inner.py:189
+        if opts.inner is InnerSolver.GMRES:
+            v, its, _, _ = host_gmres(ops, P, g, v, eff, cap)
+        else:
+            v, its, _, _ = host_richardson(ops, P, g, v, eff, cap, opts.richardson_scale)
+        inner_total += its
+        k += 1
+    values = ops.allgather(v).clone() if hasattr(v, "clone") else ops.allgather(v).copy()
+    pol_full = ops.allgather(pol.to(values.dtype) if hasattr(pol, "to") else pol.astype(values.dtype))
+    import numpy as _np
+    vals_np = values.cpu().numpy() if hasattr(values, "cpu") else _np.asarray(values)
+    pol_np = (pol_full.cpu().numpy() if hasattr(pol_full, "cpu") else _np.asarray(pol_full))
+    return SolveResult(values=vals_np.copy(), policy=pol_np.astype(_np.int64),
+                       outer_iterations=k, inner_iterations_total=inner_total,
+                       residual_history=history, status=status,
+                       wall_time=time.perf_counter() - t0)

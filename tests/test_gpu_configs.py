@@ -259,3 +259,24 @@ def test_c2_full_size_oracle_parity(c2_full):
         assert np.all(q[:, 1] - q[:, 0] < TIE_GAP)
     _, _, r = co.greedy(rp, col, val, cost, spec.gamma, res_gpu.values, nthreads=nt)
     assert r <= spec.atol
+
+
+# ----------------------------------------------------------------------------
+# sharded iPI driver with the real device kernels (world size 1 on one GPU;
+# the multi-rank control flow is covered over gloo in test_host.py)
+# ----------------------------------------------------------------------------
+
+@pytest.mark.parametrize("kind", ["gmres", "richardson"])
+def test_sharded_driver_matches_persistent_solver(kind):
+    from paper_2507_22538_b200.parallel import MdpShard, RankContext, ShardOps, solve_sharded
+    mdp, spec = devgen.build_instance(2, n=8192)
+    ctx = RankContext.from_env(mdp.n)
+    shard = MdpShard(mdp.n, mdp.m, spec.gamma, 0, mdp.stage_cost, mdp.transitions)
+    opts = ipi.SolveOptions(alpha=spec.alpha, tol=spec.atol, inner=ipi.InnerSolver.from_name(kind),
+                            max_outer=200)
+    res = solve_sharded(ShardOps(shard, ctx), opts, mdp.n)
+    ref = ipi.solve(mdp, opts)
+    assert res.status == ref.status
+    assert abs(res.outer_iterations - ref.outer_iterations) <= 1
+    np.testing.assert_allclose(res.values, ref.values, rtol=1e-8, atol=1e-8)
+    np.testing.assert_array_equal(res.policy, ref.policy)

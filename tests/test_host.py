@@ -286,3 +286,105 @@ def test_rowblock_sharding_gloo_world2():
         assert res == float(np.max(np.abs(v - applied)))
         assert np.isclose(tot, applied.sum(), rtol=1e-14)
         np.testing.assert_array_equal(np.concatenate([np.asarray(p) for p in pis]), pi)
+
+
+# ----------------------------------------------------------------------------
+# sharded iPI control flow over gloo (world size 2) with oracle stand-ins for
+# the device kernels; must reproduce the single-process oracle solve
+# ----------------------------------------------------------------------------
+
+class _CpuShardOps:
+    """Test stand-in for parallel.ShardOps: same interface, numpy oracle math."""
+
+    def __init__(self, arrays, gamma, ctx):
+        import torch
+        from oracle import mdp_oracle as orc
+        self.orc = orc
+        rp, col, val, cost = arrays
+        self.ctx = ctx
+        self.gamma = gamma
+        lo, hi = ctx.block
+        m = cost.shape[1]
+        r0, r1 = lo * m, hi * m
+        self.rp = rp[r0:r1 + 1] - rp[r0]
+        self.col = col[rp[r0]:rp[r1]]
+        self.val = val[rp[r0]:rp[r1]]
+        self.cost = cost[lo:hi]
+        self.lo = lo
+        self.full = torch.zeros(cost.shape[0], dtype=torch.float64)
+
+    def allgather(self, local):
+        from paper_2507_22538_b200.parallel import allgather_blocks
+        return allgather_blocks(local, self.full, self.ctx.partition)
+
+    def dot(self, a, b):
+        import torch
+        from paper_2507_22538_b200.parallel import rank_ordered_sum
+        return float(rank_ordered_sum(torch.dot(a, b).reshape(1), self.ctx.world)[0])
+
+    def greedy(self, v_local):
+        import torch
+        from paper_2507_22538_b200.parallel import rank_max
+        vf = self.allgather(v_local).numpy()
+        pi, applied = self.orc.greedy(self.rp, self.col, self.val, self.cost, self.gamma, vf)
+        res = float(np.max(np.abs(v_local.numpy() - applied)))
+        return (torch.as_tensor(pi.astype(np.int32)), torch.as_tensor(applied),
+                float(rank_max(torch.tensor([res], dtype=torch.float64))[0]))
+
+    def gather_policy(self, pol):
+        import torch
+        rpp, cp, vp, g = self.orc.gather_policy(self.rp, self.col, self.val, self.cost,
+                                                pol.numpy().astype(np.int64))
+        return (rpp, cp, vp), torch.as_tensor(g)
+
+    def apply(self, P, x_local, b_local=None):
+        import torch
+        xf = self.allgather(x_local).numpy()
+        rpp, cp, vp = P
+        n_loc = x_local.shape[0]
+        y = xf[self.lo:self.lo + n_loc] - self.gamma * self.orc.spmv(rpp, cp, vp, xf)
+        y = torch.as_tensor(y)
+        return b_local - y if b_local is not None else y
+
+
+def _sharded_solve_worker(rank, world, port, kind, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2507_22538_b200.parallel import RankContext, solve_sharded
+        arrays = gen.random_locality_host(61, 4, 6, 8, seed=2)
+        ctx = RankContext.from_env(61)
+        ops = _CpuShardOps(arrays, 0.95, ctx)
+        lo, hi = ctx.block
+        res = solve_sharded(ops, ipi.SolveOptions(inner=ipi.InnerSolver.from_name(kind)), 61,
+                            torch.zeros(hi - lo, dtype=torch.float64))
+        q.put((rank, res.status.value, res.outer_iterations, res.values.tolist(),
+               res.policy.tolist(), res.residual_history))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind", ["gmres", "richardson"])
+def test_sharded_ipi_gloo_world2_matches_oracle(kind):
+    import torch.multiprocessing as mp
+    from oracle import mdp_oracle as orc
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sharded_solve_worker, args=(r, 2, port, kind, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=180) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    rp, col, val, cost = gen.random_locality_host(61, 4, 6, 8, seed=2)
+    ref = orc.solve(rp, col, val, cost, 0.95, kind=kind)
+    (_, st0, k0, v0, p0, h0), (_, st1, k1, v1, p1, h1) = out
+    assert (st0, k0, p0, h0) == (st1, k1, p1, h1) and v0 == v1   # ranks agree exactly
+    assert st0 == ref.status and k0 == ref.outer_iterations
+    np.testing.assert_allclose(v0, ref.values, rtol=1e-10, atol=1e-10)
+    np.testing.assert_array_equal(p0, ref.policy)
+    np.testing.assert_allclose(h0, ref.residual_history, rtol=1e-6, atol=1e-12)
