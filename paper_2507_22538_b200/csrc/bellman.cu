@@ -283,6 +283,137 @@ __global__ void __launch_bounds__(kK1Threads) k1_bellman_uniform(K1Args a, int K
   }
 }
 
+// ---------------------------------------------------------------------------
+// Flat-rows fast path for very short uniform rows (K <= 4, e.g. C3's bilinear
+// rows): one (s,a) row per lane over a warp-contiguous row range that ignores
+// state boundaries, so no lane idles when 32 is not a multiple of m (C3:
+// m = 21).  The per-state first-index argmin is a segmented shuffle scan keyed
+// by state id, with the partial best of a state that straddles two batches
+// carried in registers.  Loads of batch b+1 are issued before batch b is
+// reduced.
+// ---------------------------------------------------------------------------
+struct FlatBatch {
+  double2 v0, v1;
+  int2 c0, c1;
+  double g;
+};
+
+template <bool WIN>
+__global__ void __launch_bounds__(kK1Threads, 2) k1_bellman_flat(K1Args a, int K) {
+  extern __shared__ double win[];
+  __shared__ double red[32];
+  const int64_t s_lo = a.bounds[blockIdx.x], s_hi = a.bounds[blockIdx.x + 1];
+  int w_lo = 0;
+  uint32_t w_len = 0;
+  if (WIN) {
+    int64_t lo = a.state0 + s_lo - a.halo;
+    int64_t hi = a.state0 + s_hi + a.halo;
+    lo = lo < 0 ? 0 : lo;
+    hi = hi > a.n_global ? a.n_global : hi;
+    w_lo = (int)lo;
+    w_len = hi > lo ? (uint32_t)(hi - lo) : 0u;
+    for (uint32_t i = threadIdx.x; i < w_len; i += blockDim.x) win[i] = __ldg(a.v + lo + i);
+    __syncthreads();
+  }
+  const uint64_t pol = policy_evict_first();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const bool mx = a.maximize != 0;
+  const int m = a.m;
+  double res = 0.0;
+  auto gather = [&](int c) -> double {
+    if (WIN) {
+      const uint32_t off = (uint32_t)(c - w_lo);
+      if (off < w_len) return win[off];
+    }
+    return __ldg(a.v + c);
+  };
+  // this warp's contiguous state range -> row range
+  const int64_t ns = s_hi - s_lo;
+  const int64_t ws0 = s_lo + ns * warp / nwarps, ws1 = s_lo + ns * (warp + 1) / nwarps;
+  const int64_t r_beg = ws0 * m, r_end = ws1 * m;
+  const int pairs = K >> 1;
+  auto load = [&](int64_t base, FlatBatch& b) {
+    const int64_t r = base + lane;
+    const bool ok = r < r_end;
+    const double* vp = a.val + r * K;
+    const int* cp = a.col + r * K;
+    b.v0 = ok ? ld_stream_v2(vp, pol) : make_double2(0.0, 0.0);
+    b.c0 = ok ? ld_stream_v2(cp, pol) : make_int2(-1, -1);
+    const bool ok1 = ok && pairs > 1;
+    b.v1 = ok1 ? ld_stream_v2(vp + 2, pol) : make_double2(0.0, 0.0);
+    b.c1 = ok1 ? ld_stream_v2(cp + 2, pol) : make_int2(-1, -1);
+    b.g = ok ? __ldg(a.cost + r) : 0.0;
+  };
+  double carry_q = mx ? -INFINITY : INFINITY;
+  int carry_a = INT_MAX;
+  int64_t carry_s = -1;
+  if (r_beg < r_end) {
+    FlatBatch cur, nxt;
+    load(r_beg, cur);
+    for (int64_t base = r_beg; base < r_end; base += 32) {
+      const bool has_next = base + 32 < r_end;
+      if (has_next) load(base + 32, nxt);
+      const int64_t r = base + lane;
+      const bool ok = r < r_end;
+      double acc = 0.0;
+      if (ok) {
+        if (cur.c0.x >= 0) acc = add_rn(acc, mul_rn(cur.v0.x, gather(cur.c0.x)));
+        if (cur.c0.y >= 0) acc = add_rn(acc, mul_rn(cur.v0.y, gather(cur.c0.y)));
+        if (cur.c1.x >= 0) acc = add_rn(acc, mul_rn(cur.v1.x, gather(cur.c1.x)));
+        if (cur.c1.y >= 0) acc = add_rn(acc, mul_rn(cur.v1.y, gather(cur.c1.y)));
+      }
+      // state id and action of this lane's row
+      const int64_t sb = base / m;
+      const int rem = (int)(base - sb * m);
+      const int t = rem + lane;
+      const int ds = t / m;
+      int64_t sid = ok ? sb + ds : INT64_MAX;
+      int act = t - ds * m;
+      double q = ok ? add_rn(cur.g, mul_rn(a.gamma, acc)) : (mx ? -INFINITY : INFINITY);
+      int aa = ok ? act : INT_MAX;
+      // merge the carried partial of a state begun in the previous batch
+      if (lane == 0 && sid == carry_s && better(carry_q, carry_a, q, aa, mx)) {
+        q = carry_q;
+        aa = carry_a;
+      }
+      // segmented inclusive scan (first-index argmin) by state id
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const double oq = __shfl_up_sync(kFull, q, off);
+        const int oa = __shfl_up_sync(kFull, aa, off);
+        const long long os = __shfl_up_sync(kFull, (long long)sid, off);
+        if (lane >= off && os == sid && better(oq, oa, q, aa, mx)) {
+          q = oq;
+          aa = oa;
+        }
+      }
+      if (ok && act == m - 1) {  // last row of a state: its best is final
+        const int64_t s = sid;
+        const int ba = aa == INT_MAX ? 0 : aa;
+        a.policy[s] = ba;
+        a.applied[s] = q;
+        if (a.gpi) a.gpi[s] = __ldg(a.cost + s * m + ba);
+        if (a.lenpi) a.lenpi[s] = K;
+        res = fmax(res, fabs(sub_rn(gather((int)(a.state0 + s)), q)));
+      }
+      carry_q = __shfl_sync(kFull, q, 31);
+      carry_a = __shfl_sync(kFull, aa, 31);
+      carry_s = __shfl_sync(kFull, (long long)sid, 31);
+      if (has_next) cur = nxt;
+    }
+  }
+  if (a.res_bits) {
+    res = warp_max(res);
+    if (lane == 0) red[warp] = res;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < nwarps; ++w) t = fmax(t, red[w]);
+      atomicMax(a.res_bits, (unsigned long long)__double_as_longlong(t));
+    }
+  }
+}
+
 // (G, P) for the uniform path: pairs = K/2 <= P*G, P = 2 (or 4 for very long rows)
 bool uniform_shape(int K, int* G, int* P) {
   if (K <= 0 || (K & 1)) return false;
@@ -344,6 +475,8 @@ int k1_set_smem(int lanes, int smem) {
     default: e = set_smem_attr<32>(smem); break;
   }
   if (e != cudaSuccess) return fail(IPI_ECUDA, std::string("k1 smem attr: ") + cudaGetErrorString(e));
+  e = cudaFuncSetAttribute(k1_bellman_flat<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return fail(IPI_ECUDA, std::string("k1 smem attr: ") + cudaGetErrorString(e));
   for (int K = 2; K <= 256; K *= 2) {  // make every uniform instance launchable too
     int G, P;
     if (uniform_shape(K, &G, &P)) {
@@ -358,7 +491,9 @@ int k1_set_smem(int lanes, int smem) {
 int k1_occupancy(int lanes, int uniform_K, bool win, int smem) {
   int G = 0, P = 0, nb = 0;
   const void* fn = nullptr;
-  if (uniform_K > 0 && uniform_shape(uniform_K, &G, &P)) {
+  if (uniform_K > 0 && uniform_K <= 4 && uniform_K % 2 == 0) {
+    fn = win ? (const void*)k1_bellman_flat<true> : (const void*)k1_bellman_flat<false>;
+  } else if (uniform_K > 0 && uniform_shape(uniform_K, &G, &P)) {
 #define U_FN(GG, PP) fn = (win ? (const void*)k1_bellman_uniform<GG, PP, true> \
                            : (const void*)k1_bellman_uniform<GG, PP, false>)
     IPI_DISPATCH_UNIFORM(G, P, U_FN);
@@ -407,6 +542,15 @@ int launch_bellman(ipi_mdp* h, const double* v_full, int32_t mode, int32_t* poli
   const bool win = h->plan.halo >= 0;
   const int blocks = h->plan.k1_blocks, smem = h->plan.k1_smem_bytes;
   int G = 0, P = 0;
+  if (h->plan.uniform_rows && h->plan.row_len_max <= 4 && (h->plan.row_len_max % 2) == 0) {
+    const int K = h->plan.row_len_max;
+    if (win)
+      k1_bellman_flat<true><<<blocks, kK1Threads, smem, st>>>(a, K);
+    else
+      k1_bellman_flat<false><<<blocks, kK1Threads, 0, st>>>(a, K);
+    IPI_LAUNCH_CHECK();
+    return IPI_OK;
+  }
   if (h->plan.uniform_rows && uniform_shape(h->plan.row_len_max, &G, &P)) {
     const int K = h->plan.row_len_max;
 #define IPI_U_LAUNCH(GG, PP) launch_u<GG, PP>(a, K, win, blocks, smem, st)
