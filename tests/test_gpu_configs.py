@@ -280,3 +280,25 @@ def test_sharded_driver_matches_persistent_solver(kind):
     assert abs(res.outer_iterations - ref.outer_iterations) <= 1
     np.testing.assert_allclose(res.values, ref.values, rtol=1e-8, atol=1e-8)
     np.testing.assert_array_equal(res.policy, ref.policy)
+
+
+def test_k1_on_row_shards_equals_full_instance():
+    """K1 on rank-local row blocks (state0 > 0, global columns, V window in
+    global coordinates) reproduces the full-instance backup on those states."""
+    from paper_2507_22538_b200.parallel import MdpShard
+    from paper_2507_22538_b200.model import make_partition
+    n = 12_000
+    mdp, spec = devgen.build_instance(2, n=n)
+    v = torch.rand(n, dtype=torch.float64, device="cuda") * 5
+    pi_f, tv_f, _ = greedy_device(mdp, v, ipi.Mode.MIN)
+    part = make_partition(n, 7)   # unequal blocks (12000 mod 7 != 0)
+    for r in range(7):
+        lo, hi = part.block(r)
+        rp, col, val, cost = devgen.locality(n, spec.m, spec.K, spec.window, 0, lo, hi - lo)
+        sh = MdpShard(n, spec.m, spec.gamma, lo, cost,
+                      ipi.CsrMatrix((hi - lo) * spec.m, n, rp, col, val))
+        pol, app, bits = sh.bellman(v)
+        assert torch.equal(pol.long(), pi_f[lo:hi].long())
+        assert torch.equal(app, tv_f[lo:hi])
+        r_loc = float(bits.view(torch.float64)[0])
+        assert r_loc == float((v[lo:hi] - tv_f[lo:hi]).abs().max())

@@ -388,3 +388,32 @@ def test_sharded_ipi_gloo_world2_matches_oracle(kind):
     np.testing.assert_allclose(v0, ref.values, rtol=1e-10, atol=1e-10)
     np.testing.assert_array_equal(p0, ref.policy)
     np.testing.assert_allclose(h0, ref.residual_history, rtol=1e-6, atol=1e-12)
+
+
+def test_fromfile_errors_carry_offsets(tmp_path):
+    bad = tmp_path / "bad.bin"
+    bad.write_bytes(b"WRONGMAG" + b"\x00" * 40)
+    with pytest.raises(ipi.FileFormatError) as err:
+        mf.Matrix.fromFile(bad)
+    assert err.value.offset == 0
+    short = tmp_path / "short.bin"
+    short.write_bytes(b"MDPMAT01")
+    with pytest.raises(ipi.FileFormatError, match="shorter than the header"):
+        mf.Matrix.fromFile(short)
+
+
+def test_dense_file_round_trip_host(tmp_path):
+    a = np.arange(12, dtype=np.float64).reshape(3, 4)
+    ipi.write_matrix(tmp_path / "d.bin", a)
+    np.testing.assert_array_equal(mf.Matrix.fromFile(tmp_path / "d.bin").data, a)
+
+
+def test_creator_argument_errors_before_device():
+    with pytest.raises(ipi.ValidationError, match="empty distribution"):
+        mf.createTransitionProbabilityTensor(2, 1, lambda s, a: ([], []))
+    with pytest.raises(ipi.ValidationError, match="outside"):
+        mf.createTransitionProbabilityTensor(2, 1, lambda s, a: ([5], [1.0]))
+    with pytest.raises(ipi.ValidationError, match="twice"):
+        mf.createTransitionProbabilityTensor(2, 1, lambda s, a: ([0, 0], [0.5, 0.5]))
+    with pytest.raises(ipi.ValidationError, match="negative"):
+        mf.createTransitionProbabilityTensor(2, 1, lambda s, a: ([0, 1], [1.5, -0.5]))
