@@ -605,11 +605,18 @@ int ipi_inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* v
   int64_t nnz = 0;
   IPI_CUDA_TRY(cudaMemcpyAsync(&nnz, rp_pi + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   IPI_CUDA_TRY(cudaStreamSynchronize(st));
+  // plan the standalone operator like an m = 1 instance (row stats + locality
+  // profile -> lanes per row, uniform rows, V-window halo)
+  ipi_mdp* view = nullptr;
+  int rc = ipi_mdp_create(rp_pi, col_pi, val_pi, b, n, n, 1, 0, gamma, IPI_MODE_MIN, stream, &view);
+  if (rc) return rc;
+  const ipi_plan pl = view->plan;
+  ipi_mdp_destroy(view);
   ipi_inner_report* d_rep = nullptr;
   IPI_CUDA_TRY(cudaMalloc(&d_rep, sizeof(ipi_inner_report)));
-  int rc = inner_solve(rp_pi, col_pi, val_pi, n, gamma, b, x, target_2norm, max_it, kind,
-                       richardson_scale, pick_lanes_per_row((double)nnz / (double)n), -1, 0, d_rep,
-                       st);
+  rc = inner_solve(rp_pi, col_pi, val_pi, n, gamma, b, x, target_2norm, max_it, kind,
+                   richardson_scale, pl.lanes_per_row, pl.halo,
+                   pl.uniform_rows ? pl.row_len_max : 0, d_rep, st);
   if (rc == IPI_OK && report) {
     cudaError_t e = cudaMemcpyAsync(report, d_rep, sizeof(*report), cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);

@@ -95,7 +95,8 @@ __device__ __forceinline__ void grid_allreduce(double (&v)[NV], const KArgs& a, 
 }
 
 // Row sums of P_pi over this CTA's rows with an optional shared-memory window
-// of the input vector; epi(s, Px_s) is called by one lane per row.  P == 0:
+// of the input vector; epi(s, Px_s, x_s) is called by one lane per row, x_s
+// being the input's own entry (from the window when it is resident).  P == 0:
 // generic rows (G lanes strided over the row, 4 loads in flight); P > 0:
 // uniform even-length rows, P 16-byte value pairs per lane, batches
 // software-pipelined across row groups (same scheme as K1's fast path).
@@ -154,7 +155,7 @@ __device__ __forceinline__ void spmv_rows(const KArgs& a, const double* xin, int
         }
       }
       acc = group_sum<G>(acc);
-      if (s < s_hi && gl == 0) epi(s, acc);
+      if (s < s_hi && gl == 0) epi(s, acc, gather((int)s));
     }
   } else {
     const int K = a.K, pairs = K >> 1;
@@ -191,7 +192,7 @@ __device__ __forceinline__ void spmv_rows(const KArgs& a, const double* xin, int
         }
         acc = group_sum<G>(acc);
         const int64_t s = base + grp;
-        if (s < s_hi && gl == 0) epi(s, acc);
+        if (s < s_hi && gl == 0) epi(s, acc, gather((int)s));
         if (!has_next) break;
         cur = nxt;
         base = nb;
@@ -231,8 +232,8 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
   // ---- r = b - (x - gamma P x), ||b||, ||r|| --------------------------------
   double acc2[2] = {0.0, 0.0};
   for (int64_t i = s_lo + tid; i < s_hi; i += nthr) acc2[0] = add_rn(acc2[0], mul_rn(b[i], b[i]));
-  spmv_rows<G, P, WIN>(a, x, s_lo, s_hi, win, pol, [&](int64_t s, double px) {
-    const double ri = sub_rn(b[s], sub_rn(x[s], mul_rn(gam, px)));
+  spmv_rows<G, P, WIN>(a, x, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
+    const double ri = sub_rn(b[s], sub_rn(xs, mul_rn(gam, px)));
     r[s] = ri;
     acc2[1] = add_rn(acc2[1], mul_rn(ri, ri));
   });
@@ -245,8 +246,8 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
   auto true_residual = [&]() -> double {
     grid.sync();
     double q[1] = {0.0};
-    spmv_rows<G, P, WIN>(a, x, s_lo, s_hi, win, pol, [&](int64_t s, double px) {
-      const double ri = sub_rn(b[s], sub_rn(x[s], mul_rn(gam, px)));
+    spmv_rows<G, P, WIN>(a, x, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
+      const double ri = sub_rn(b[s], sub_rn(xs, mul_rn(gam, px)));
       r[s] = ri;
       q[0] = add_rn(q[0], mul_rn(ri, ri));
     });
@@ -276,8 +277,8 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
       }
       grid.sync();
       double p2[2] = {0.0, 0.0};
-      spmv_rows<G, P, WIN>(a, yv, s_lo, s_hi, win, pol, [&](int64_t s, double px) {
-        const double u = sub_rn(yv[s], mul_rn(gam, px));
+      spmv_rows<G, P, WIN>(a, yv, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
+        const double u = sub_rn(xs, mul_rn(gam, px));
         uv[s] = u;
         vv[s] = u;
         p2[0] = add_rn(p2[0], mul_rn(r0[s], u));
@@ -306,12 +307,12 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
           } else {
             for (int64_t i = s_lo + tid; i < s_hi; i += nthr) yv[i] = sub_rn(yv[i], mul_rn(alpha, vv[i]));
             grid.sync();
-            spmv_rows<G, P, WIN>(a, yv, s_lo, s_hi, win, pol, [&](int64_t s, double px) {
-              const double u = sub_rn(yv[s], mul_rn(gam, px));
+            spmv_rows<G, P, WIN>(a, yv, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
+              const double u = sub_rn(xs, mul_rn(gam, px));
               uv[s] = u;
               const double w = sub_rn(wv[s], mul_rn(alpha, u));
               wv[s] = w;
-              dv[s] = add_rn(yv[s], mul_rn(coef, dv[s]));
+              dv[s] = add_rn(xs, mul_rn(coef, dv[s]));
               pw[0] = add_rn(pw[0], mul_rn(w, w));
               pw[1] = add_rn(pw[1], mul_rn(r0[s], w));
             });
@@ -352,8 +353,8 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
         }
         grid.sync();
         p2[0] = p2[1] = 0.0;
-        spmv_rows<G, P, WIN>(a, yv, s_lo, s_hi, win, pol, [&](int64_t s, double px) {
-          const double u = sub_rn(yv[s], mul_rn(gam, px));
+        spmv_rows<G, P, WIN>(a, yv, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
+          const double u = sub_rn(xs, mul_rn(gam, px));
           uv[s] = u;
           const double v = add_rn(vt[s], u);
           vv[s] = v;
@@ -384,8 +385,8 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
         if (fabs(rho) <= mul_rn(mul_rn(1e-14, rtn), est)) { brk = 1; break; }
         grid.sync();
         double p2[2] = {0.0, 0.0};
-        spmv_rows<G, P, WIN>(a, pv, s_lo, s_hi, win, pol, [&](int64_t s, double px) {
-          const double v = sub_rn(pv[s], mul_rn(gam, px));
+        spmv_rows<G, P, WIN>(a, pv, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
+          const double v = sub_rn(xs, mul_rn(gam, px));
           vv[s] = v;
           p2[0] = add_rn(p2[0], mul_rn(rt[s], v));
           p2[1] = add_rn(p2[1], mul_rn(v, v));
@@ -408,8 +409,8 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
           ++it;
           grid.sync();
           double q[1] = {0.0};
-          spmv_rows<G, P, WIN>(a, x, s_lo, s_hi, win, pol, [&](int64_t s, double px) {
-            const double ri = sub_rn(b[s], sub_rn(x[s], mul_rn(gam, px)));
+          spmv_rows<G, P, WIN>(a, x, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
+            const double ri = sub_rn(b[s], sub_rn(xs, mul_rn(gam, px)));
             r[s] = ri;
             q[0] = add_rn(q[0], mul_rn(ri, ri));
           });
@@ -431,8 +432,8 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
         }
         grid.sync();
         double p3[2] = {0.0, 0.0};
-        spmv_rows<G, P, WIN>(a, sv, s_lo, s_hi, win, pol, [&](int64_t s, double px) {
-          const double t = sub_rn(sv[s], mul_rn(gam, px));
+        spmv_rows<G, P, WIN>(a, sv, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
+          const double t = sub_rn(xs, mul_rn(gam, px));
           tv[s] = t;
           p3[0] = add_rn(p3[0], mul_rn(t, t));
           p3[1] = add_rn(p3[1], mul_rn(t, sv[s]));
@@ -477,8 +478,8 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
       ++it;
       grid.sync();
       double acc1[1] = {0.0};
-      spmv_rows<G, P, WIN>(a, x, s_lo, s_hi, win, pol, [&](int64_t s, double px) {
-        const double ri = sub_rn(b[s], sub_rn(x[s], mul_rn(gam, px)));
+      spmv_rows<G, P, WIN>(a, x, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
+        const double ri = sub_rn(b[s], sub_rn(xs, mul_rn(gam, px)));
         r[s] = ri;
         acc1[0] = add_rn(acc1[0], mul_rn(ri, ri));
       });
@@ -503,13 +504,14 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
         const double* Vj = a.V + (int64_t)j * n;
         const double* V0 = a.V;
         double p[1] = {0.0};
-        spmv_rows<G, P, WIN>(a, Vj, s_lo, s_hi, win, pol, [&](int64_t s, double px) {
-          const double wi = sub_rn(Vj[s], mul_rn(gam, px));
-          wl[s - s_lo] = wi;
-          p[0] = add_rn(p[0], mul_rn(V0[s], wi));
+        spmv_rows<G, P, WIN>(a, Vj, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
+          wl[s - s_lo] = sub_rn(xs, mul_rn(gam, px));
         });
         ++it;
         __syncthreads();  // w rows written by group leaders, read per-thread below
+        // h_0 partial in a coalesced pass (keeps dependent V0 loads out of the SpMV)
+        for (int64_t i = s_lo + tid; i < s_hi; i += nthr)
+          p[0] = add_rn(p[0], mul_rn(V0[i], wl[i - s_lo]));
         for (int l = 0; l <= j; ++l) {
           grid_allreduce<1>(p, a, slot, grid, sh);
           const double hlj = p[0];
@@ -585,8 +587,8 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
       }
       grid.sync();
       double acc1[1] = {0.0};
-      spmv_rows<G, P, WIN>(a, x, s_lo, s_hi, win, pol, [&](int64_t s, double px) {
-        const double ri = sub_rn(b[s], sub_rn(x[s], mul_rn(gam, px)));
+      spmv_rows<G, P, WIN>(a, x, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
+        const double ri = sub_rn(b[s], sub_rn(xs, mul_rn(gam, px)));
         r[s] = ri;
         acc1[0] = add_rn(acc1[0], mul_rn(ri, ri));
       });
