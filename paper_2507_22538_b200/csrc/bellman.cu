@@ -68,10 +68,15 @@ __global__ void __launch_bounds__(kK1Threads) k1_bellman(K1Args a) {
   const int m = a.m;
   double res = 0.0;
 
+  const uint32_t win_s = (uint32_t)__cvta_generic_to_shared(win);
   auto gather = [&](int c) -> double {
     if (WIN) {
       const uint64_t off = (uint64_t)((int64_t)c - w_lo);
-      if (off < (uint64_t)w_len) return win[off];
+      if (off < (uint64_t)w_len) {
+        double x;
+        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(x) : "r"(win_s + (uint32_t)off * 8u));
+        return x;
+      }
     }
     return __ldg(a.v + c);
   };
@@ -85,11 +90,13 @@ __global__ void __launch_bounds__(kK1Threads) k1_bellman(K1Args a) {
       double acc = 0.0;
       if (act < m) {
         const int64_t p0 = __ldg(a.rp + row0 + act), p1 = __ldg(a.rp + row0 + act + 1);
-        for (int64_t p = p0 + gl; p < p1; p += 4 * G) {
-          double vv[4];
-          int cc[4];
+        // long rows (G = 32, e.g. C4's ~570-entry rows): 8 loads in flight per lane
+        constexpr int U = G == 32 ? 8 : 4;
+        for (int64_t p = p0 + gl; p < p1; p += U * G) {
+          double vv[U];
+          int cc[U];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
+          for (int u = 0; u < U; ++u) {
             const int64_t q = p + (int64_t)u * G;
             if (q < p1) {
               vv[u] = ld_stream(a.val + q, pol);
@@ -99,11 +106,11 @@ __global__ void __launch_bounds__(kK1Threads) k1_bellman(K1Args a) {
               cc[u] = -1;
             }
           }
-          double xx[4];
+          double xx[U];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) xx[u] = cc[u] >= 0 ? gather(cc[u]) : 0.0;
+          for (int u = 0; u < U; ++u) xx[u] = cc[u] >= 0 ? gather(cc[u]) : 0.0;
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
+          for (int u = 0; u < U; ++u)
             if (cc[u] >= 0) acc = add_rn(acc, mul_rn(vv[u], xx[u]));
         }
       }
