@@ -124,12 +124,17 @@ def ncu_traffic():
     return None, None
 
 
-def k1_bytes(n: int, m: int, nnz: int) -> int:
+def k1_bytes(n: int, m: int, nnz: int, uniform: bool, n_v: int | None = None) -> int:
     """Algorithmic bytes of one K1 launch:
-    values+indices, row pointers (int64), stage costs, V (once), outputs
-    (applied f64 + policy i32)."""
+    values + int32 columns (12 B/nnz), stage costs (8 B/row), V once (8 B per
+    gathered-vector entry), outputs (applied f64 + policy i32 per state) and,
+    only for variable-length rows, the int64 row pointers (the uniform-row
+    kernels address row r at r*K and never read them)."""
     rows = n * m
-    return nnz * 12 + (rows + 1) * 8 + rows * 8 + n * 8 + n * 12
+    b = nnz * 12 + rows * 8 + (n_v if n_v is not None else n) * 8 + n * 12
+    if not uniform:
+        b += (rows + 1) * 8
+    return b
 
 
 # ----------------------------------------------------------------------------
@@ -348,8 +353,7 @@ def run_ours(args):
 
     # ---- roofline --------------------------------------------------------------
     nnz = plan["nnz"]
-    alg = k1_bytes(hi - lo, spec.m, nnz) + (n - (hi - lo)) * 0  # V counted once (n*8 inside)
-    alg = nnz * 12 + ((hi - lo) * spec.m + 1) * 8 + (hi - lo) * spec.m * 8 + n * 8 + (hi - lo) * 12
+    alg = k1_bytes(hi - lo, spec.m, nnz, bool(plan["uniform_rows"]), n_v=n)
     peak, peak_src = peaks()
     achieved = alg / (ms_k1 * 1e-3) / 1e9
     traffic, traffic_meta = ncu_traffic()

@@ -35,9 +35,10 @@ def peak():
     return float(json.loads(p.read_text())["hbm_gbs"]) if p.exists() else 6650.0
 
 
-def k1_bytes(n, m, nnz):
+def k1_bytes(n, m, nnz, uniform):
+    """row pointers count only for variable-length rows."""
     rows = n * m
-    return nnz * 12 + (rows + 1) * 8 + rows * 8 + n * 8 + n * 12
+    return nnz * 12 + rows * 8 + n * 8 + n * 12 + (0 if uniform else (rows + 1) * 8)
 
 
 def time_k1(mdp, reps=20):
@@ -103,7 +104,7 @@ def main():
         plan = mdp.plan()
         nnz = plan["nnz"]
         t1 = time_k1(mdp)
-        b1 = k1_bytes(mdp.n, mdp.m, nnz)
+        b1 = k1_bytes(mdp.n, mdp.m, nnz, bool(plan["uniform_rows"]))
         rec = {"config": spec.name, "n": mdp.n, "m": mdp.m, "nnz": nnz, "build_s": t_build,
                "plan": plan, "k1_ms": t1 * 1e3, "k1_bytes": b1, "k1_gbs": b1 / t1 / 1e9,
                "k1_frac": b1 / t1 / 1e9 / peak(), "backups_per_s": mdp.n * mdp.m / t1,
@@ -119,7 +120,7 @@ def main():
                                  ipi.Mode.MIN)
         p_pi = ipi.gather_policy_matrix(mdp, pi.long())
         t3 = time_apply(p_pi, spec.gamma)
-        b3 = p_pi.nnz * 12 + (mdp.n + 1) * 8 + mdp.n * 16
+        b3 = p_pi.nnz * 12 + (mdp.n + 1) * 8 + mdp.n * 16  # standalone K3 reads row_ptr
         rec.update({"k3_ms": t3 * 1e3, "k3_bytes": b3, "k3_gbs": b3 / t3 / 1e9,
                     "k3_frac": b3 / t3 / 1e9 / peak(), "nnz_pi": p_pi.nnz})
         del p_pi
