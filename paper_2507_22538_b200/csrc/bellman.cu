@@ -421,6 +421,183 @@ __global__ void __launch_bounds__(kK1Threads, 2) k1_bellman_flat(K1Args a, int K
   }
 }
 
+// ---------------------------------------------------------------------------
+// Deep-pipeline uniform kernel: 16 warps per SM with up to 128 registers each
+// (one 512-thread CTA per SM, one V window per SM).  Bytes in flight are
+// bounded by registers, so fewer warps with deeper rings beat many shallow
+// warps: a ring of 4 CSR batches (values/columns/cost of batch b+3 are issued
+// while b is reduced) and a ring of 2 gather batches (V gathers of b+1 are
+// issued before b is reduced), indices resolved at compile time (loop unrolled
+// by 4) so no register copy waits on an outstanding load.
+// ---------------------------------------------------------------------------
+template <int P>
+struct DeepCsr {
+  double2 v[P];
+  int2 c[P];
+  double g;
+};
+
+template <int G, int P, bool WIN>
+__global__ void __launch_bounds__(kK1Threads, 1) k1_bellman_deep(K1Args a, int K) {
+  extern __shared__ double win[];
+  __shared__ double red[32];
+  const int64_t s_lo = a.bounds[blockIdx.x], s_hi = a.bounds[blockIdx.x + 1];
+  int w_lo = 0;
+  uint32_t w_len = 0;
+  if (WIN) {
+    int64_t lo = a.state0 + s_lo - a.halo;
+    int64_t hi = a.state0 + s_hi + a.halo;
+    lo = lo < 0 ? 0 : lo;
+    hi = hi > a.n_global ? a.n_global : hi;
+    w_lo = (int)lo;
+    w_len = hi > lo ? (uint32_t)(hi - lo) : 0u;
+    for (uint32_t i = threadIdx.x; i < w_len; i += blockDim.x) win[i] = __ldg(a.v + lo + i);
+    __syncthreads();
+  }
+  const uint32_t win_s = (uint32_t)__cvta_generic_to_shared(win);
+  const uint64_t pol = policy_evict_first();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  constexpr int GPW = 32 / G;
+  const int grp = lane / G, gl = lane % G;
+  const bool mx = a.maximize != 0;
+  const int m = a.m;
+  const int nit = (m + GPW - 1) / GPW;
+  const int pairs = K >> 1;
+  double res = 0.0;
+
+  auto gather = [&](int c) -> double {
+    if (WIN) {
+      const uint32_t off = (uint32_t)(c - w_lo);
+      if (off < w_len) {
+        double x;
+        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(x) : "r"(win_s + off * 8u));
+        return x;
+      }
+    }
+    return __ldg(a.v + c);
+  };
+  auto load = [&](int64_t s, int it, DeepCsr<P>& b) {
+    const int act = it * GPW + grp;
+    const bool ok = s < s_hi && act < m;
+    const int64_t row = s * (int64_t)m + act;
+    const double* vp = a.val + row * K;
+    const int* cp = a.col + row * K;
+#pragma unroll
+    for (int t = 0; t < P; ++t) {
+      const int j = gl + G * t;
+      if (ok && j < pairs) {
+        b.v[t] = ld_stream_v2(vp + 2 * j, pol);
+        b.c[t] = ld_stream_v2(cp + 2 * j, pol);
+      } else {
+        b.v[t] = make_double2(0.0, 0.0);
+        b.c[t] = make_int2(-1, -1);
+      }
+    }
+    b.g = ok ? __ldg(a.cost + row) : 0.0;
+  };
+  auto gather_batch = [&](const DeepCsr<P>& b, double2 (&x)[P]) {
+#pragma unroll
+    for (int t = 0; t < P; ++t)
+      x[t] = make_double2(b.c[t].x >= 0 ? gather(b.c[t].x) : 0.0,
+                          b.c[t].y >= 0 ? gather(b.c[t].y) : 0.0);
+  };
+  // flattened (state, row-step) coordinates of batch k after the current one
+  auto advance = [&](int64_t& s, int& it) {
+    if (++it == nit) {
+      it = 0;
+      s += nwarps;
+    }
+  };
+
+  int64_t sC = s_lo + warp;
+  if (sC < s_hi) {
+    int itC = 0;
+    // coordinates of batches b+1 (gather stage) and b+3 (load stage)
+    int64_t s1 = sC, s3;
+    int it1 = 0, it3;
+    advance(s1, it1);
+    s3 = s1;
+    it3 = it1;
+    advance(s3, it3);
+    DeepCsr<P> R[4];
+    double2 X[2][P];
+    {
+      int64_t s2 = s3;
+      int i2 = it3;
+      load(sC, itC, R[0]);
+      load(s1, it1, R[1]);
+      load(s2, i2, R[2]);
+      advance(s3, it3);
+    }
+    gather_batch(R[0], X[0]);
+    double bq = mx ? -INFINITY : INFINITY;
+    int ba = INT_MAX;
+    bool live = true;
+    while (live) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (live) {
+          load(s3, it3, R[(u + 3) & 3]);                // predicated off past s_hi
+          const bool has1 = s1 < s_hi;
+          if (has1) gather_batch(R[(u + 1) & 3], X[(u + 1) & 1]);
+          double acc = 0.0;
+#pragma unroll
+          for (int t = 0; t < P; ++t) {
+            acc = add_rn(acc, mul_rn(R[u].v[t].x, X[u & 1][t].x));
+            acc = add_rn(acc, mul_rn(R[u].v[t].y, X[u & 1][t].y));
+          }
+          acc = group_sum<G>(acc);
+          const int act = itC * GPW + grp;
+          if (act < m) {
+            const double q = add_rn(R[u].g, mul_rn(a.gamma, acc));
+            if (better(q, act, bq, ba, mx)) {
+              bq = q;
+              ba = act;
+            }
+          }
+          if (itC == nit - 1) {
+#pragma unroll
+            for (int off = 16; off >= G; off >>= 1) {
+              const double oq = __shfl_xor_sync(kFull, bq, off);
+              const int oa = __shfl_xor_sync(kFull, ba, off);
+              if (better(oq, oa, bq, ba, mx)) {
+                bq = oq;
+                ba = oa;
+              }
+            }
+            if (ba == INT_MAX) ba = 0;
+            if (lane == 0) {
+              const int64_t row0 = sC * (int64_t)m;
+              a.policy[sC] = ba;
+              a.applied[sC] = bq;
+              if (a.gpi) a.gpi[sC] = __ldg(a.cost + row0 + ba);
+              if (a.lenpi) a.lenpi[sC] = K;
+              res = fmax(res, fabs(sub_rn(gather((int)(a.state0 + sC)), bq)));
+            }
+            bq = mx ? -INFINITY : INFINITY;
+            ba = INT_MAX;
+          }
+          live = has1;
+          sC = s1;
+          itC = it1;
+          advance(s1, it1);
+          advance(s3, it3);
+        }
+      }
+    }
+  }
+  if (a.res_bits) {
+    res = warp_max(res);
+    if (lane == 0) red[warp] = res;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < nwarps; ++w) t = fmax(t, red[w]);
+      atomicMax(a.res_bits, (unsigned long long)__double_as_longlong(t));
+    }
+  }
+}
+
 // (G, P) for the uniform path: pairs = K/2 <= P*G, P = 2 (or 4 for very long rows)
 bool uniform_shape(int K, int* G, int* P) {
   if (K <= 0 || (K & 1)) return false;
@@ -445,6 +622,9 @@ static void launch_u(const K1Args& a, int K, bool win, int blocks, int smem, cud
 
 template <int G, int P>
 static cudaError_t set_smem_attr_u(int smem) {
+  cudaError_t e = cudaFuncSetAttribute(k1_bellman_deep<G, P, true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(k1_bellman_uniform<G, P, true>,
                               cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
 }
@@ -549,6 +729,16 @@ int launch_bellman(ipi_mdp* h, const double* v_full, int32_t mode, int32_t* poli
   const bool win = h->plan.halo >= 0;
   const int blocks = h->plan.k1_blocks, smem = h->plan.k1_smem_bytes;
   int G = 0, P = 0;
+  if (h->plan.k1_variant == 3 && uniform_shape(h->plan.row_len_max, &G, &P)) {
+    const int K = h->plan.row_len_max;
+#define IPI_D_LAUNCH(GG, PP)                                                             \
+  (win ? k1_bellman_deep<GG, PP, true><<<blocks, kK1Threads, smem, st>>>(a, K)            \
+       : k1_bellman_deep<GG, PP, false><<<blocks, kK1Threads, 0, st>>>(a, K))
+    IPI_DISPATCH_UNIFORM(G, P, IPI_D_LAUNCH);
+#undef IPI_D_LAUNCH
+    IPI_LAUNCH_CHECK();
+    return IPI_OK;
+  }
   if (h->plan.uniform_rows && h->plan.row_len_max <= 4 && (h->plan.row_len_max % 2) == 0) {
     const int K = h->plan.row_len_max;
     if (win)

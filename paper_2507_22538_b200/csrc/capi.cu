@@ -356,6 +356,40 @@ int ipi_mdp_create(const int64_t* row_ptr, const int32_t* col, const double* val
   p.inner_smem_bytes = 0;
   int Gu = 0, Pu = 0;
   p.k1_variant = (p.uniform_rows && uniform_shape(p.row_len_max, &Gu, &Pu)) ? 1 : 0;
+  // ---- deep-pipeline uniform kernel: one 512-thread CTA per SM ---------------
+  {
+    const char* env = getenv("IPI_K1_DEEP");
+    const bool allow = env && env[0] == '1';
+    if (allow && p.k1_variant == 1 && p.row_len_max > 4 && n_local > 0) {
+      const int blocks = (int)std::min<int64_t>(h->num_sms, std::max<int64_t>(1, (n_local + 15) / 16));
+      std::vector<int64_t> hb(blocks + 1);
+      for (int c = 0; c <= blocks; ++c) hb[c] = (int64_t)((double)n_local * c / blocks);
+      hb[blocks] = n_local;
+      int64_t worst = 0;
+      for (int c = 0; c < blocks; ++c) worst = std::max<int64_t>(worst, hb[c + 1] - hb[c]);
+      int smem = 0;
+      int halo = p.halo;
+      if (halo >= 0) {
+        const int64_t wlen = std::min<int64_t>(n_global, worst + 2 * (int64_t)halo);
+        if (wlen * 8 + 1024 <= 200 * 1024) smem = (int)(wlen * 8 + 1024);
+        else halo = -1;
+      }
+      int64_t* db = nullptr;
+      if (cudaMalloc(&db, sizeof(int64_t) * (blocks + 1)) == cudaSuccess &&
+          cudaMemcpy(db, hb.data(), sizeof(int64_t) * (blocks + 1), cudaMemcpyHostToDevice) ==
+              cudaSuccess &&
+          (smem == 0 || k1_set_smem(p.lanes_per_row, smem) == IPI_OK)) {
+        cudaFree(h->k1_bounds);
+        h->k1_bounds = db;
+        p.k1_blocks = blocks;
+        p.k1_smem_bytes = smem;
+        p.halo = halo;
+        p.k1_variant = 3;
+      } else if (db) {
+        cudaFree(db);
+      }
+    }
+  }
   // ---- TMA ring plan for uniform rows (one persistent CTA per SM) ------------
   {
     // Experimental: off unless IPI_K1_TMA=1.  Measured on C2
