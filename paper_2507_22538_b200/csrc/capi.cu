@@ -198,6 +198,8 @@ static int ensure_scratch(ipi_mdp* h) {
   IPI_CUDA_TRY(cudaMalloc(&h->res_bits, sizeof(unsigned long long) * 2));
   IPI_CUDA_TRY(cudaMalloc(&h->xbuf, sizeof(double) * n));
   IPI_CUDA_TRY(cudaMalloc(&h->d_report, sizeof(ipi_inner_report)));
+  h->kry_len = krylov_workspace_doubles(n);
+  IPI_CUDA_TRY(cudaMalloc(&h->kry, sizeof(double) * h->kry_len));
   const int64_t cap = std::max<int64_t>((int64_t)h->plan.row_len_max * h->n_local, 1);
   IPI_CUDA_TRY(cudaMalloc(&h->rp_pi, sizeof(int64_t) * (n + 1)));
   IPI_CUDA_TRY(cudaMalloc(&h->col_pi, sizeof(int32_t) * cap));
@@ -454,6 +456,7 @@ void ipi_mdp_destroy(ipi_mdp* h) {
   cudaFree(h->xbuf);
   cudaFree(h->scan_tmp);
   cudaFree(h->d_report);
+  cudaFree(h->kry);
   if (h->host_pinned) cudaFreeHost(h->host_pinned);
   delete h;
 }
@@ -752,7 +755,8 @@ int ipi_solve(ipi_mdp* h, const ipi_opts* o, double* v, int32_t* policy, double*
     IPI_CUDA_TRY(cudaMemcpyAsync(vnext, vcur, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
     rc = inner_solve(h->rp_pi, h->col_pi, h->val_pi, n, h->gamma, h->gpi, vnext, target, cap,
                      o->ksp_type, o->richardson_scale, h->plan.lanes_per_row, h->plan.halo,
-                     h->plan.uniform_rows ? h->plan.row_len_max : 0, h->d_report, st);
+                     h->plan.uniform_rows ? h->plan.row_len_max : 0, h->d_report, st, h->kry,
+                     h->kry_len);
     if (rc) return rc;
     if (o->ksp_type == IPI_KSP_TFQMR || o->ksp_type == IPI_KSP_BICGSTAB) {
       // these kinds can break down: read the report now (driver.py:189-193)

@@ -31,6 +31,8 @@ struct ipi_mdp {
   int64_t cap_pi = 0;
   double* xbuf = nullptr;
   int64_t* scan_tmp = nullptr;
+  double* kry = nullptr;        // per-handle Krylov workspace (ipi_solve)
+  int64_t kry_len = 0;
   int64_t scan_tmp_len = 0;
   ipi_inner_report* d_report = nullptr;
   void* host_pinned = nullptr;  // small pinned staging area
@@ -103,7 +105,12 @@ int launch_spmv(const int64_t* rp, const int32_t* col, const double* val, int64_
 int inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi, int64_t n,
                 double gamma, const double* b, double* x, double target, int32_t max_it,
                 int32_t kind, double scale, int lanes, int halo, int uniform_K,
-                ipi_inner_report* d_report, cudaStream_t st);
+                ipi_inner_report* d_report, cudaStream_t st, double* workspace = nullptr,
+                int64_t workspace_doubles = 0);
+// doubles of Krylov workspace inner_solve needs for an n-row system
+inline int64_t krylov_workspace_doubles(int64_t n) {
+  return (int64_t)(kGmresRestart + 1) * n + 2 * n + 4 * 1024;
+}
 
 // device scratch arena for the inner solver (per device, grown on demand)
 double* krylov_workspace(int64_t n, int64_t doubles_needed);

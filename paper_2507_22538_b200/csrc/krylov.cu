@@ -55,7 +55,8 @@ double* krylov_workspace(int64_t /*n*/, int64_t doubles_needed) {
 int inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi, int64_t n,
                 double gamma, const double* b, double* x, double target, int32_t max_it,
                 int32_t kind, double scale, int lanes, int halo, int uniform_K,
-                ipi_inner_report* d_report, cudaStream_t st) {
+                ipi_inner_report* d_report, cudaStream_t st, double* workspace,
+                int64_t workspace_doubles) {
   if (kind < IPI_KSP_RICHARDSON || kind > IPI_KSP_TFQMR)
     return fail(IPI_EVALIDATION, "unknown inner solver kind " + std::to_string(kind));
   if (max_it < 1) return fail(IPI_EVALIDATION, "iteration cap must be >= 1, got " + std::to_string(max_it));
@@ -68,7 +69,9 @@ int inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_p
   int blocks = sms;
   if ((int64_t)blocks * 32 > n) blocks = (int)std::max<int64_t>(1, n / 32);
   const int64_t need = (int64_t)(R + 1) * n + 2 * n + 4 * (int64_t)blocks;
-  double* ws = krylov_workspace(n, need);
+  // caller-owned workspace (per handle, so concurrent handles never share it)
+  // or the per-device arena used by the standalone API
+  double* ws = (workspace && workspace_doubles >= need) ? workspace : krylov_workspace(n, need);
   if (!ws) return fail(IPI_ERESOURCE, "cannot allocate Krylov workspace of " + std::to_string(need * 8) + " bytes");
   KArgs a;
   a.rp = rp_pi;

@@ -58,17 +58,24 @@ class CsrMatrix:
             return [f"negative shape ({rows}, {cols})"]
         rp = _to_dev(row_ptr, torch.int64).reshape(-1)
         vals = _to_dev(values, torch.float64).reshape(-1)
-        ci_src = col_idx if isinstance(col_idx, torch.Tensor) else np.asarray(col_idx)
-        ci_wide = _to_dev(ci_src, torch.int64).reshape(-1)
+        narrow = isinstance(col_idx, torch.Tensor) and col_idx.dtype == torch.int32
+        if narrow:  # already the device layout: no int64 round trip (2^31-nnz shards)
+            ci_wide = None
+            ci = _to_dev(col_idx, torch.int32).reshape(-1)
+        else:
+            ci_src = col_idx if isinstance(col_idx, torch.Tensor) else np.asarray(col_idx)
+            ci_wide = _to_dev(ci_src, torch.int64).reshape(-1)
         problems: list[str] = []
         self.row_ptr, self.values = rp, vals
         if rp.shape[0] != rows + 1:
-            self.col_idx = ci_wide.to(torch.int32)
+            self.col_idx = ci if narrow else ci_wide.to(torch.int32)
             return [f"row_ptr length {rp.shape[0]} != rows+1 = {rows + 1}"]
         if cols > np.iinfo(np.int32).max:
             raise DimensionError("column count exceeds the int32 index range of the device layout")
-        # narrowing to int32 keeps order; anything beyond int32 is out of range anyway
-        ci = ci_wide.clamp(-(2 ** 31), 2 ** 31 - 1).to(torch.int32)
+        if not narrow:
+            # narrowing to int32 keeps order; anything beyond int32 is out of range anyway
+            ci = ci_wide.clamp(-(2 ** 31), 2 ** 31 - 1).to(torch.int32)
+            del ci_wide
         self.col_idx = ci
         rep = _lib.CsrReport()
         _lib.check(_lib.lib().ipi_csr_check(_lib.ptr(rp), _lib.ptr(ci), _lib.ptr(vals), rows, cols,
