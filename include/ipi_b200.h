@@ -159,7 +159,7 @@ int ipi_validate(ipi_mdp* h, ipi_validation* out, void* stream);
  * (driver.py:136).  v_full: n_global values.  policy int32[n_local],
  * applied f64[n_local]; g_pi / len_pi / res_inf_bits nullable.  res_inf_bits
  * is an 8-byte device word receiving the max via integer atomicMax on the
- * IEEE bits of |v-applied| (>= 0); the caller zeroes it. */
+ * IEEE bits of |v-applied| (>= 0); ipi_bellman zeroes it first (memset). */
 int ipi_bellman(ipi_mdp* h, const double* v_full, int32_t mode, int32_t* policy, double* applied,
                 double* g_pi, int32_t* len_pi, unsigned long long* res_inf_bits, void* stream);
 

@@ -580,6 +580,8 @@ int ipi_validate(ipi_mdp* h, ipi_validation* out, void* stream) {
 int ipi_bellman(ipi_mdp* h, const double* v_full, int32_t mode, int32_t* policy, double* applied,
                 double* g_pi, int32_t* len_pi, unsigned long long* res_inf_bits, void* stream) {
   if (!h) return fail(IPI_EVALIDATION, "null handle");
+  if (res_inf_bits)  // zeroed here (a memset, not a kernel) so callers cannot forget
+    IPI_CUDA_TRY(cudaMemsetAsync(res_inf_bits, 0, sizeof(unsigned long long), (cudaStream_t)stream));
   return launch_bellman(h, v_full, mode, policy, applied, g_pi, len_pi, res_inf_bits,
                         (cudaStream_t)stream);
 }

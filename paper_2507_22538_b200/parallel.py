@@ -148,8 +148,6 @@ class MdpShard:
 
     def bellman(self, v_full: torch.Tensor, *, residual: bool = True, stream=None):
         """K1 over the local rows with the full V; returns (policy, applied, res_bits)."""
-        if residual:
-            self.res_bits.zero_()
         _lib.check(_lib.lib().ipi_bellman(
             self._handle, _lib.ptr(v_full), _lib.MODE_MAX if self.mode is Mode.MAX else _lib.MODE_MIN,
             _lib.ptr(self.policy), _lib.ptr(self.applied), None, None,
