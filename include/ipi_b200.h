@@ -46,6 +46,10 @@ extern "C" {
 #define IPI_KSP_BICGSTAB 2
 #define IPI_KSP_TFQMR 3
 
+/* preconditioners on the device path (inner.py:65-84, 113-118) */
+#define IPI_PC_NONE 0
+#define IPI_PC_JACOBI 1
+
 /* outer status (driver.py:41-44) */
 #define IPI_CONVERGED 0
 #define IPI_OUTER_CAP 1
@@ -73,7 +77,7 @@ typedef struct {
   int32_t ksp_max_it;      /* -ksp_max_it, <=0 = unset */
   double richardson_scale; /* -ksp_richardson_scale */
   int32_t mode;            /* IPI_MODE_* */
-  int32_t pad;
+  int32_t pc_type;         /* -pc_type: IPI_PC_NONE or IPI_PC_JACOBI */
 } ipi_opts;
 
 /* Solve statistics (driver.py:93-106 SolveResult minus the arrays). */
@@ -184,12 +188,17 @@ int ipi_apply_J_shard(const int64_t* rp_pi, const int32_t* col_pi, const double*
                       const double* b, double* y, void* stream);
 
 /* ---- K4: policy evaluation (inner.py:163-292) ------------------------- */
+/* Jacobi preconditioner of I - gamma P_pi: inv_diag[s] = 1/(1 - gamma P_pi[s,s])
+ * (build_preconditioner JACOBI, inner.py:115-118). */
+int ipi_jacobi_inv_diag(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi,
+                        int64_t n, double gamma, double* inv_diag, void* stream);
 /* Solve (I - gamma P_pi) x = b from x (in/out) to the floored 2-norm target
- * or max_it iterations, one persistent cooperative kernel per call. */
+ * or max_it iterations, one persistent cooperative kernel per call.
+ * inv_diag == NULL: pc = identity; else left Jacobi preconditioning. */
 int ipi_inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi, int64_t n,
                     double gamma, const double* b, double* x, double target_2norm,
                     int32_t max_it, int32_t kind, double richardson_scale,
-                    ipi_inner_report* report, void* stream);
+                    const double* inv_diag, ipi_inner_report* report, void* stream);
 
 /* ---- outer iPI loop (driver.py:109-209) ------------------------------- */
 /* v (device, n) holds V0 on entry and the final V on exit; policy (device,

@@ -128,8 +128,26 @@ class InnerReport:
     target_2norm: float
 
 
-def _richardson(apply_a, b, theta0, eff, max_it, scale):
-    """inner.py:216-226 (pc = identity)."""
+def _identity(r):
+    return r
+
+
+def jacobi(rp_pi, col_pi, val_pi, gamma):
+    """Jacobi preconditioner of I - gamma P_pi (inner.py:115-118; diagonal as
+    CsrMatrix.diagonal, sparse.py:102-109)."""
+    rp = np.asarray(rp_pi, dtype=np.int64)
+    n = rp.shape[0] - 1
+    d = np.zeros(n)
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(rp))
+    col = np.asarray(col_pi, dtype=np.int64)
+    mask = rows == col
+    d[col[mask]] = np.asarray(val_pi)[mask]
+    inv_diag = 1.0 / (1.0 - gamma * d)
+    return lambda r: r * inv_diag
+
+
+def _richardson(apply_a, b, theta0, eff, max_it, scale, pc=_identity):
+    """inner.py:216-226."""
     theta = theta0.copy()
     it = 0
     while True:
@@ -137,7 +155,7 @@ def _richardson(apply_a, b, theta0, eff, max_it, scale):
         rn = norm2(r)
         if rn <= eff or it >= max_it or not math.isfinite(rn):
             break
-        theta = theta + scale * r
+        theta = theta + scale * pc(r)
         it += 1
     return theta, it, rn, False
 
@@ -152,7 +170,7 @@ def _back_substitute(r_mat, rhs):
     return y
 
 
-def _gmres(apply_a, b, theta0, eff, max_it):
+def _gmres(apply_a, b, theta0, eff, max_it, pc=_identity):
     """Restarted GMRES(30), MGS, Givens, estimate-then-verify (inner.py:229-283)."""
     x = theta0.copy()
     it = 0
@@ -162,7 +180,7 @@ def _gmres(apply_a, b, theta0, eff, max_it):
     n = x.shape[0]
     R = GMRES_RESTART
     while rn > eff and it < max_it:
-        z = r
+        z = pc(r)
         beta = norm2(z)
         if beta == 0.0 or not math.isfinite(beta):
             break
@@ -175,7 +193,7 @@ def _gmres(apply_a, b, theta0, eff, max_it):
         g[0] = beta
         j = 0
         while j < R and it < max_it:
-            w = apply_a(V[j])
+            w = pc(apply_a(V[j]))
             it += 1
             for l in range(j + 1):
                 H[l, j] = dot(V[l], w)
@@ -216,7 +234,7 @@ def _tighten(est, eff, rn, current):
     return min(current, est * (eff / rn) * 0.5)
 
 
-def _bicgstab(apply_a, b, theta0, eff, max_it):
+def _bicgstab(apply_a, b, theta0, eff, max_it, pc=_identity):
     """BiCGStab with estimate-then-verify stopping (inner.py:295-373), pc = identity."""
     x = theta0.copy()
     r_true = b - apply_a(x)
@@ -225,7 +243,7 @@ def _bicgstab(apply_a, b, theta0, eff, max_it):
     breakdown = False
     if rn <= eff:
         return x, it, rn, breakdown
-    r = np.array(r_true, dtype=np.float64, copy=True)
+    r = np.array(pc(r_true), dtype=np.float64, copy=True)
     rtilde = r.copy()
     rtilde_norm = norm2(rtilde)
     rho = dot(rtilde, r)
@@ -237,7 +255,7 @@ def _bicgstab(apply_a, b, theta0, eff, max_it):
         if abs(rho) <= 1e-14 * rtilde_norm * est:
             breakdown = True
             break
-        v = apply_a(p)
+        v = pc(apply_a(p))
         sigma = dot(rtilde, v)
         if abs(sigma) <= 1e-14 * rtilde_norm * norm2(v):
             breakdown = True
@@ -254,14 +272,14 @@ def _bicgstab(apply_a, b, theta0, eff, max_it):
             if rn <= eff:
                 break
             est_target = _tighten(s_norm, eff, rn, est_target)
-            r = np.array(r_true, dtype=np.float64, copy=True)
+            r = np.array(pc(r_true), dtype=np.float64, copy=True)
             rtilde = r.copy()
             rtilde_norm = norm2(rtilde)
             rho = dot(rtilde, r)
             p = r.copy()
             est = norm2(r)
             continue
-        t = apply_a(s)
+        t = pc(apply_a(s))
         tt = dot(t, t)
         if tt == 0.0:
             breakdown = True
@@ -297,7 +315,7 @@ def _bicgstab(apply_a, b, theta0, eff, max_it):
     return x, it, rn, breakdown
 
 
-def _tfqmr(apply_a, b, theta0, eff, max_it):
+def _tfqmr(apply_a, b, theta0, eff, max_it, pc=_identity):
     """Transpose-free QMR with estimate-then-verify stopping (inner.py:376-450)."""
     x = theta0.copy()
     r_true = b - apply_a(x)
@@ -306,11 +324,11 @@ def _tfqmr(apply_a, b, theta0, eff, max_it):
     breakdown = False
     if rn <= eff:
         return x, it, rn, breakdown
-    r0 = np.array(r_true, dtype=np.float64, copy=True)
+    r0 = np.array(pc(r_true), dtype=np.float64, copy=True)
     w = r0.copy()
     y = r0.copy()
     d = np.zeros_like(r0)
-    u = apply_a(y)
+    u = pc(apply_a(y))
     v = u.copy()
     tau = norm2(r0)
     r0_norm = tau
@@ -332,7 +350,7 @@ def _tfqmr(apply_a, b, theta0, eff, max_it):
         for half in (1, 2):
             if half == 2:
                 y = y - alpha * v
-                u = apply_a(y)
+                u = pc(apply_a(y))
             w = w - alpha * u
             d = y + (theta_q * theta_q * eta / alpha) * d
             if tau == 0.0:
@@ -367,7 +385,7 @@ def _tfqmr(apply_a, b, theta0, eff, max_it):
         rho = rho_new
         y = w + beta * y
         v = beta * u + beta * beta * v
-        u = apply_a(y)
+        u = pc(apply_a(y))
         v = v + u
     if stale or breakdown:
         r_true = b - apply_a(x)
@@ -376,8 +394,8 @@ def _tfqmr(apply_a, b, theta0, eff, max_it):
 
 
 def inner_solve(rp_pi, col_pi, val_pi, gamma, b, theta0, target, max_it,
-                kind="gmres", richardson_scale=1.0):
-    """Floor the target, dispatch, report (inner.py:163-213); pc = NONE."""
+                kind="gmres", richardson_scale=1.0, pc="none"):
+    """Floor the target, dispatch, report (inner.py:163-213); pc none | jacobi."""
     b = np.asarray(b, dtype=np.float64)
     theta0 = np.asarray(theta0, dtype=np.float64)
     if max_it < 1:
@@ -386,14 +404,15 @@ def inner_solve(rp_pi, col_pi, val_pi, gamma, b, theta0, target, max_it,
         raise ValueError(f"residual target must be >= 0, got {target}")
     eff = max(target, TARGET_FLOOR_SCALE * max(1.0, norm2(b)))
     apply_a = lambda x: apply_J(rp_pi, col_pi, val_pi, gamma, x)  # noqa: E731
+    P = jacobi(rp_pi, col_pi, val_pi, gamma) if pc == "jacobi" else _identity
     if kind == "richardson":
-        theta, its, rn, broke = _richardson(apply_a, b, theta0, eff, max_it, richardson_scale)
+        theta, its, rn, broke = _richardson(apply_a, b, theta0, eff, max_it, richardson_scale, P)
     elif kind == "gmres":
-        theta, its, rn, broke = _gmres(apply_a, b, theta0, eff, max_it)
+        theta, its, rn, broke = _gmres(apply_a, b, theta0, eff, max_it, P)
     elif kind == "tfqmr":
-        theta, its, rn, broke = _tfqmr(apply_a, b, theta0, eff, max_it)
+        theta, its, rn, broke = _tfqmr(apply_a, b, theta0, eff, max_it, P)
     elif kind == "bicgstab":
-        theta, its, rn, broke = _bicgstab(apply_a, b, theta0, eff, max_it)
+        theta, its, rn, broke = _bicgstab(apply_a, b, theta0, eff, max_it, P)
     else:
         raise ValueError(f"oracle has no inner solver {kind!r}")
     return theta, InnerReport(its, rn, bool(rn <= eff) and not broke, broke, eff)
@@ -415,7 +434,7 @@ class OracleResult:
 
 def solve(row_ptr, col, val, cost, gamma, *, maximize=False, tol=1e-8, alpha=1e-4,
           max_outer=1000, max_inner=1000, kind="gmres", ksp_max_it=None,
-          richardson_scale=1.0, v0=None) -> OracleResult:
+          richardson_scale=1.0, v0=None, pc="none") -> OracleResult:
     """Algorithm 1: greedy -> inf-norm residual -> tests -> gather -> inner solve.
 
     Mirrors driver.py:117-209: history appended before the tests; CONVERGED,
@@ -452,7 +471,7 @@ def solve(row_ptr, col, val, cost, gamma, *, maximize=False, tol=1e-8, alpha=1e-
         else:
             target, cap = alpha * res, max_inner
         theta, rep = inner_solve(rp_pi, col_pi, val_pi, gamma, g_pi, v, target, cap,
-                                 kind, richardson_scale)
+                                 kind, richardson_scale, pc)
         inner_total += rep.iterations
         if rep.breakdown:
             theta = g_pi + gamma * spmv(rp_pi, col_pi, val_pi, v)

@@ -20,6 +20,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libipi_b200.so"
 IPI_OK, IPI_EVALIDATION, IPI_EDIMENSION, IPI_ECUDA, IPI_ERESOURCE = 0, 1, 2, 3, 4
 MODE_MIN, MODE_MAX = 0, 1
 KSP = {"richardson": 0, "gmres": 1, "bicgstab": 2, "tfqmr": 3}
+PC = {"none": 0, "jacobi": 1}
 STATUS = {0: "converged", 1: "outer_cap", 2: "stalled"}
 
 _p = C.c_void_p
@@ -36,7 +37,7 @@ class InnerReport(C.Structure):
 class Opts(C.Structure):
     _fields_ = [("tol", _f64), ("alpha", _f64), ("max_outer", _i32), ("max_inner", _i32),
                 ("ksp_type", _i32), ("ksp_max_it", _i32), ("richardson_scale", _f64),
-                ("mode", _i32), ("pad", _i32)]
+                ("mode", _i32), ("pc_type", _i32)]
 
 
 class Stats(C.Structure):
@@ -86,7 +87,8 @@ _SIGS = {
     "ipi_spmv": (C.c_int, [_p, _p, _p, _i64, _i64, _p, _p, _p]),
     "ipi_apply_J": (C.c_int, [_p, _p, _p, _i64, _f64, _p, _p, _p, _p]),
     "ipi_apply_J_shard": (C.c_int, [_p, _p, _p, _i64, _i64, _f64, _p, _p, _p, _p]),
-    "ipi_inner_solve": (C.c_int, [_p, _p, _p, _i64, _f64, _p, _p, _f64, _i32, _i32, _f64,
+    "ipi_jacobi_inv_diag": (C.c_int, [_p, _p, _p, _i64, _f64, _p, _p]),
+    "ipi_inner_solve": (C.c_int, [_p, _p, _p, _i64, _f64, _p, _p, _f64, _i32, _i32, _f64, _p,
                                   C.POINTER(InnerReport), _p]),
     "ipi_solve": (C.c_int, [_p, C.POINTER(Opts), _p, _p, _p, _i32, C.POINTER(Stats), _p]),
     "ipi_gen_locality": (C.c_int, [_i64, _i32, _i32, _i64, C.c_uint64, _i64, _i64, _p, _p, _p,

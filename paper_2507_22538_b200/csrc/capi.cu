@@ -457,6 +457,7 @@ void ipi_mdp_destroy(ipi_mdp* h) {
   cudaFree(h->scan_tmp);
   cudaFree(h->d_report);
   cudaFree(h->kry);
+  cudaFree(h->invd);
   if (h->host_pinned) cudaFreeHost(h->host_pinned);
   delete h;
 }
@@ -635,10 +636,16 @@ int ipi_apply_J_shard(const int64_t* rp_pi, const int32_t* col_pi, const double*
                      state0);
 }
 
+int ipi_jacobi_inv_diag(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi,
+                        int64_t n, double gamma, double* inv_diag, void* stream) {
+  if (!inv_diag) return fail(IPI_EVALIDATION, "null output");
+  return jacobi_inv_diag(rp_pi, col_pi, val_pi, n, gamma, inv_diag, (cudaStream_t)stream);
+}
+
 int ipi_inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi, int64_t n,
                     double gamma, const double* b, double* x, double target_2norm,
                     int32_t max_it, int32_t kind, double richardson_scale,
-                    ipi_inner_report* report, void* stream) {
+                    const double* inv_diag, ipi_inner_report* report, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (n <= 0) return fail(IPI_EDIMENSION, "empty system");
   int64_t nnz = 0;
@@ -655,7 +662,7 @@ int ipi_inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* v
   IPI_CUDA_TRY(cudaMalloc(&d_rep, sizeof(ipi_inner_report)));
   rc = inner_solve(rp_pi, col_pi, val_pi, n, gamma, b, x, target_2norm, max_it, kind,
                    richardson_scale, pl.lanes_per_row, pl.halo,
-                   pl.uniform_rows ? pl.row_len_max : 0, d_rep, st);
+                   pl.uniform_rows ? pl.row_len_max : 0, d_rep, st, nullptr, 0, inv_diag);
   if (rc == IPI_OK && report) {
     cudaError_t e = cudaMemcpyAsync(report, d_rep, sizeof(*report), cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
@@ -676,6 +683,8 @@ int ipi_solve(ipi_mdp* h, const ipi_opts* o, double* v, int32_t* policy, double*
   if (!(o->alpha > 0.0 && o->alpha < 1.0)) return fail(IPI_EVALIDATION, "alpha must lie in (0, 1)");
   if (o->max_outer < 1 || o->max_inner < 1) return fail(IPI_EVALIDATION, "iteration caps must be >= 1");
   if (hist_cap < 1) return fail(IPI_EVALIDATION, "history capacity must be >= 1");
+  if (o->pc_type != IPI_PC_NONE && o->pc_type != IPI_PC_JACOBI)
+    return fail(IPI_EVALIDATION, "only the none and jacobi preconditioners run on the device");
   cudaStream_t st = (cudaStream_t)stream;
   int rc = ensure_scratch(h);
   if (rc) return rc;
@@ -741,6 +750,11 @@ int ipi_solve(ipi_mdp* h, const ipi_opts* o, double* v, int32_t* policy, double*
     cudaEventRecord(pa.a, st);
     rc = gather_policy(h, h->pi, nullptr, h->rp_pi, h->col_pi, h->val_pi, nullptr, nullptr, st);
     if (rc) return rc;
+    if (o->pc_type == IPI_PC_JACOBI) {
+      if (!h->invd) IPI_CUDA_TRY(cudaMalloc(&h->invd, sizeof(double) * std::max<int64_t>(n, 1)));
+      rc = jacobi_inv_diag(h->rp_pi, h->col_pi, h->val_pi, n, h->gamma, h->invd, st);
+      if (rc) return rc;
+    }
     cudaEventRecord(pa.b, st);
     phases.push_back(pa);
     double target;
@@ -758,7 +772,7 @@ int ipi_solve(ipi_mdp* h, const ipi_opts* o, double* v, int32_t* policy, double*
     rc = inner_solve(h->rp_pi, h->col_pi, h->val_pi, n, h->gamma, h->gpi, vnext, target, cap,
                      o->ksp_type, o->richardson_scale, h->plan.lanes_per_row, h->plan.halo,
                      h->plan.uniform_rows ? h->plan.row_len_max : 0, h->d_report, st, h->kry,
-                     h->kry_len);
+                     h->kry_len, o->pc_type == IPI_PC_JACOBI ? h->invd : nullptr);
     if (rc) return rc;
     if (o->ksp_type == IPI_KSP_TFQMR || o->ksp_type == IPI_KSP_BICGSTAB) {
       // these kinds can break down: read the report now (driver.py:189-193)

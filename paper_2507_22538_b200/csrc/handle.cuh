@@ -32,6 +32,7 @@ struct ipi_mdp {
   double* xbuf = nullptr;
   int64_t* scan_tmp = nullptr;
   double* kry = nullptr;        // per-handle Krylov workspace (ipi_solve)
+  double* invd = nullptr;       // Jacobi inverse diagonal (ipi_solve with pc = jacobi)
   int64_t kry_len = 0;
   int64_t scan_tmp_len = 0;
   ipi_inner_report* d_report = nullptr;
@@ -106,7 +107,10 @@ int inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_p
                 double gamma, const double* b, double* x, double target, int32_t max_it,
                 int32_t kind, double scale, int lanes, int halo, int uniform_K,
                 ipi_inner_report* d_report, cudaStream_t st, double* workspace = nullptr,
-                int64_t workspace_doubles = 0);
+                int64_t workspace_doubles = 0, const double* inv_diag = nullptr);
+// Jacobi: inv_diag[s] = 1 / (1 - gamma * P_pi[s, s])  (inner.py:115-118)
+int jacobi_inv_diag(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi, int64_t n,
+                    double gamma, double* inv_diag, cudaStream_t st);
 // doubles of Krylov workspace inner_solve needs for an n-row system
 inline int64_t krylov_workspace_doubles(int64_t n) {
   return (int64_t)(kGmresRestart + 1) * n + 2 * n + 4 * 1024;

@@ -56,7 +56,7 @@ int inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_p
                 double gamma, const double* b, double* x, double target, int32_t max_it,
                 int32_t kind, double scale, int lanes, int halo, int uniform_K,
                 ipi_inner_report* d_report, cudaStream_t st, double* workspace,
-                int64_t workspace_doubles) {
+                int64_t workspace_doubles, const double* inv_diag) {
   if (kind < IPI_KSP_RICHARDSON || kind > IPI_KSP_TFQMR)
     return fail(IPI_EVALIDATION, "unknown inner solver kind " + std::to_string(kind));
   if (max_it < 1) return fail(IPI_EVALIDATION, "iteration cap must be >= 1, got " + std::to_string(max_it));
@@ -90,6 +90,7 @@ int inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_p
   a.kind = kind;
   a.scale = scale;
   a.rep = d_report;
+  a.invd = inv_diag;
   int G = lanes, P = 0;
   a.K = 0;
   if (uniform_K > 0 && uniform_shape(uniform_K, &G, &P)) a.K = uniform_K;

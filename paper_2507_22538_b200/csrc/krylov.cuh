@@ -53,6 +53,7 @@ struct KArgs {
   int win_cap;   // doubles of the shared-memory window (0 = none)
   int own_cap;   // doubles of the shared-memory w slice (0 = w in global)
   int K;         // uniform row length of P_pi (0 = variable)
+  const double* invd;  // Jacobi: 1 / (1 - gamma diag(P_pi)); nullptr = identity (inner.py:113-118)
   ipi_inner_report* rep;
 };
 
@@ -256,9 +257,24 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
   };
   const double eff = fmax(a.target, 1e-14 * fmax(1.0, bnorm));
   int it = 0;
+  // left preconditioner pc(v)[s] (identity or Jacobi: elementwise multiply)
+  const double* invd = a.invd;
+  auto pcv = [&](int64_t s, double v) -> double { return invd ? mul_rn(v, invd[s]) : v; };
+  // z = pc(r) on own rows into dst; returns ||z||^2 (the same sum rn^2 when pc = I)
+  auto precond_residual = [&](double* dst) -> double {
+    double q[1] = {0.0};
+    for (int64_t i = s_lo + tid; i < s_hi; i += nthr) {
+      const double z = pcv(i, r[i]);
+      dst[i] = z;
+      q[0] = add_rn(q[0], mul_rn(z, z));
+    }
+    if (!invd) return -1.0;  // caller reuses rn^2
+    grid_allreduce<1>(q, a, slot, grid, sh);
+    return q[0];
+  };
 
   if constexpr (KIND == IPI_KSP_TFQMR) {
-    // ---- TFQMR (inner.py:376-450), pc = identity ------------------------------
+    // ---- TFQMR (inner.py:376-450) ------------------------------
     double* r0 = a.V;
     double* wv = a.V + n;
     double* yv = a.V + 2 * n;
@@ -268,9 +284,9 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
     double* vt = a.V + 6 * n;
     bool stale = false;
     if (!(rn <= eff)) {
+      const double zz = precond_residual(r0);     // r0 = pc(r_true)
       for (int64_t i = s_lo + tid; i < s_hi; i += nthr) {
-        const double ri = r[i];
-        r0[i] = ri;
+        const double ri = r0[i];
         wv[i] = ri;
         yv[i] = ri;
         dv[i] = 0.0;
@@ -278,14 +294,15 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
       grid.sync();
       double p2[2] = {0.0, 0.0};
       spmv_rows<G, P, WIN>(a, yv, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
-        const double u = sub_rn(xs, mul_rn(gam, px));
+        const double u = pcv(s, sub_rn(xs, mul_rn(gam, px)));
         uv[s] = u;
         vv[s] = u;
         p2[0] = add_rn(p2[0], mul_rn(r0[s], u));
         p2[1] = add_rn(p2[1], mul_rn(u, u));
       });
-      double tau = rn, thq = 0.0, eta = 0.0, rho = rr0, est_target = eff;
-      const double r0n = rn;
+      const double r0nn = invd ? sqrt(zz) : rn;
+      double tau = r0nn, thq = 0.0, eta = 0.0, rho = invd ? zz : rr0, est_target = eff;
+      const double r0n = r0nn;
       while (it < a.max_it) {
         grid_allreduce<2>(p2, a, slot, grid, sh);
         const double sigma = p2[0], vn = sqrt(p2[1]);
@@ -308,7 +325,7 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
             for (int64_t i = s_lo + tid; i < s_hi; i += nthr) yv[i] = sub_rn(yv[i], mul_rn(alpha, vv[i]));
             grid.sync();
             spmv_rows<G, P, WIN>(a, yv, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
-              const double u = sub_rn(xs, mul_rn(gam, px));
+              const double u = pcv(s, sub_rn(xs, mul_rn(gam, px)));
               uv[s] = u;
               const double w = sub_rn(wv[s], mul_rn(alpha, u));
               wv[s] = w;
@@ -354,7 +371,7 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
         grid.sync();
         p2[0] = p2[1] = 0.0;
         spmv_rows<G, P, WIN>(a, yv, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
-          const double u = sub_rn(xs, mul_rn(gam, px));
+          const double u = pcv(s, sub_rn(xs, mul_rn(gam, px)));
           uv[s] = u;
           const double v = add_rn(vt[s], u);
           vv[s] = v;
@@ -365,7 +382,7 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
       if (stale || brk) rn = true_residual();
     }
   } else if constexpr (KIND == IPI_KSP_BICGSTAB) {
-    // ---- BiCGStab (inner.py:295-373), pc = identity ---------------------------
+    // ---- BiCGStab (inner.py:295-373) ---------------------------
     double* rv = a.V;          // recurrence residual
     double* rt = a.V + n;      // shadow residual
     double* pv = a.V + 2 * n;
@@ -374,19 +391,19 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
     double* tv = a.V + 5 * n;
     bool stale = false;
     if (!(rn <= eff)) {
+      double zz = precond_residual(rv);           // r = pc(r_true)
       for (int64_t i = s_lo + tid; i < s_hi; i += nthr) {
-        const double ri = r[i];
-        rv[i] = ri;
+        const double ri = rv[i];
         rt[i] = ri;
         pv[i] = ri;
       }
-      double rtn = rn, rho = rr0, est = rn, est_target = eff;
+      double rtn = invd ? sqrt(zz) : rn, rho = invd ? zz : rr0, est = rtn, est_target = eff;
       while (it < a.max_it) {
         if (fabs(rho) <= mul_rn(mul_rn(1e-14, rtn), est)) { brk = 1; break; }
         grid.sync();
         double p2[2] = {0.0, 0.0};
         spmv_rows<G, P, WIN>(a, pv, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
-          const double v = sub_rn(xs, mul_rn(gam, px));
+          const double v = pcv(s, sub_rn(xs, mul_rn(gam, px)));
           vv[s] = v;
           p2[0] = add_rn(p2[0], mul_rn(rt[s], v));
           p2[1] = add_rn(p2[1], mul_rn(v, v));
@@ -419,21 +436,21 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
           stale = false;
           if (rn <= eff) break;
           est_target = fmin(est_target, mul_rn(mul_rn(s_norm, eff / rn), 0.5));
+          zz = precond_residual(rv);
           for (int64_t i = s_lo + tid; i < s_hi; i += nthr) {
-            const double ri = r[i];
-            rv[i] = ri;
+            const double ri = rv[i];
             rt[i] = ri;
             pv[i] = ri;
           }
-          rtn = rn;
-          rho = q[0];
-          est = rn;
+          rtn = invd ? sqrt(zz) : rn;
+          rho = invd ? zz : q[0];
+          est = rtn;
           continue;
         }
         grid.sync();
         double p3[2] = {0.0, 0.0};
         spmv_rows<G, P, WIN>(a, sv, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
-          const double t = sub_rn(xs, mul_rn(gam, px));
+          const double t = pcv(s, sub_rn(xs, mul_rn(gam, px)));
           tv[s] = t;
           p3[0] = add_rn(p3[0], mul_rn(t, t));
           p3[1] = add_rn(p3[1], mul_rn(t, sv[s]));
@@ -474,7 +491,8 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
   } else   if (a.kind == IPI_KSP_RICHARDSON) {
     while (true) {
       if (rn <= eff || it >= a.max_it || !isfinite(rn)) break;
-      for (int64_t i = s_lo + tid; i < s_hi; i += nthr) x[i] = add_rn(x[i], mul_rn(a.scale, r[i]));
+      for (int64_t i = s_lo + tid; i < s_hi; i += nthr)
+        x[i] = add_rn(x[i], mul_rn(a.scale, pcv(i, r[i])));
       ++it;
       grid.sync();
       double acc1[1] = {0.0};
@@ -489,9 +507,11 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
   } else {  // GMRES(30)
     double est_target = eff;
     while (rn > eff && it < a.max_it) {
-      const double beta = rn;  // ||pc(r)|| with pc = identity: same vector, same reduction
+      // z = pc(r); beta = ||z|| (with pc = I: same vector and reduction as rn)
+      const double zz = precond_residual(a.V);
+      const double beta = invd ? sqrt(zz) : rn;
       if (beta == 0.0 || !isfinite(beta)) break;
-      for (int64_t i = s_lo + tid; i < s_hi; i += nthr) a.V[i] = r[i] / beta;
+      for (int64_t i = s_lo + tid; i < s_hi; i += nthr) a.V[i] = a.V[i] / beta;
       if (tid == 0) {
         for (int k = 0; k < (R + 1) * R; ++k) sh.H[k] = 0.0;
         for (int k = 0; k < R; ++k) sh.cs[k] = sh.sn[k] = 0.0;
@@ -505,7 +525,7 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
         const double* V0 = a.V;
         double p[1] = {0.0};
         spmv_rows<G, P, WIN>(a, Vj, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
-          wl[s - s_lo] = sub_rn(xs, mul_rn(gam, px));
+          wl[s - s_lo] = pcv(s, sub_rn(xs, mul_rn(gam, px)));
         });
         ++it;
         __syncthreads();  // w rows written by group leaders, read per-thread below

@@ -133,6 +133,38 @@ __global__ void __launch_bounds__(256) copy_rows(const int64_t* __restrict__ rp,
   }
 }
 
+// warp per row of P_pi: the lane holding column s supplies the diagonal entry;
+// absent diagonal -> 0 -> inv_diag = 1 (CsrMatrix.diagonal, sparse.py:102-109)
+__global__ void jacobi_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                              const double* __restrict__ val, int64_t n, double gamma,
+                              double* __restrict__ invd) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t s = wg; s < n; s += nw) {
+    double d = 0.0;
+    int found = 0;
+    for (int64_t p = rp[s] + lane; p < rp[s + 1]; p += 32)
+      if (col[p] == (int)s) {
+        d = val[p];
+        found = 1;
+      }
+    const unsigned who = __ballot_sync(kFull, found);
+    const double dd = __shfl_sync(kFull, d, who ? __ffs(who) - 1 : 0);
+    if (lane == 0) invd[s] = 1.0 / sub_rn(1.0, mul_rn(gamma, who ? dd : 0.0));
+  }
+}
+
+int jacobi_inv_diag(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi, int64_t n,
+                    double gamma, double* inv_diag, cudaStream_t st) {
+  if (n <= 0) return IPI_OK;
+  int64_t blocks = (n + 7) / 8;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  jacobi_kernel<<<(int)blocks, 256, 0, st>>>(rp_pi, col_pi, val_pi, n, gamma, inv_diag);
+  IPI_LAUNCH_CHECK();
+  return IPI_OK;
+}
+
 static int ensure_scan_tmp(ipi_mdp* h, int64_t nb) {
   if (h->scan_tmp_len >= nb + 1) return IPI_OK;
   if (h->scan_tmp) cudaFree(h->scan_tmp);

@@ -3,9 +3,9 @@
 ``inner_solve`` (inner.py:163-213) runs the whole solve — Richardson,
 restarted GMRES(30) with MGS/Givens, BiCGStab or TFQMR, each with the
 reference's estimate-then-verify stopping and breakdown reporting — as one
-persistent cooperative kernel (krylov*.cu).  Preconditioning is NONE on
-the device path (every BASELINE config uses none); the other reference
-preconditioners are listed in DESIGN.md as out of scope for this round.
+persistent cooperative kernel (krylov*.cu).  Preconditioning: NONE or
+JACOBI on the device path (left preconditioning exactly as the reference
+applies it); SOR and EXACT (dense) are out of scope this round.
 """
 
 from __future__ import annotations
@@ -77,10 +77,32 @@ class InnerSolveReport:
     target_2norm: float
 
 
+class JacobiPreconditioner:
+    """pc(r) = r / (1 - gamma diag(P_pi)) (inner.py:115-118), inverse diagonal in HBM."""
+
+    def __init__(self, op: PolicyOperator):
+        p = op.p_pi
+        self.inv_diag = torch.empty(op.n, dtype=torch.float64, device=p.values.device)
+        _lib.check(_lib.lib().ipi_jacobi_inv_diag(_lib.ptr(p.row_ptr), _lib.ptr(p.col_idx),
+                                                  _lib.ptr(p.values), op.n, op.gamma,
+                                                  _lib.ptr(self.inv_diag), _lib.stream_ptr()),
+                   "ipi_jacobi_inv_diag")
+
+    def __call__(self, r):
+        was_np = not isinstance(r, torch.Tensor)
+        t = torch.as_tensor(np.asarray(r, dtype=np.float64), device=self.inv_diag.device) \
+            if was_np else r.to(self.inv_diag.device, torch.float64)
+        out = t * self.inv_diag
+        return out.cpu().numpy() if was_np else out
+
+
 def build_preconditioner(op, kind: Preconditioner, **_):
-    """Only the identity runs on the device path (inner.py:113-114)."""
+    """NONE -> None (identity), JACOBI -> JacobiPreconditioner (inner.py:98-133).
+    SOR / EXACT need explicit assembly and are not on the device path."""
     if kind is Preconditioner.NONE:
         return None
+    if kind is Preconditioner.JACOBI:
+        return JacobiPreconditioner(op)
     raise NotImplementedError(f"preconditioner {kind.value!r} is not on the B200 device path")
 
 
@@ -100,8 +122,8 @@ def inner_solve(op: PolicyOperator, b, theta0, target_2norm: float, max_it: int,
         raise ValueError(f"iteration cap must be >= 1, got {max_it}")
     if target_2norm < 0.0:
         raise ValueError(f"residual target must be >= 0, got {target_2norm}")
-    if pc is not None:
-        raise NotImplementedError("only the identity preconditioner runs on the device path")
+    if pc is not None and not isinstance(pc, JacobiPreconditioner):
+        raise NotImplementedError("only the identity and Jacobi preconditioners run on the device")
     if kind not in DEVICE_KINDS:
         raise NotImplementedError(f"inner solver {kind.value!r} is not on the device path yet")
     bt = bt.contiguous()
@@ -112,6 +134,7 @@ def inner_solve(op: PolicyOperator, b, theta0, target_2norm: float, max_it: int,
                                           _lib.ptr(p.values), op.n, op.gamma, _lib.ptr(bt),
                                           _lib.ptr(x), float(target_2norm), int(max_it),
                                           _lib.KSP[kind.value], float(richardson_scale),
+                                          _lib.ptr(pc.inv_diag) if pc is not None else None,
                                           _lib.C.byref(rep), _lib.stream_ptr()), "ipi_inner_solve")
     report = InnerSolveReport(iterations=rep.iterations,
                               final_linear_residual_2norm=rep.final_linear_residual_2norm,

@@ -41,6 +41,12 @@ def golden_meta(name):
     return next(m for m in idx if m["name"] == name)
 
 
+def solve_key(key):
+    """'gmres' -> ('gmres', 'none'); 'gmres_jacobi' -> ('gmres', 'jacobi')."""
+    kind, _, pc = key.partition("_")
+    return kind, (pc or "none")
+
+
 def load_golden(name):
     with np.load(GOLDEN / f"{name}.npz") as z:
         return {k: z[k] for k in z.files}

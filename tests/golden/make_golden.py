@@ -73,7 +73,8 @@ def _digest(*arrs) -> str:
     return h.hexdigest()[:16]
 
 
-def record(name, inst, *, kinds=("gmres",), opts=None, seed=7, exact=True, tol=1e-8):
+def record(name, inst, *, kinds=("gmres",), opts=None, seed=7, exact=True, tol=1e-8,
+           jacobi_kinds=()):
     opts = dict(opts or {})
     rp, col, val, cost = _arrays(inst)
     n, m = cost.shape
@@ -121,6 +122,18 @@ def record(name, inst, *, kinds=("gmres",), opts=None, seed=7, exact=True, tol=1
                                             for k, v in opts.items()}, "tol": tol}
         if exact and n <= 4096 and res.status is ref.SolveStatus.CONVERGED:
             out[f"solve_{kind}_exact"] = ref.policy_cost_exact(inst, res.policy)
+    # the same solves with the Jacobi preconditioner (inner.py:115-118)
+    for kind in jacobi_kinds:
+        so = ref.SolveOptions(inner=ref.InnerSolver.from_name(kind), tol=tol,
+                              pc=ref.Preconditioner.JACOBI, **opts)
+        res = ref.solve(inst, so)
+        key = f"{kind}_jacobi"
+        out[f"solve_{key}_values"] = res.values
+        out[f"solve_{key}_policy"] = res.policy.astype(np.int64)
+        out[f"solve_{key}_history"] = np.asarray(res.residual_history)
+        meta["solves"][key] = {"status": res.status.value, "outer": res.outer_iterations,
+                               "inner": res.inner_iterations_total, "options": {"pc": "jacobi"},
+                               "tol": tol}
     np.savez_compressed(HERE / f"{name}.npz", **out)
     return meta
 
@@ -139,12 +152,13 @@ def main():
     # --- reference fixtures -------------------------------------------------
     fixture = ref.gen_random(RandomParams(n=20, m=4, nnz_per_row=6, gamma=0.9, seed=123))
     metas.append(record("ref_fixture_random", fixture,
-                        kinds=("gmres", "richardson", "tfqmr", "bicgstab")))
+                        kinds=("gmres", "richardson", "tfqmr", "bicgstab"),
+                        jacobi_kinds=("gmres", "richardson", "tfqmr", "bicgstab")))
     rp, col, val, cost = _arrays(fixture)
     metas.append(record("ref_fixture_random_max", _instance(rp, col, val, cost, 0.9, "max"),
                         kinds=("gmres", "richardson")))
     metas.append(record("ref_maze33", ref.gen_maze(MazeParams(height=33, width=33)),
-                        kinds=("gmres", "tfqmr")))
+                        kinds=("gmres", "tfqmr"), jacobi_kinds=("gmres",)))
     rng = np.random.default_rng(20240817)
     p = rng.random((5, 3, 5))
     p /= p.sum(axis=2, keepdims=True)
@@ -174,14 +188,16 @@ def main():
     # --- scaled BASELINE-config instances (our generators, reference solve) --
     c1 = gen.random_dirichlet(100, 10, 25, seed=0)
     metas.append(record("cfg1_dirichlet_n100", _instance(*c1, 0.99),
-                        kinds=("gmres", "richardson", "tfqmr", "bicgstab")))
+                        kinds=("gmres", "richardson", "tfqmr", "bicgstab"),
+                        jacobi_kinds=("gmres", "richardson")))
     c2 = gen.random_locality_host(256, 8, 16, 16, seed=0)
     metas.append(record("cfg2_locality_n256", _instance(*c2, 0.999), kinds=("gmres",)))
     c3 = gen.pendulum_host(12, 21)
     metas.append(record("cfg3_pendulum_g12", _instance(*c3, 0.9999),
                         kinds=("gmres", "tfqmr")))
     c4 = gen.sis_host(60)
-    metas.append(record("cfg4_sis_n60", _instance(*c4, 0.9999), kinds=("gmres", "tfqmr", "bicgstab")))
+    metas.append(record("cfg4_sis_n60", _instance(*c4, 0.9999), kinds=("gmres", "tfqmr", "bicgstab"),
+                        jacobi_kinds=("gmres",)))
     c2max = _instance(*c2, 0.999, "max")
     metas.append(record("cfg2_locality_n256_max", c2max, kinds=("gmres",)))
     (HERE / "golden_index.json").write_text(json.dumps(metas, indent=1) + "\n")

@@ -13,7 +13,7 @@ from __future__ import annotations
 import numpy as np
 import pytest
 
-from conftest import golden_meta, golden_names, load_golden
+from conftest import golden_meta, golden_names, load_golden, solve_key
 from oracle import mdp_oracle as orc
 
 pytestmark = pytest.mark.gpu
@@ -121,7 +121,9 @@ def test_solve_matches_reference(name, kind):
     g = load_golden(name)
     s = golden_meta(name)["solves"][kind]
     mdp = instance(g)
-    res = ipi.solve(mdp, ipi.SolveOptions(inner=ipi.InnerSolver.from_name(kind), tol=s["tol"]))
+    k, pc = solve_key(kind)
+    res = ipi.solve(mdp, ipi.SolveOptions(inner=ipi.InnerSolver.from_name(k), tol=s["tol"],
+                                          pc=ipi.Preconditioner.from_name(pc)))
     ref_v = g[f"solve_{kind}_values"]
     assert res.status.value == s["status"]
     assert res.outer_iterations == s["outer"]
@@ -139,7 +141,7 @@ def test_solve_matches_reference(name, kind):
     # V is asserted at 1e-8 above.
     # (BiCGStab/TFQMR stop on a cheap estimate and may overshoot the target by a wide
     # margin, so their iterates are pinned an order of magnitude more loosely.)
-    alpha = 1e-4 * (10.0 if kind in ("bicgstab", "tfqmr") else 1.0)
+    alpha = 1e-4 * (10.0 if k in ("bicgstab", "tfqmr") else 1.0)
     slack = np.concatenate(([0.0], alpha * ref_h[:-1]))
     big = ref_h > 1e-10
     err = np.abs(hist - ref_h)
@@ -150,6 +152,29 @@ def test_solve_matches_reference(name, kind):
     _, applied = orc.greedy(g["row_ptr"], g["col"], g["val"], g["cost"], float(g["gamma"]),
                             res.values, bool(g["maximize"]))
     assert np.max(np.abs(res.values - applied)) <= s["tol"] * 1.0001
+
+
+@pytest.mark.parametrize("name", ["ref_fixture_random", "cfg1_dirichlet_n100", "ref_maze33"])
+@pytest.mark.parametrize("kind", ["gmres", "richardson", "tfqmr", "bicgstab"])
+def test_inner_solve_jacobi_matches_oracle(name, kind):
+    g = load_golden(name)
+    mdp = instance(g)
+    p_pi = ipi.gather_policy_matrix(mdp, g["greedy_policy"])
+    op = ipi.PolicyOperator(p_pi, float(g["gamma"]))
+    pc = ipi.build_preconditioner(op, ipi.Preconditioner.JACOBI)
+    tgt = 1e-3 * float(np.max(np.abs(g["greedy_v"] - g["greedy_applied"])))
+    theta, rep = ipi.inner_solve(op, g["gather_cost"], g["greedy_v"], tgt, 200,
+                                 kind=ipi.InnerSolver.from_name(kind), pc=pc)
+    ref_t, ref = orc.inner_solve(g["gather_row_ptr"], g["gather_col"], g["gather_val"],
+                                 float(g["gamma"]), g["gather_cost"], g["greedy_v"], tgt, 200,
+                                 kind, pc="jacobi")
+    assert rep.converged == ref.converged and rep.breakdown == ref.breakdown
+    if ref.converged:
+        assert np.max(np.abs(theta - ref_t)) <= 2 * ref.target_2norm / (1 - float(g["gamma"])) + 1e-12
+    # the preconditioner itself: bit-exact against the oracle's inverse diagonal
+    r = np.linspace(-1, 1, mdp.n)
+    np.testing.assert_array_equal(pc(r), orc.jacobi(g["gather_row_ptr"], g["gather_col"],
+                                                    g["gather_val"], float(g["gamma"]))(r))
 
 
 def test_solve_bitwise_rerun():

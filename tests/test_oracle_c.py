@@ -32,7 +32,7 @@ def _cases():
     out = []
     for name in NAMES:
         for kind, s in golden_meta(name)["solves"].items():
-            if kind in ("gmres", "richardson") and s["inner"] <= 50_000:
+            if kind in ("gmres", "richardson") and s["inner"] <= 50_000:  # no pc in the C port
                 out.append(pytest.param(name, kind, id=f"{name}-{kind}"))
     return out
 

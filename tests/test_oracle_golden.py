@@ -10,7 +10,7 @@ from __future__ import annotations
 import numpy as np
 import pytest
 
-from conftest import golden_meta, golden_names, load_golden
+from conftest import golden_meta, golden_names, load_golden, solve_key
 from oracle import mdp_oracle as orc
 
 NAMES = golden_names()
@@ -64,8 +64,9 @@ def test_solve_bitwise(name, kind):
     s = golden_meta(name)["solves"][kind]
     if s["inner"] > 50_000:
         pytest.skip("oracle replay of a non-converging 1e6-iteration run is too slow for CI")
+    k, pc = solve_key(kind)
     res = orc.solve(g["row_ptr"], g["col"], g["val"], g["cost"], float(g["gamma"]),
-                    maximize=bool(g["maximize"]), kind=kind, tol=s["tol"])
+                    maximize=bool(g["maximize"]), kind=k, tol=s["tol"], pc=pc)
     assert res.status == s["status"]
     assert res.outer_iterations == s["outer"]
     assert res.inner_iterations_total == s["inner"]
