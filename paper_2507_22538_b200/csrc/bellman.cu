@@ -42,7 +42,6 @@ struct K1Args {
   double* gpi;
   int32_t* lenpi;
   unsigned long long* res_bits;
-  int32_t debug;  // experiment hook (IPI_K1_DEBUG): bit 0 = skip V gathers (streaming-only probe)
 };
 
 template <int G, bool WIN>
@@ -69,15 +68,10 @@ __global__ void __launch_bounds__(kK1Threads) k1_bellman(K1Args a) {
   const int m = a.m;
   double res = 0.0;
 
-  const uint32_t win_s = (uint32_t)__cvta_generic_to_shared(win);
   auto gather = [&](int c) -> double {
     if (WIN) {
       const uint64_t off = (uint64_t)((int64_t)c - w_lo);
-      if (off < (uint64_t)w_len) {
-        double x;
-        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(x) : "r"(win_s + (uint32_t)off * 8u));
-        return x;
-      }
+      if (off < (uint64_t)w_len) return win[off];
     }
     return __ldg(a.v + c);
   };
@@ -192,17 +186,10 @@ __global__ void __launch_bounds__(kK1Threads) k1_bellman_uniform(K1Args a, int K
   const int pairs = K >> 1;
   double res = 0.0;
 
-  const uint32_t win_s = (uint32_t)__cvta_generic_to_shared(win);
-  const bool probe = (a.debug & 1) != 0;
   auto gather = [&](int c) -> double {
-    if (probe) return 1.0;
     if (WIN) {
       const uint64_t off = (uint64_t)((int64_t)c - w_lo);
-      if (off < (uint64_t)w_len) {
-        double x;
-        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(x) : "r"(win_s + (uint32_t)off * 8u));
-        return x;
-      }
+      if (off < (uint64_t)w_len) return win[off];
     }
     return __ldg(a.v + c);
   };
@@ -478,7 +465,7 @@ __global__ void __launch_bounds__(kK1Threads, 1) k1_bellman_deep(K1Args a, int K
       const uint32_t off = (uint32_t)(c - w_lo);
       if (off < w_len) {
         double x;
-        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(x) : "r"(win_s + off * 8u));
+        asm("ld.shared.f64 %0, [%1];" : "=d"(x) : "r"(win_s + off * 8u));
         return x;
       }
     }
@@ -734,13 +721,6 @@ int launch_bellman(ipi_mdp* h, const double* v_full, int32_t mode, int32_t* poli
   a.gpi = g_pi;
   a.lenpi = len_pi;
   a.res_bits = res_bits;
-  {
-    static const int dbg = [] {
-      const char* e = getenv("IPI_K1_DEBUG");
-      return e ? atoi(e) : 0;
-    }();
-    a.debug = dbg;
-  }
   const bool win = h->plan.halo >= 0;
   const int blocks = h->plan.k1_blocks, smem = h->plan.k1_smem_bytes;
   int G = 0, P = 0;
