@@ -51,7 +51,7 @@ class Plan(C.Structure):
                 ("row_len_mean", _f64), ("lanes_per_row", _i32), ("halo", _i32),
                 ("k1_blocks", _i32), ("k1_threads", _i32), ("k1_smem_bytes", _i32),
                 ("inner_blocks", _i32), ("inner_threads", _i32), ("inner_smem_bytes", _i32),
-                ("uniform_rows", _i32), ("k1_variant", _i32), ("k1_tma_stages", _i32),
+                ("uniform_rows", _i32), ("k1_variant", _i32), ("k1_stages", _i32),
                 ("k1_tma_chunk_states", _i32)]
 
     def as_dict(self):

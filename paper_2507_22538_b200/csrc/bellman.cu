@@ -358,11 +358,13 @@ __global__ void __launch_bounds__(kK1Threads, 2) k1_bellman_flat(K1Args a, int K
       const int64_t r = base + lane;
       const bool ok = r < r_end;
       double acc = 0.0;
-      if (ok) {
-        if (cur.c0.x >= 0) acc = add_rn(acc, mul_rn(cur.v0.x, gather(cur.c0.x)));
-        if (cur.c0.y >= 0) acc = add_rn(acc, mul_rn(cur.v0.y, gather(cur.c0.y)));
-        if (cur.c1.x >= 0) acc = add_rn(acc, mul_rn(cur.v1.x, gather(cur.c1.x)));
-        if (cur.c1.y >= 0) acc = add_rn(acc, mul_rn(cur.v1.y, gather(cur.c1.y)));
+      if (ok) {  // reduceat order: p0 + (((0 + p1) + p2) + p3)
+        acc = add_rn(0.0, mul_rn(cur.v0.y, gather(cur.c0.y)));
+        if (pairs > 1) {
+          acc = add_rn(acc, mul_rn(cur.v1.x, gather(cur.c1.x)));
+          acc = add_rn(acc, mul_rn(cur.v1.y, gather(cur.c1.y)));
+        }
+        acc = add_rn(mul_rn(cur.v0.x, gather(cur.c0.x)), acc);
       }
       // state id and action of this lane's row
       const int64_t sb = base / m;
@@ -414,6 +416,273 @@ __global__ void __launch_bounds__(kK1Threads, 2) k1_bellman_flat(K1Args a, int K
       atomicMax(a.res_bits, (unsigned long long)__double_as_longlong(t));
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// Flat rows, shared-memory ring (K <= 4, C3: n = 4.2M, m = 21, K = 4).
+//
+// The register-pipelined flat kernel above spends ~390 instructions per
+// 32-row batch, 2/3 of them in the segmented argmin scan (5 shuffle rounds on
+// q, action and state id), and waits on V gathers issued one batch ahead, so
+// it is issue/latency-bound at ~50% of HBM.  This kernel:
+//   * streams each warp's contiguous row range through a private S-stage
+//     shared-memory ring with cp.async: every instruction moves 512
+//     contiguous bytes (lane l copies 16-byte chunk l), nothing occupies
+//     registers while in flight, and S-3..S-2 batches stay outstanding;
+//   * issues the V gathers of batch i+2 while batch i is reduced (three
+//     rotating register sets, loop unrolled by 3 so no register copy waits
+//     on an outstanding load);
+//   * lane = row for the products (q = g + gamma*acc, numpy reduceat order
+//     p0 + (((0 + p1) + p2) + p3), so Q is bitwise the reference's), q goes to
+//     a per-warp shared buffer of 32 states, and after every m batches
+//     (= 32 states) lane = state runs the first-index argmin/argmax over its
+//     m entries sequentially: no shuffles, and the policy / applied / g_pi /
+//     residual traffic becomes coalesced.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes,
+                                           uint64_t pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;" ::"r"(dst),
+               "l"(src), "r"(src_bytes), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int K>
+struct RingLayout {
+  static constexpr int kVal = 32 * K * 8;             // values of 32 rows
+  static constexpr int kCol = 32 * K * 4;             // columns of 32 rows
+  static constexpr int kCost = 17 * 16;               // 16-byte chunks covering 32 (+1) costs
+  static constexpr int kStage = kVal + kCol + kCost;  // multiple of 16
+};
+
+// dynamic shared memory: [V window][NW rings of S stages][NW q buffers of 32*m]
+int flat_ring_smem(int K, int stages, int warps, int m, int window_bytes) {
+  const int st = K == 2 ? RingLayout<2>::kStage : RingLayout<4>::kStage;
+  return ((window_bytes + 15) & ~15) + warps * (stages * st + 32 * m * 8);
+}
+
+template <int K, int S, int NW, bool WIN>
+__global__ void __launch_bounds__(NW * 32, 1) k1_bellman_ring(K1Args a, int win_bytes) {
+  static_assert(K == 2 || K == 4, "flat ring handles K = 2 or 4");
+  static_assert(S >= 4, "ring needs >= 4 stages (gathers run two batches ahead)");
+  using L = RingLayout<K>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double red[32];
+  double* win = reinterpret_cast<double*>(smem_raw);
+  const int64_t s_lo = a.bounds[blockIdx.x], s_hi = a.bounds[blockIdx.x + 1];
+  int w_lo = 0;
+  uint32_t w_len = 0;
+  if (WIN) {
+    int64_t lo = a.state0 + s_lo - a.halo;
+    int64_t hi = a.state0 + s_hi + a.halo;
+    lo = lo < 0 ? 0 : lo;
+    hi = hi > a.n_global ? a.n_global : hi;
+    w_lo = (int)lo;
+    w_len = hi > lo ? (uint32_t)(hi - lo) : 0u;
+    for (uint32_t i = threadIdx.x; i < w_len; i += blockDim.x) win[i] = __ldg(a.v + lo + i);
+    __syncthreads();
+  }
+  const uint64_t pol = policy_evict_first();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int m = a.m;
+  unsigned char* rings = smem_raw + (((WIN ? win_bytes : 0) + 15) & ~15);
+  unsigned char* ring = rings + warp * S * L::kStage;
+  double* qb = reinterpret_cast<double*>(rings + NW * S * L::kStage) + warp * 32 * m;
+  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
+  const bool mx = a.maximize != 0;
+  double res = 0.0;
+  auto gather = [&](int c) -> double {
+    if (WIN) {
+      const uint32_t off = (uint32_t)(c - w_lo);
+      if (off < w_len) return win[off];
+    }
+    return __ldg(a.v + c);
+  };
+  const int64_t ns = s_hi - s_lo;
+  const int64_t ws0 = s_lo + ns * warp / NW, ws1 = s_lo + ns * (warp + 1) / NW;
+  const int64_t r_beg = ws0 * m, r_end = ws1 * m;
+  const int64_t r_valid = s_hi * (int64_t)m;  // rows < r_valid exist in the arrays
+  const int64_t nb = (r_end - r_beg + 31) >> 5;
+
+  // batch i -> stage stg: values, columns, costs (one commit group, maybe empty)
+  auto issue = [&](int64_t i, int stg) {
+    if (i < nb) {
+      const int64_t base = r_beg + (i << 5);
+      const int64_t left = r_end - base;
+      const int nr = left < 32 ? (int)left : 32;
+      const uint32_t st = ring_s + (uint32_t)(stg * L::kStage);
+      const double* vp = a.val + base * K;
+#pragma unroll
+      for (int c = lane; c < 32 * K / 2; c += 32)  // 16-byte value chunks
+        if (c < nr * K / 2) cp_async16(st + 16 * c, vp + 2 * c, 16, pol);
+      if (K == 4) {
+        if (lane < nr) cp_async16(st + L::kVal + 16 * lane, a.col + (base + lane) * 4, 16, pol);
+      } else {
+        if (lane < nr) cp_async8(st + L::kVal + 8 * lane, a.col + (base + lane) * 2);
+      }
+      const int64_t c0 = base & ~(int64_t)1;  // 16-byte aligned cost chunk start
+      const int nch = (int)((base + nr - c0 + 1) >> 1);
+      if (lane < nch) {
+        const int64_t lo = c0 + 2 * lane;
+        const uint32_t bytes = lo + 1 < r_valid ? 16u : 8u;
+        cp_async16(st + L::kVal + L::kCol + 16 * lane, a.cost + lo, bytes, pol);
+      }
+    }
+    cp_async_commit();
+  };
+  // V gathers of batch i (its columns must have landed)
+  auto fetch = [&](int64_t i, int stg, double (&x)[K]) {
+    if (i < nb && r_beg + (i << 5) + lane < r_end) {
+      const unsigned char* st = ring + stg * L::kStage;
+      if (K == 4) {
+        const int4 c = *reinterpret_cast<const int4*>(st + L::kVal + 16 * lane);
+        x[0] = gather(c.x);
+        x[1] = gather(c.y);
+        x[2 % K] = gather(c.z);
+        x[3 % K] = gather(c.w);
+      } else {
+        const int2 c = *reinterpret_cast<const int2*>(st + L::kVal + 8 * lane);
+        x[0] = gather(c.x);
+        x[1 % K] = gather(c.y);
+      }
+    }
+  };
+  int bi = 0;        // batch index inside the current 32-state group
+  int64_t gs0 = ws0;  // first state of the current group
+  // q of batch i's rows -> q buffer; after the group's last batch, lane = state
+  auto compute = [&](int64_t i, int stg, const double (&x)[K]) {
+    const int64_t base = r_beg + (i << 5);
+    const unsigned char* st = ring + stg * L::kStage;
+    if (base + lane < r_end) {
+      const double2 v0 = *reinterpret_cast<const double2*>(st + lane * K * 8);
+      double acc = add_rn(0.0, mul_rn(v0.y, x[1 % K]));
+      if (K == 4) {
+        const double2 v1 = *reinterpret_cast<const double2*>(st + lane * K * 8 + 16);
+        acc = add_rn(acc, mul_rn(v1.x, x[2 % K]));
+        acc = add_rn(acc, mul_rn(v1.y, x[3 % K]));
+      }
+      acc = add_rn(mul_rn(v0.x, x[0]), acc);
+      const double g = reinterpret_cast<const double*>(st + L::kVal + L::kCol)[(base & 1) + lane];
+      qb[bi * 32 + lane] = add_rn(g, mul_rn(a.gamma, acc));
+    }
+    ++bi;
+    if (bi == m || i + 1 == nb) {  // group complete: 32 states (fewer in the tail)
+      __syncwarp();
+      const int64_t left = ws1 - gs0;
+      const int nst = left < 32 ? (int)left : 32;
+      if (lane < nst) {
+        const double* q = qb + lane * m;
+        double bq = q[0];
+        int ba = 0;
+        if (mx) {
+          for (int t = 1; t < m; ++t) {
+            const double v = q[t];
+            if (v > bq) { bq = v; ba = t; }
+          }
+        } else {
+          for (int t = 1; t < m; ++t) {
+            const double v = q[t];
+            if (v < bq) { bq = v; ba = t; }
+          }
+        }
+        const int64_t s = gs0 + lane;
+        a.policy[s] = ba;
+        a.applied[s] = bq;
+        if (a.gpi) a.gpi[s] = __ldg(a.cost + s * m + ba);
+        if (a.lenpi) a.lenpi[s] = K;
+        res = fmax(res, fabs(sub_rn(gather((int)(a.state0 + s)), bq)));
+      }
+      __syncwarp();
+      bi = 0;
+      gs0 += 32;
+    }
+  };
+  // step i: batch i+2's gathers go out, batch i is reduced, stage i % S is
+  // refilled with batch i+S
+  int stg = 0;
+  auto step = [&](int64_t i, const double (&cur)[K], double (&ahead)[K]) {
+    const int s2 = stg + 2 >= S ? stg + 2 - S : stg + 2;
+    cp_async_wait<S - 3>();  // batch i+2 landed (this lane's copies)
+    __syncwarp();            // ... and every lane's
+    fetch(i + 2, s2, ahead);
+    compute(i, stg, cur);
+    __syncwarp();  // stage i fully consumed
+    issue(i + S, stg);
+    stg = stg + 1 == S ? 0 : stg + 1;
+  };
+
+  if (nb > 0) {
+#pragma unroll 1
+    for (int j = 0; j < S; ++j) issue(j, j);
+    double x0[K], x1[K], x2[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) x0[k] = x1[k] = x2[k] = 0.0;
+    cp_async_wait<S - 2>();  // batches 0 and 1 landed
+    __syncwarp();
+    fetch(0, 0, x0);
+    fetch(1, 1, x1);
+#pragma unroll 1
+    for (int64_t i = 0; i < nb; i += 3) {
+      step(i, x0, x2);
+      if (i + 1 < nb) step(i + 1, x1, x0);
+      if (i + 2 < nb) step(i + 2, x2, x1);
+    }
+  }
+  cp_async_wait<0>();
+  if (a.res_bits) {
+    res = warp_max(res);
+    if (lane == 0) red[warp] = res;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < NW; ++w) t = fmax(t, red[w]);
+      atomicMax(a.res_bits, (unsigned long long)__double_as_longlong(t));
+    }
+  }
+}
+
+template <int K, int S, int NW, bool WIN>
+static cudaError_t ring_attr(int smem) {
+  return cudaFuncSetAttribute(k1_bellman_ring<K, S, NW, WIN>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+}
+
+template <int K, int S, int NW>
+static void ring_go(const K1Args& a, bool win, int blocks, int smem, int win_bytes, cudaStream_t st) {
+  if (win)
+    k1_bellman_ring<K, S, NW, true><<<blocks, NW * 32, smem, st>>>(a, win_bytes);
+  else
+    k1_bellman_ring<K, S, NW, false><<<blocks, NW * 32, smem, st>>>(a, 0);
+}
+
+// (stages, warps) shapes with an instance: deeper rings for fewer warps
+#define IPI_RING_SHAPES(K, MACRO) \
+  MACRO(K, 4, 18) MACRO(K, 4, 16) MACRO(K, 6, 12) MACRO(K, 5, 12) MACRO(K, 8, 8)
+#define IPI_DISPATCH_RING(K, S, W, MACRO)                           \
+  do {                                                              \
+    ok = false;                                                     \
+    if ((K) == 2) { IPI_RING_SHAPES(2, MACRO) }                     \
+    else if ((K) == 4) { IPI_RING_SHAPES(4, MACRO) }                \
+  } while (0)
+
+bool k1_ring_prepare(int K, int S, int NW, bool win, int smem) {
+  bool ok = false;
+  cudaError_t e = cudaSuccess;
+#define IPI_R_ATTR(KK, SS, WW)                                                             \
+  if (!ok && K == KK && S == SS && NW == WW) {                                             \
+    ok = true;                                                                             \
+    e = win ? ring_attr<KK, SS, WW, true>(smem) : ring_attr<KK, SS, WW, false>(smem);      \
+  }
+  IPI_DISPATCH_RING(K, S, NW, IPI_R_ATTR);
+#undef IPI_R_ATTR
+  return ok && e == cudaSuccess;
 }
 
 // ---------------------------------------------------------------------------
@@ -731,6 +1000,21 @@ int launch_bellman(ipi_mdp* h, const double* v_full, int32_t mode, int32_t* poli
        : k1_bellman_deep<GG, PP, false><<<blocks, kK1Threads, 0, st>>>(a, K))
     IPI_DISPATCH_UNIFORM(G, P, IPI_D_LAUNCH);
 #undef IPI_D_LAUNCH
+    IPI_LAUNCH_CHECK();
+    return IPI_OK;
+  }
+  if (h->plan.k1_variant == 4) {
+    bool ok = false;
+    const int K = h->plan.row_len_max, S = h->plan.k1_stages, NW = h->plan.k1_threads / 32;
+    const bool rw = h->ring_win_bytes > 0;
+#define IPI_R_LAUNCH(KK, SS, WW)                                                     \
+  if (!ok && K == KK && S == SS && NW == WW) {                                       \
+    ok = true;                                                                       \
+    ring_go<KK, SS, WW>(a, rw, blocks, smem, h->ring_win_bytes, st);                 \
+  }
+    IPI_DISPATCH_RING(K, S, NW, IPI_R_LAUNCH);
+#undef IPI_R_LAUNCH
+    if (!ok) return fail(IPI_ECUDA, "k1 ring: no instance for this (K, stages, warps)");
     IPI_LAUNCH_CHECK();
     return IPI_OK;
   }

@@ -392,6 +392,58 @@ int ipi_mdp_create(const int64_t* row_ptr, const int32_t* col, const double* val
       }
     }
   }
+  // ---- flat rows (K <= 4): cp.async ring per warp (bellman.cu) ---------------
+  if (p.uniform_rows && p.row_len_max <= 4 && (p.row_len_max % 2) == 0 && n_local > 0) {
+    p.k1_variant = 5;  // register-pipelined flat kernel unless a ring shape fits
+    const char* env = getenv("IPI_K1_RING");
+    const bool aligned = ((uintptr_t)values % 16 == 0) && ((uintptr_t)stage_cost % 16 == 0) &&
+                         ((uintptr_t)col % (p.row_len_max == 4 ? 16 : 8) == 0);
+    // (stages, warps): forced by IPI_RING_STAGES / IPI_RING_WARPS, else the first that fits
+    int shapes[4][2] = {{4, 18}, {4, 16}, {6, 12}, {8, 8}};  // measured order on C3
+    int nshape = 4;
+    if (getenv("IPI_RING_STAGES") && getenv("IPI_RING_WARPS")) {
+      shapes[0][0] = atoi(getenv("IPI_RING_STAGES"));
+      shapes[0][1] = atoi(getenv("IPI_RING_WARPS"));
+      nshape = 1;
+    }
+    const int budget = 227 * 1024 - 256;  // one CTA per SM
+    for (int si = 0; si < nshape && !(env && env[0] == '0') && aligned && p.k1_variant == 5; ++si) {
+      const int S = shapes[si][0], NW = shapes[si][1];
+      const int blocks = (int)std::min<int64_t>(h->num_sms, std::max<int64_t>(1, (n_local + 31) / 32));
+      std::vector<int64_t> hb(blocks + 1);
+      for (int c = 0; c <= blocks; ++c) hb[c] = (int64_t)((double)n_local * c / blocks);
+      hb[blocks] = n_local;
+      int64_t worst = 0;
+      for (int c = 0; c < blocks; ++c) worst = std::max<int64_t>(worst, hb[c + 1] - hb[c]);
+      int wbytes = 0;
+      if (p.halo >= 0) {
+        const int64_t wlen = std::min<int64_t>(n_global, worst + 2 * (int64_t)p.halo);
+        wbytes = (int)std::min<int64_t>(wlen * 8, INT32_MAX / 2);
+        if (flat_ring_smem(p.row_len_max, S, NW, m, wbytes) > budget) wbytes = 0;  // L1 gathers
+      }
+      const int smem = flat_ring_smem(p.row_len_max, S, NW, m, wbytes);
+      if (smem > budget || !k1_ring_prepare(p.row_len_max, S, NW, wbytes > 0, smem)) {
+        cudaGetLastError();
+        continue;
+      }
+      int64_t* db = nullptr;
+      if (cudaMalloc(&db, sizeof(int64_t) * (blocks + 1)) == cudaSuccess &&
+          cudaMemcpy(db, hb.data(), sizeof(int64_t) * (blocks + 1), cudaMemcpyHostToDevice) ==
+              cudaSuccess) {
+        cudaFree(h->k1_bounds);
+        h->k1_bounds = db;
+        h->ring_win_bytes = wbytes;
+        p.k1_blocks = blocks;
+        p.k1_threads = NW * 32;
+        p.k1_smem_bytes = smem;  // p.halo stays: the inner solver plans its own window from it
+        p.k1_stages = S;
+        p.k1_variant = 4;
+      } else {
+        if (db) cudaFree(db);
+        cudaGetLastError();
+      }
+    }
+  }
   // ---- TMA ring plan for uniform rows (one persistent CTA per SM) ------------
   {
     // Experimental: off unless IPI_K1_TMA=1.  Measured on C2
@@ -426,7 +478,7 @@ int ipi_mdp_create(const int64_t* row_ptr, const int32_t* col, const double* val
           h->tma_stage = stage;
           h->tma_halo = wcap > 0 ? p.halo : -1;
           p.k1_variant = 2;
-          p.k1_tma_stages = NS;
+          p.k1_stages = NS;
           p.k1_tma_chunk_states = SC;
           p.k1_blocks = blocks;
           p.k1_threads = (16 + 1) * 32;

@@ -43,6 +43,8 @@ struct ipi_mdp {
   int64_t* tma_bounds = nullptr;
   int tma_blocks = 0, tma_smem = 0, tma_sc = 0, tma_ns = 0, tma_super = 0, tma_wcap = 0,
       tma_stage = 0, tma_halo = -1;
+  // K1 flat-row cp.async ring (variant 4): window bytes in front of the rings
+  int ring_win_bytes = 0;
 };
 
 namespace ipi {
@@ -83,6 +85,10 @@ bool uniform_shape(int K, int* G, int* P);
 int launch_bellman(ipi_mdp* h, const double* v_full, int32_t mode, int32_t* policy,
                    double* applied, double* g_pi, int32_t* len_pi,
                    unsigned long long* res_bits, cudaStream_t st);
+
+// bellman.cu: flat-row cp.async ring (variant 4)
+int flat_ring_smem(int K, int stages, int warps, int m, int window_bytes);
+bool k1_ring_prepare(int K, int S, int NW, bool win, int smem);
 
 // bellman_tma.cu
 bool k1_tma_plan(int64_t n_states_max_cta, int m, int K, int halo, int64_t n_global, int* SC,

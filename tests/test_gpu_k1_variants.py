@@ -1,0 +1,129 @@
+"""K1 variants against the oracle on identical inputs.
+
+The planner picks one K1 kernel per instance (``plan()["k1_variant"]``); the
+environment switches below force the alternatives so every variant is checked
+on the same arrays.  Flat rows (K <= 4) sum each row left to right from 0.0
+exactly like numpy's reduceat on a segment shorter than 8 (first element, then
+sequential adds), so their Q values are asserted **bitwise** against the
+oracle (`bellman.py:44-68` via `oracle.mdp_oracle.greedy`).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import mdp_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2507_22538_b200 as ipi  # noqa: E402
+from paper_2507_22538_b200.bellman import greedy_device  # noqa: E402
+
+
+def uniform_instance(n, m, K, seed):
+    """K distinct sorted columns per row inside a 100-state band around s."""
+    rng = np.random.default_rng(seed)
+    rows = n * m
+    s = np.arange(rows) // m
+    lo = np.clip(s - 50, 0, n - 100)
+    off = np.sort(rng.random((rows, 100)).argsort(axis=1)[:, :K], axis=1)
+    col = (lo[:, None] + off).astype(np.int64)
+    e = rng.standard_exponential((rows, K))
+    val = e / e.sum(axis=1, keepdims=True)
+    cost = rng.random((n, m))
+    rp = np.arange(rows + 1, dtype=np.int64) * K
+    return rp, col.reshape(-1), val.reshape(-1), cost
+
+
+VARIANTS = {
+    "ring6x12": {"IPI_K1_RING": "1", "IPI_RING_STAGES": "6", "IPI_RING_WARPS": "12"},
+    "ring5x12": {"IPI_K1_RING": "1", "IPI_RING_STAGES": "5", "IPI_RING_WARPS": "12"},
+    "ring4x16": {"IPI_K1_RING": "1", "IPI_RING_STAGES": "4", "IPI_RING_WARPS": "16"},
+    "ring8x8": {"IPI_K1_RING": "1", "IPI_RING_STAGES": "8", "IPI_RING_WARPS": "8"},
+    "ring4x18": {"IPI_K1_RING": "1", "IPI_RING_STAGES": "4", "IPI_RING_WARPS": "18"},
+    "registers": {"IPI_K1_RING": "0"},
+}
+
+
+def expected_variant(variant, K, m):
+    """4 (cp.async ring) when the forced shape fits one CTA per SM, else 5."""
+    if not variant.startswith("ring"):
+        return 5
+    S, NW = (int(x) for x in variant[4:].split("x"))
+    stage = 32 * K * 12 + 17 * 16
+    return 4 if NW * (S * stage + 32 * m * 8) <= 227 * 1024 - 256 else 5
+
+
+@pytest.mark.parametrize("variant", sorted(VARIANTS))
+@pytest.mark.parametrize("K,m,n", [(4, 21, 3000), (4, 1, 20000), (4, 3, 7001), (2, 21, 3000),
+                                   (2, 33, 2500), (4, 40, 1500), (2, 5, 9001)])
+@pytest.mark.parametrize("maximize", [False, True])
+def test_flat_rows_bitwise(monkeypatch, variant, K, m, n, maximize):
+    for k, v in VARIANTS[variant].items():
+        monkeypatch.setenv(k, v)
+    rp, col, val, cost = uniform_instance(n, m, K, seed=K * 1000 + m)
+    gamma = 0.97
+    mode = ipi.Mode.MAX if maximize else ipi.Mode.MIN
+    csr = ipi.CsrMatrix(n * m, n, rp, col, val)
+    mdp = ipi.MdpInstance(n=n, m=m, gamma=gamma, stage_cost=cost, transitions=csr, mode=mode)
+    plan = mdp.plan()
+    assert plan["k1_variant"] == expected_variant(variant, K, m), plan
+    v = np.random.default_rng(7).random(n) * 10
+    res = ipi.greedy_policy(mdp, v)
+    pi_ref, ap_ref = orc.greedy(rp, col, val, cost, gamma, v, maximize)
+    np.testing.assert_array_equal(res.policy, pi_ref)
+    np.testing.assert_array_equal(res.applied, ap_ref)  # bitwise
+    # the fused residual equals the host max |v - TV|
+    vd = torch.as_tensor(v, device="cuda")
+    _, ap, rb = greedy_device(mdp, vd, mode, with_residual=True)
+    assert float(rb.view(torch.float64)[0]) == float(np.max(np.abs(v - ap_ref)))
+
+
+@pytest.mark.parametrize("variant", ["ring6x12", "ring8x8", "registers"])
+def test_flat_rows_ties_first_index(monkeypatch, variant):
+    for k, v in VARIANTS[variant].items():
+        monkeypatch.setenv(k, v)
+    n, m, K = 4000, 6, 4
+    rp, col, val, cost = uniform_instance(n, m, K, seed=5)
+    # make actions 0, 2, 4 and 1, 3, 5 identical rows: exact ties everywhere
+    col2 = col.reshape(n, m, K)
+    val2 = val.reshape(n, m, K)
+    col2[:, 2] = col2[:, 4] = col2[:, 0]
+    val2[:, 2] = val2[:, 4] = val2[:, 0]
+    col2[:, 3] = col2[:, 5] = col2[:, 1]
+    val2[:, 3] = val2[:, 5] = val2[:, 1]
+    cost[:, 2] = cost[:, 4] = cost[:, 0]
+    cost[:, 3] = cost[:, 5] = cost[:, 1]
+    col, val = col2.reshape(-1), val2.reshape(-1)
+    csr = ipi.CsrMatrix(n * m, n, rp, col, val)
+    mdp = ipi.MdpInstance(n=n, m=m, gamma=0.9, stage_cost=cost, transitions=csr)
+    v = np.random.default_rng(3).random(n)
+    res = ipi.greedy_policy(mdp, v)
+    pi_ref, ap_ref = orc.greedy(rp, col, val, cost, 0.9, v, False)
+    np.testing.assert_array_equal(res.policy, pi_ref)
+    assert set(np.unique(res.policy)) <= {0, 1}
+    np.testing.assert_array_equal(res.applied, ap_ref)
+
+
+def test_flat_ring_matches_registers_on_c3_slice(monkeypatch):
+    """Pendulum rows (explicit zero weights, periodic wrap) through both flat kernels."""
+    from paper_2507_22538_b200 import devgen
+    outs = []
+    for variant in ("ring6x12", "registers"):
+        for k, v in VARIANTS[variant].items():
+            monkeypatch.setenv(k, v)
+        rp, col, val, cost, spec, nn = devgen.build_arrays(3, grid=256)
+        csr = ipi.CsrMatrix(nn * spec.m, nn, rp, col, val)
+        mdp = ipi.MdpInstance(nn, spec.m, spec.gamma, cost, csr)
+        v = torch.linspace(0, 10, nn, dtype=torch.float64, device="cuda")
+        pi, ap, rb = greedy_device(mdp, v, ipi.Mode.MIN, with_residual=True)
+        torch.cuda.synchronize()
+        outs.append((pi.cpu(), ap.cpu(), int(rb[0])))
+    assert torch.equal(outs[0][0], outs[1][0])
+    assert torch.equal(outs[0][1], outs[1][1])
+    assert outs[0][2] == outs[1][2]
