@@ -108,8 +108,8 @@ typedef struct {
   int32_t uniform_rows;    /* all rows have the same length: P_pi row_ptr is s*K */
   int32_t k1_variant;      /* 0 generic rows, 1 uniform rows (registers), 2 uniform rows (TMA ring),
                               3 uniform rows (deep registers), 4 flat rows (cp.async ring),
-                              5 flat rows (registers) */
-  int32_t k1_stages;       /* shared-memory ring stages (variants 2 and 4) */
+                              5 flat rows (registers), 6 uniform rows (cp.async ring) */
+  int32_t k1_stages;       /* shared-memory ring stages (variants 2, 4, 6) */
   int32_t k1_tma_chunk_states; /* states per TMA stage (variant 2) */
 } ipi_plan;
 

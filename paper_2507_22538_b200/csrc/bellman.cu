@@ -686,6 +686,242 @@ bool k1_ring_prepare(int K, int S, int NW, bool win, int smem) {
 }
 
 // ---------------------------------------------------------------------------
+// Uniform rows, shared-memory ring (9 <= K <= 129, K % 4 == 0, m % 4 == 0;
+// C2/C5: K = 64, m = 32).
+//
+// Same streaming scheme as the flat ring above: each warp moves its
+// contiguous row range through a private S-stage cp.async ring (4 rows per
+// stage), so the CSR stream costs no registers in flight and every copy
+// instruction moves 512 contiguous bytes.  A stage is one warp step: 8 lanes
+// per row, 4 rows.  The row sum restates numpy's reduceat arithmetic exactly
+// (a[0] + pairwise(a[1:]); for 8 <= K-1 <= 128 pairwise keeps 8 running sums
+// r[j] = a[1+j] + a[9+j] + ..., folds them as ((r0+r1)+(r2+r3))+((r4+r5)+
+// (r6+r7)) and adds the (K-1) % 8 leftover terms in order): lane j of a row
+// owns r[j], the fold is three xor shuffles, the leftovers are added in
+// order from shuffles -- so Q is bitwise the reference's.  Shared-memory
+// stage rows are XOR-swizzled at 16-byte granularity so the 4 rows of a
+// step hit disjoint banks.  V gathers of step i+1 are issued before step i
+// is reduced.  The argmin keeps one running (q, a) per row group (actions
+// a = g mod 4) and merges the 4 groups with two xor shuffles per state.
+// ---------------------------------------------------------------------------
+template <int K>
+struct URingLayout {
+  static constexpr int kVal = 4 * K * 8;   // 4 rows of values
+  static constexpr int kCol = 4 * K * 4;   // 4 rows of columns
+  static constexpr int kStage = kVal + kCol + 32;  // + 4 costs
+};
+
+int uniform_ring_smem(int K, int stages, int warps, int window_bytes) {
+  const int st = 4 * K * 12 + 32;
+  return ((window_bytes + 15) & ~15) + warps * stages * st;
+}
+
+template <int K, int NW, int S, bool WIN>
+__global__ void __launch_bounds__(NW * 32, 1) k1_bellman_uring(K1Args a, int win_bytes) {
+  constexpr int N1 = K - 1;       // pairwise runs over a[1 .. K-1]
+  constexpr int NC = N1 / 8;      // terms per running sum
+  constexpr int TAIL = N1 % 8;    // leftover terms added in order
+  static_assert(N1 >= 8 && N1 <= 128 && K % 4 == 0, "uniform ring: 9 <= K <= 129, K % 4 == 0");
+  static_assert(S >= 3, "ring needs >= 3 stages");
+  using L = URingLayout<K>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double red[32];
+  double* win = reinterpret_cast<double*>(smem_raw);
+  const int64_t s_lo = a.bounds[blockIdx.x], s_hi = a.bounds[blockIdx.x + 1];
+  int w_lo = 0;
+  uint32_t w_len = 0;
+  if (WIN) {
+    int64_t lo = a.state0 + s_lo - a.halo;
+    int64_t hi = a.state0 + s_hi + a.halo;
+    lo = lo < 0 ? 0 : lo;
+    hi = hi > a.n_global ? a.n_global : hi;
+    w_lo = (int)lo;
+    w_len = hi > lo ? (uint32_t)(hi - lo) : 0u;
+    for (uint32_t i = threadIdx.x; i < w_len; i += blockDim.x) win[i] = __ldg(a.v + lo + i);
+    __syncthreads();
+  }
+  const uint64_t pol = policy_evict_first();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int grp = lane >> 3, j = lane & 7;  // row of the step, lane within the row
+  const int m = a.m;
+  unsigned char* ring = smem_raw + (((WIN ? win_bytes : 0) + 15) & ~15) + warp * S * L::kStage;
+  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
+  const bool mx = a.maximize != 0;
+  double res = 0.0;
+  auto gather = [&](int c) -> double {
+    if (WIN) {
+      const uint32_t off = (uint32_t)(c - w_lo);
+      if (off < w_len) return win[off];
+    }
+    return __ldg(a.v + c);
+  };
+  const int64_t ns = s_hi - s_lo;
+  const int64_t ws0 = s_lo + ns * warp / NW, ws1 = s_lo + ns * (warp + 1) / NW;
+  const int64_t r_beg = ws0 * m;
+  const int64_t nb = (ws1 - ws0) * m / 4;  // steps (m % 4 == 0)
+
+  // 16-byte chunk cc of row r lives at chunk cc ^ swz(r): rows of a step on disjoint banks
+  // values: LDS.64 half-warp = rows {0,1} / {2,3}: flip 64 B for odd rows
+  // columns: LDS.32 full warp = rows 0..3: flip 32 B * r
+  auto issue = [&](int64_t i, int stg) {
+    if (i < nb) {
+      const int64_t row0 = r_beg + 4 * i;
+      const uint32_t st = ring_s + (uint32_t)(stg * L::kStage);
+      const double* vp = a.val + row0 * K;
+      const int* cp = a.col + row0 * K;
+#pragma unroll
+      for (int c = lane; c < 4 * K / 2; c += 32) {  // value chunks (2 doubles)
+        const int r = c / (K / 2), cc = c % (K / 2);
+        cp_async16(st + r * K * 8 + 16 * (cc ^ ((r & 1) << 2)), vp + 2 * c, 16, pol);
+      }
+#pragma unroll
+      for (int c = lane; c < 4 * K / 4; c += 32) {  // column chunks (4 ints)
+        const int r = c / (K / 4), cc = c % (K / 4);
+        cp_async16(st + L::kVal + r * K * 4 + 16 * (cc ^ (r << 1)), cp + 4 * c, 16, pol);
+      }
+      if (lane < 2) cp_async16(st + L::kVal + L::kCol + 16 * lane, a.cost + row0 + 2 * lane, 16, pol);
+    }
+    cp_async_commit();
+  };
+  auto vaddr = [&](int r, int e) {  // byte offset of value e of row r
+    return r * K * 8 + ((((e >> 1) ^ ((r & 1) << 2))) << 4) + ((e & 1) << 3);
+  };
+  auto caddr = [&](int r, int e) {  // byte offset of column e of row r
+    return L::kVal + r * K * 4 + ((((e >> 2) ^ (r << 1))) << 4) + ((e & 3) << 2);
+  };
+  // gathers of step i: NC chain terms a[1+j+8k] and one leftover/first term
+  constexpr int NG = NC + 1;
+  auto fetch = [&](int stg, double (&x)[NG]) {
+    const unsigned char* st = ring + stg * L::kStage;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) x[k] = gather(*reinterpret_cast<const int*>(st + caddr(grp, 1 + j + 8 * k)));
+    const int e_last = j < TAIL ? 1 + 8 * NC + j : 0;  // leftover term, lane 7: a[0]
+    if (j < TAIL || j == 7) x[NC] = gather(*reinterpret_cast<const int*>(st + caddr(grp, e_last)));
+  };
+  int t_in_state = 0;
+  int64_t s_cur = ws0;
+  double bq = INFINITY;
+  int ba = INT_MAX;
+  auto compute = [&](int stg, const double (&x)[NG]) {
+    const unsigned char* st = ring + stg * L::kStage;
+    auto val = [&](int e) { return *reinterpret_cast<const double*>(st + vaddr(grp, e)); };
+    double r = mul_rn(val(1 + j), x[0]);
+#pragma unroll
+    for (int k = 1; k < NC; ++k) r = add_rn(r, mul_rn(val(1 + j + 8 * k), x[k]));
+    r = add_rn(r, __shfl_xor_sync(kFull, r, 1));
+    r = add_rn(r, __shfl_xor_sync(kFull, r, 2));
+    r = add_rn(r, __shfl_xor_sync(kFull, r, 4));
+    const int e_last = j < TAIL ? 1 + 8 * NC + j : 0;
+    const double pl = (j < TAIL || j == 7) ? mul_rn(val(e_last), x[NC]) : 0.0;
+#pragma unroll
+    for (int t = 0; t < TAIL; ++t) r = add_rn(r, __shfl_sync(kFull, pl, (grp << 3) + t));
+    const double total = add_rn(__shfl_sync(kFull, pl, (grp << 3) + 7), r);
+    const double g = reinterpret_cast<const double*>(st + L::kVal + L::kCol)[grp];
+    double q = add_rn(g, mul_rn(a.gamma, total));
+    if (mx) q = -q;  // argmax(q) == argmin(-q), first index on ties either way
+    const int act = 4 * t_in_state + grp;
+    if (q < bq) {  // actions of a group arrive in increasing order
+      bq = q;
+      ba = act;
+    }
+    if (++t_in_state == (m >> 2)) {  // state complete: merge the 4 groups
+#pragma unroll
+      for (int off = 8; off <= 16; off <<= 1) {
+        const double oq = __shfl_xor_sync(kFull, bq, off);
+        const int oa = __shfl_xor_sync(kFull, ba, off);
+        if (oq < bq || (oq == bq && oa < ba)) {
+          bq = oq;
+          ba = oa;
+        }
+      }
+      if (lane == 0) {
+        const int64_t s = s_cur;
+        const double ap = mx ? -bq : bq;
+        const int pa = ba == INT_MAX ? 0 : ba;
+        a.policy[s] = pa;
+        a.applied[s] = ap;
+        if (a.gpi) a.gpi[s] = __ldg(a.cost + s * m + pa);
+        if (a.lenpi) a.lenpi[s] = K;
+        res = fmax(res, fabs(sub_rn(gather((int)(a.state0 + s)), ap)));
+      }
+      t_in_state = 0;
+      ++s_cur;
+      bq = INFINITY;
+      ba = INT_MAX;
+    }
+  };
+  int stg = 0;
+  auto step = [&](int64_t i, const double (&cur)[NG], double (&nxt)[NG]) {
+    const int s1 = stg + 1 == S ? 0 : stg + 1;
+    cp_async_wait<S - 2>();  // step i+1 landed (this lane's copies)
+    __syncwarp();            // ... and every lane's
+    if (i + 1 < nb) fetch(s1, nxt);
+    compute(stg, cur);
+    __syncwarp();  // stage i fully consumed
+    issue(i + S, stg);
+    stg = s1;
+  };
+  if (nb > 0) {
+#pragma unroll 1
+    for (int q = 0; q < S; ++q) issue(q, q);
+    double x0[NG], x1[NG];
+#pragma unroll
+    for (int k = 0; k < NG; ++k) x0[k] = x1[k] = 0.0;
+    cp_async_wait<S - 1>();
+    __syncwarp();
+    fetch(0, x0);
+#pragma unroll 1
+    for (int64_t i = 0; i < nb; i += 2) {
+      step(i, x0, x1);
+      if (i + 1 < nb) step(i + 1, x1, x0);
+    }
+  }
+  cp_async_wait<0>();
+  if (a.res_bits) {
+    res = warp_max(res);
+    if (lane == 0) red[warp] = res;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < NW; ++w) t = fmax(t, red[w]);
+      atomicMax(a.res_bits, (unsigned long long)__double_as_longlong(t));
+    }
+  }
+}
+
+template <int K, int NW, int S, bool WIN>
+static cudaError_t uring_attr(int smem) {
+  return cudaFuncSetAttribute(k1_bellman_uring<K, NW, S, WIN>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+}
+
+template <int K, int NW, int S>
+static void uring_go(const K1Args& a, bool win, int blocks, int smem, int win_bytes, cudaStream_t st) {
+  if (win)
+    k1_bellman_uring<K, NW, S, true><<<blocks, NW * 32, smem, st>>>(a, win_bytes);
+  else
+    k1_bellman_uring<K, NW, S, false><<<blocks, NW * 32, smem, st>>>(a, 0);
+}
+
+// (K, warps, stages) instances
+#define IPI_URING_SHAPES(MACRO)                                                           \
+  MACRO(64, 8, 4) MACRO(64, 10, 3) MACRO(64, 8, 3) MACRO(64, 8, 5) MACRO(64, 10, 4)    \
+  MACRO(64, 12, 3) MACRO(64, 6, 6) MACRO(64, 16, 3) MACRO(64, 11, 3) MACRO(64, 14, 3)
+
+bool k1_uring_prepare(int K, int NW, int S, bool win, int smem) {
+  bool ok = false;
+  cudaError_t e = cudaSuccess;
+#define IPI_U_ATTR(KK, WW, SS)                                                           \
+  if (!ok && K == KK && NW == WW && S == SS) {                                           \
+    ok = true;                                                                           \
+    e = win ? uring_attr<KK, WW, SS, true>(smem) : uring_attr<KK, WW, SS, false>(smem);  \
+  }
+  IPI_URING_SHAPES(IPI_U_ATTR)
+#undef IPI_U_ATTR
+  return ok && e == cudaSuccess;
+}
+
+// ---------------------------------------------------------------------------
 // Deep-pipeline uniform kernel: 16 warps per SM with up to 128 registers each
 // (one 512-thread CTA per SM, one V window per SM).  Bytes in flight are
 // bounded by registers, so fewer warps with deeper rings beat many shallow
@@ -1000,6 +1236,21 @@ int launch_bellman(ipi_mdp* h, const double* v_full, int32_t mode, int32_t* poli
        : k1_bellman_deep<GG, PP, false><<<blocks, kK1Threads, 0, st>>>(a, K))
     IPI_DISPATCH_UNIFORM(G, P, IPI_D_LAUNCH);
 #undef IPI_D_LAUNCH
+    IPI_LAUNCH_CHECK();
+    return IPI_OK;
+  }
+  if (h->plan.k1_variant == 6) {
+    bool ok = false;
+    const int K = h->plan.row_len_max, S = h->plan.k1_stages, NW = h->plan.k1_threads / 32;
+    const bool rw = h->ring_win_bytes > 0;
+#define IPI_U_LAUNCH(KK, WW, SS)                                                     \
+  if (!ok && K == KK && NW == WW && S == SS) {                                       \
+    ok = true;                                                                       \
+    uring_go<KK, WW, SS>(a, rw, blocks, smem, h->ring_win_bytes, st);                \
+  }
+    IPI_URING_SHAPES(IPI_U_LAUNCH)
+#undef IPI_U_LAUNCH
+    if (!ok) return fail(IPI_ECUDA, "k1 uniform ring: no instance for this (K, warps, stages)");
     IPI_LAUNCH_CHECK();
     return IPI_OK;
   }

@@ -392,6 +392,64 @@ int ipi_mdp_create(const int64_t* row_ptr, const int32_t* col, const double* val
       }
     }
   }
+  // ---- uniform rows, K = 64: cp.async ring per warp (bellman.cu) -------------
+  // Shapes (warps, stages, waves): waves > 1 splits each SM's state range over
+  // several CTAs so the V window per CTA shrinks and leaves room for the rings.
+  if (p.k1_variant == 1 && p.uniform_rows && p.row_len_max == 64 && m % 4 == 0 && n_local > 0) {
+    const char* env = getenv("IPI_K1_URING");
+    const bool aligned = ((uintptr_t)values % 16 == 0) && ((uintptr_t)stage_cost % 16 == 0) &&
+                         ((uintptr_t)col % 16 == 0);
+    // measured on C2 (scripts/uring_ab.sh, profiles/r01_uring_shapes.txt): 2 or 4 waves
+    // beat 1, 3 or 6; 10-12 warps x 3 stages beat deeper rings with fewer warps
+    int shapes[6][3] = {{12, 3, 4}, {10, 3, 2}, {11, 3, 2}, {10, 4, 2}, {8, 4, 2}, {8, 3, 2}};
+    int nshape = 6;
+    if (getenv("IPI_URING_WARPS") && getenv("IPI_URING_STAGES") && getenv("IPI_URING_WAVES")) {
+      shapes[0][0] = atoi(getenv("IPI_URING_WARPS"));
+      shapes[0][1] = atoi(getenv("IPI_URING_STAGES"));
+      shapes[0][2] = atoi(getenv("IPI_URING_WAVES"));
+      nshape = 1;
+    }
+    const int budget = 227 * 1024 - 256;  // one CTA per SM
+    bool done = false;
+    for (int si = 0; si < nshape && !(env && env[0] == '0') && aligned && !done; ++si) {
+      const int NW = shapes[si][0], S = shapes[si][1], waves = shapes[si][2];
+      const int blocks = (int)std::min<int64_t>((int64_t)h->num_sms * waves,
+                                                std::max<int64_t>(1, (n_local + 63) / 64));
+      std::vector<int64_t> hb(blocks + 1);
+      for (int c = 0; c <= blocks; ++c) hb[c] = (int64_t)((double)n_local * c / blocks);
+      hb[blocks] = n_local;
+      int64_t worst = 0;
+      for (int c = 0; c < blocks; ++c) worst = std::max<int64_t>(worst, hb[c + 1] - hb[c]);
+      int wbytes = 0;
+      if (p.halo >= 0) {
+        const int64_t wlen = std::min<int64_t>(n_global, worst + 2 * (int64_t)p.halo);
+        wbytes = (int)std::min<int64_t>(wlen * 8, INT32_MAX / 2);
+        if (uniform_ring_smem(64, S, NW, wbytes) > budget) continue;  // keep the window
+      }
+      const int smem = uniform_ring_smem(64, S, NW, wbytes);
+      if (smem > budget || !k1_uring_prepare(64, NW, S, wbytes > 0, smem)) {
+        cudaGetLastError();
+        continue;
+      }
+      int64_t* db = nullptr;
+      if (cudaMalloc(&db, sizeof(int64_t) * (blocks + 1)) == cudaSuccess &&
+          cudaMemcpy(db, hb.data(), sizeof(int64_t) * (blocks + 1), cudaMemcpyHostToDevice) ==
+              cudaSuccess) {
+        cudaFree(h->k1_bounds);
+        h->k1_bounds = db;
+        h->ring_win_bytes = wbytes;
+        p.k1_blocks = blocks;
+        p.k1_threads = NW * 32;
+        p.k1_smem_bytes = smem;
+        p.k1_stages = S;
+        p.k1_variant = 6;
+        done = true;
+      } else {
+        if (db) cudaFree(db);
+        cudaGetLastError();
+      }
+    }
+  }
   // ---- flat rows (K <= 4): cp.async ring per warp (bellman.cu) ---------------
   if (p.uniform_rows && p.row_len_max <= 4 && (p.row_len_max % 2) == 0 && n_local > 0) {
     p.k1_variant = 5;  // register-pipelined flat kernel unless a ring shape fits

@@ -89,6 +89,8 @@ int launch_bellman(ipi_mdp* h, const double* v_full, int32_t mode, int32_t* poli
 // bellman.cu: flat-row cp.async ring (variant 4)
 int flat_ring_smem(int K, int stages, int warps, int m, int window_bytes);
 bool k1_ring_prepare(int K, int S, int NW, bool win, int smem);
+int uniform_ring_smem(int K, int stages, int warps, int window_bytes);
+bool k1_uring_prepare(int K, int NW, int S, bool win, int smem);
 
 // bellman_tma.cu
 bool k1_tma_plan(int64_t n_states_max_cta, int m, int K, int halo, int64_t n_global, int* SC,

@@ -127,3 +127,73 @@ def test_flat_ring_matches_registers_on_c3_slice(monkeypatch):
     assert torch.equal(outs[0][0], outs[1][0])
     assert torch.equal(outs[0][1], outs[1][1])
     assert outs[0][2] == outs[1][2]
+
+
+# ---------------------------------------------------------------------------
+# uniform rows, K = 64 (C2/C5 shape): cp.async ring (variant 6) vs registers
+# ---------------------------------------------------------------------------
+def wide_instance(n, m, K, seed, band):
+    """K distinct sorted columns per row; band=None -> uniform over [0, n)."""
+    rng = np.random.default_rng(seed)
+    rows = n * m
+    s = np.arange(rows) // m
+    if band is None:
+        col = np.sort(np.stack([rng.choice(n, K, replace=False) for _ in range(rows)]), axis=1)
+    else:
+        lo = np.clip(s - band // 2, 0, n - band)
+        off = np.sort(rng.random((rows, band)).argsort(axis=1)[:, :K], axis=1)
+        col = lo[:, None] + off
+    e = rng.standard_exponential((rows, K))
+    val = e / e.sum(axis=1, keepdims=True)
+    cost = rng.random((n, m))
+    rp = np.arange(rows + 1, dtype=np.int64) * K
+    return rp, col.astype(np.int64).reshape(-1), val.reshape(-1), cost
+
+
+UVARIANTS = {
+    "uring8x4": {"IPI_K1_URING": "1", "IPI_URING_WARPS": "8", "IPI_URING_STAGES": "4",
+                 "IPI_URING_WAVES": "1"},
+    "uring10x3": {"IPI_K1_URING": "1", "IPI_URING_WARPS": "10", "IPI_URING_STAGES": "3",
+                  "IPI_URING_WAVES": "1"},
+    "uring8x4w2": {"IPI_K1_URING": "1", "IPI_URING_WARPS": "8", "IPI_URING_STAGES": "4",
+                   "IPI_URING_WAVES": "2"},
+    "uring16x3w3": {"IPI_K1_URING": "1", "IPI_URING_WARPS": "16", "IPI_URING_STAGES": "3",
+                    "IPI_URING_WAVES": "3"},
+    "registers": {"IPI_K1_URING": "0"},
+}
+
+
+@pytest.mark.parametrize("variant", sorted(UVARIANTS))
+@pytest.mark.parametrize("m,n,band", [(32, 3000, 400), (4, 20000, 300), (8, 5000, None),
+                                      (32, 700, None)])
+@pytest.mark.parametrize("maximize", [False, True])
+def test_uniform_rows_k64(monkeypatch, variant, m, n, band, maximize):
+    for k, v in UVARIANTS[variant].items():
+        monkeypatch.setenv(k, v)
+    K = 64
+    rp, col, val, cost = wide_instance(n, m, K, seed=m * 7 + n, band=band)
+    gamma = 0.999
+    mode = ipi.Mode.MAX if maximize else ipi.Mode.MIN
+    csr = ipi.CsrMatrix(n * m, n, rp, col, val)
+    mdp = ipi.MdpInstance(n=n, m=m, gamma=gamma, stage_cost=cost, transitions=csr, mode=mode)
+    plan = mdp.plan()
+    ring = variant.startswith("uring")
+    if ring and plan["k1_variant"] != 6:  # forced shape + resident V window exceed smem
+        assert plan["halo"] >= 0, plan
+        ring = False
+    assert plan["k1_variant"] == (6 if ring else 1), plan
+    v = np.random.default_rng(11).random(n) * 100
+    res = ipi.greedy_policy(mdp, v)
+    pi_ref, ap_ref = orc.greedy(rp, col, val, cost, gamma, v, maximize)
+    if ring:  # numpy reduceat order restated exactly: bitwise
+        np.testing.assert_array_equal(res.policy, pi_ref)
+        np.testing.assert_array_equal(res.applied, ap_ref)
+    else:
+        gap = orc.q_gap(rp, col, val, cost, gamma, v, maximize)
+        bad = np.flatnonzero(res.policy != pi_ref)
+        assert np.all(gap[bad] < 1e-10)
+        np.testing.assert_allclose(res.applied, ap_ref, rtol=1e-13, atol=1e-13)
+    vd = torch.as_tensor(v, device="cuda")
+    pi_d, ap_d, rb = greedy_device(mdp, vd, mode, with_residual=True)
+    want = float(np.max(np.abs(v - ap_d.cpu().numpy())))
+    assert float(rb.view(torch.float64)[0]) == want
