@@ -713,16 +713,20 @@ struct URingLayout {
 
 int uniform_ring_smem(int K, int stages, int warps, int window_bytes) {
   const int st = 4 * K * 12 + 32;
-  return ((window_bytes + 15) & ~15) + warps * stages * st;
+  return ((window_bytes + 15) & ~15) + warps * (stages * st + 256);
 }
 
-template <int K, int NW, int S, bool WIN>
+// D = gather lookahead in steps (1 or 2): V gathers of step i+D are issued
+// before step i is reduced, so the ~10% that miss the window and go to L2
+// have D steps to land.
+template <int K, int NW, int S, int D, bool WIN>
 __global__ void __launch_bounds__(NW * 32, 1) k1_bellman_uring(K1Args a, int win_bytes) {
   constexpr int N1 = K - 1;       // pairwise runs over a[1 .. K-1]
   constexpr int NC = N1 / 8;      // terms per running sum
   constexpr int TAIL = N1 % 8;    // leftover terms added in order
   static_assert(N1 >= 8 && N1 <= 128 && K % 4 == 0, "uniform ring: 9 <= K <= 129, K % 4 == 0");
-  static_assert(S >= 3, "ring needs >= 3 stages");
+  static_assert(D == 1 || D == 2, "gather lookahead is 1 or 2 steps");
+  static_assert(S >= D + 2, "ring needs D + 2 stages");
   using L = URingLayout<K>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double red[32];
@@ -744,16 +748,19 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_bellman_uring(K1Args a, int win
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int grp = lane >> 3, j = lane & 7;  // row of the step, lane within the row
   const int m = a.m;
-  unsigned char* ring = smem_raw + (((WIN ? win_bytes : 0) + 15) & ~15) + warp * S * L::kStage;
+  unsigned char* base_s = smem_raw + (((WIN ? win_bytes : 0) + 15) & ~15) + warp * (S * L::kStage + 256);
+  unsigned char* ring = base_s;
+  double* tb = reinterpret_cast<double*>(base_s + S * L::kStage);  // 32 tail products
   const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
-  const bool mx = a.maximize != 0;
+  const double sgn = a.maximize != 0 ? -1.0 : 1.0;  // argmax(q) == argmin(-q), ties alike
+  const double* __restrict__ vg = a.v;
   double res = 0.0;
   auto gather = [&](int c) -> double {
     if (WIN) {
       const uint32_t off = (uint32_t)(c - w_lo);
       if (off < w_len) return win[off];
     }
-    return __ldg(a.v + c);
+    return __ldg(vg + c);
   };
   const int64_t ns = s_hi - s_lo;
   const int64_t ws0 = s_lo + ns * warp / NW, ws1 = s_lo + ns * (warp + 1) / NW;
@@ -789,14 +796,15 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_bellman_uring(K1Args a, int win
   auto caddr = [&](int r, int e) {  // byte offset of column e of row r
     return L::kVal + r * K * 4 + ((((e >> 2) ^ (r << 1))) << 4) + ((e & 3) << 2);
   };
-  // gathers of step i: NC chain terms a[1+j+8k] and one leftover/first term
+  // gathers of one step: NC chain terms a[1+j+8k] and one leftover/first term
   constexpr int NG = NC + 1;
+  const bool has_last = j < TAIL || j == 7;
+  const int e_last = j < TAIL ? 1 + 8 * NC + j : 0;  // leftover term, lane 7: a[0]
   auto fetch = [&](int stg, double (&x)[NG]) {
     const unsigned char* st = ring + stg * L::kStage;
 #pragma unroll
     for (int k = 0; k < NC; ++k) x[k] = gather(*reinterpret_cast<const int*>(st + caddr(grp, 1 + j + 8 * k)));
-    const int e_last = j < TAIL ? 1 + 8 * NC + j : 0;  // leftover term, lane 7: a[0]
-    if (j < TAIL || j == 7) x[NC] = gather(*reinterpret_cast<const int*>(st + caddr(grp, e_last)));
+    if (has_last) x[NC] = gather(*reinterpret_cast<const int*>(st + caddr(grp, e_last)));
   };
   int t_in_state = 0;
   int64_t s_cur = ws0;
@@ -805,20 +813,27 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_bellman_uring(K1Args a, int win
   auto compute = [&](int stg, const double (&x)[NG]) {
     const unsigned char* st = ring + stg * L::kStage;
     auto val = [&](int e) { return *reinterpret_cast<const double*>(st + vaddr(grp, e)); };
+    tb[lane] = has_last ? mul_rn(val(e_last), x[NC]) : 0.0;
     double r = mul_rn(val(1 + j), x[0]);
 #pragma unroll
     for (int k = 1; k < NC; ++k) r = add_rn(r, mul_rn(val(1 + j + 8 * k), x[k]));
     r = add_rn(r, __shfl_xor_sync(kFull, r, 1));
     r = add_rn(r, __shfl_xor_sync(kFull, r, 2));
     r = add_rn(r, __shfl_xor_sync(kFull, r, 4));
-    const int e_last = j < TAIL ? 1 + 8 * NC + j : 0;
-    const double pl = (j < TAIL || j == 7) ? mul_rn(val(e_last), x[NC]) : 0.0;
+    __syncwarp();
+    const double2* t2 = reinterpret_cast<const double2*>(tb + (grp << 3));
+    double t[8];
 #pragma unroll
-    for (int t = 0; t < TAIL; ++t) r = add_rn(r, __shfl_sync(kFull, pl, (grp << 3) + t));
-    const double total = add_rn(__shfl_sync(kFull, pl, (grp << 3) + 7), r);
+    for (int q = 0; q < 4; ++q) {
+      const double2 u = t2[q];
+      t[2 * q] = u.x;
+      t[2 * q + 1] = u.y;
+    }
+#pragma unroll
+    for (int q = 0; q < TAIL; ++q) r = add_rn(r, t[q]);
+    const double total = add_rn(t[7], r);
     const double g = reinterpret_cast<const double*>(st + L::kVal + L::kCol)[grp];
-    double q = add_rn(g, mul_rn(a.gamma, total));
-    if (mx) q = -q;  // argmax(q) == argmin(-q), first index on ties either way
+    const double q = mul_rn(sgn, add_rn(g, mul_rn(a.gamma, total)));
     const int act = 4 * t_in_state + grp;
     if (q < bq) {  // actions of a group arrive in increasing order
       bq = q;
@@ -836,7 +851,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_bellman_uring(K1Args a, int win
       }
       if (lane == 0) {
         const int64_t s = s_cur;
-        const double ap = mx ? -bq : bq;
+        const double ap = mul_rn(sgn, bq);
         const int pa = ba == INT_MAX ? 0 : ba;
         a.policy[s] = pa;
         a.applied[s] = ap;
@@ -851,29 +866,39 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_bellman_uring(K1Args a, int win
     }
   };
   int stg = 0;
-  auto step = [&](int64_t i, const double (&cur)[NG], double (&nxt)[NG]) {
-    const int s1 = stg + 1 == S ? 0 : stg + 1;
-    cp_async_wait<S - 2>();  // step i+1 landed (this lane's copies)
-    __syncwarp();            // ... and every lane's
-    if (i + 1 < nb) fetch(s1, nxt);
+  auto step = [&](int64_t i, const double (&cur)[NG], double (&ahead)[NG]) {
+    const int sd = stg + D >= S ? stg + D - S : stg + D;
+    cp_async_wait<S - 1 - D>();  // step i+D landed (this lane's copies)
+    __syncwarp();                // ... and every lane's
+    if (i + D < nb) fetch(sd, ahead);
     compute(stg, cur);
-    __syncwarp();  // stage i fully consumed
+    __syncwarp();  // stage i and the tail buffer fully consumed
     issue(i + S, stg);
-    stg = s1;
+    stg = stg + 1 == S ? 0 : stg + 1;
   };
   if (nb > 0) {
 #pragma unroll 1
     for (int q = 0; q < S; ++q) issue(q, q);
-    double x0[NG], x1[NG];
+    double x0[NG], x1[NG], x2[NG];
 #pragma unroll
-    for (int k = 0; k < NG; ++k) x0[k] = x1[k] = 0.0;
-    cp_async_wait<S - 1>();
+    for (int k = 0; k < NG; ++k) x0[k] = x1[k] = x2[k] = 0.0;
+    cp_async_wait<S - D>();  // steps 0 .. D-1 landed
     __syncwarp();
     fetch(0, x0);
+    if (D == 2 && nb > 1) fetch(1, x1);
+    if (D == 1) {
 #pragma unroll 1
-    for (int64_t i = 0; i < nb; i += 2) {
-      step(i, x0, x1);
-      if (i + 1 < nb) step(i + 1, x1, x0);
+      for (int64_t i = 0; i < nb; i += 2) {
+        step(i, x0, x1);
+        if (i + 1 < nb) step(i + 1, x1, x0);
+      }
+    } else {
+#pragma unroll 1
+      for (int64_t i = 0; i < nb; i += 3) {
+        step(i, x0, x2);
+        if (i + 1 < nb) step(i + 1, x1, x0);
+        if (i + 2 < nb) step(i + 2, x2, x1);
+      }
     }
   }
   cp_async_wait<0>();
@@ -889,32 +914,33 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_bellman_uring(K1Args a, int win
   }
 }
 
-template <int K, int NW, int S, bool WIN>
+template <int K, int NW, int S, int D, bool WIN>
 static cudaError_t uring_attr(int smem) {
-  return cudaFuncSetAttribute(k1_bellman_uring<K, NW, S, WIN>,
+  return cudaFuncSetAttribute(k1_bellman_uring<K, NW, S, D, WIN>,
                               cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
 }
 
-template <int K, int NW, int S>
+template <int K, int NW, int S, int D>
 static void uring_go(const K1Args& a, bool win, int blocks, int smem, int win_bytes, cudaStream_t st) {
   if (win)
-    k1_bellman_uring<K, NW, S, true><<<blocks, NW * 32, smem, st>>>(a, win_bytes);
+    k1_bellman_uring<K, NW, S, D, true><<<blocks, NW * 32, smem, st>>>(a, win_bytes);
   else
-    k1_bellman_uring<K, NW, S, false><<<blocks, NW * 32, smem, st>>>(a, 0);
+    k1_bellman_uring<K, NW, S, D, false><<<blocks, NW * 32, smem, st>>>(a, 0);
 }
 
-// (K, warps, stages) instances
+// (K, warps, stages, lookahead) instances
 #define IPI_URING_SHAPES(MACRO)                                                           \
-  MACRO(64, 8, 4) MACRO(64, 10, 3) MACRO(64, 8, 3) MACRO(64, 8, 5) MACRO(64, 10, 4)    \
-  MACRO(64, 12, 3) MACRO(64, 6, 6) MACRO(64, 16, 3) MACRO(64, 11, 3) MACRO(64, 14, 3)
+  MACRO(64, 12, 3, 1) MACRO(64, 10, 3, 1) MACRO(64, 11, 3, 1) MACRO(64, 10, 4, 1)        \
+  MACRO(64, 8, 4, 1) MACRO(64, 8, 3, 1) MACRO(64, 10, 4, 2) MACRO(64, 8, 4, 2)           \
+  MACRO(64, 8, 5, 2) MACRO(64, 12, 4, 2) MACRO(64, 6, 6, 2)
 
-bool k1_uring_prepare(int K, int NW, int S, bool win, int smem) {
+bool k1_uring_prepare(int K, int NW, int S, int D, bool win, int smem) {
   bool ok = false;
   cudaError_t e = cudaSuccess;
-#define IPI_U_ATTR(KK, WW, SS)                                                           \
-  if (!ok && K == KK && NW == WW && S == SS) {                                           \
-    ok = true;                                                                           \
-    e = win ? uring_attr<KK, WW, SS, true>(smem) : uring_attr<KK, WW, SS, false>(smem);  \
+#define IPI_U_ATTR(KK, WW, SS, DD)                                                               \
+  if (!ok && K == KK && NW == WW && S == SS && D == DD) {                                        \
+    ok = true;                                                                                   \
+    e = win ? uring_attr<KK, WW, SS, DD, true>(smem) : uring_attr<KK, WW, SS, DD, false>(smem);  \
   }
   IPI_URING_SHAPES(IPI_U_ATTR)
 #undef IPI_U_ATTR
@@ -1242,11 +1268,12 @@ int launch_bellman(ipi_mdp* h, const double* v_full, int32_t mode, int32_t* poli
   if (h->plan.k1_variant == 6) {
     bool ok = false;
     const int K = h->plan.row_len_max, S = h->plan.k1_stages, NW = h->plan.k1_threads / 32;
+    const int D = h->uring_lookahead;
     const bool rw = h->ring_win_bytes > 0;
-#define IPI_U_LAUNCH(KK, WW, SS)                                                     \
-  if (!ok && K == KK && NW == WW && S == SS) {                                       \
+#define IPI_U_LAUNCH(KK, WW, SS, DD)                                                 \
+  if (!ok && K == KK && NW == WW && S == SS && D == DD) {                            \
     ok = true;                                                                       \
-    uring_go<KK, WW, SS>(a, rw, blocks, smem, h->ring_win_bytes, st);                \
+    uring_go<KK, WW, SS, DD>(a, rw, blocks, smem, h->ring_win_bytes, st);            \
   }
     IPI_URING_SHAPES(IPI_U_LAUNCH)
 #undef IPI_U_LAUNCH

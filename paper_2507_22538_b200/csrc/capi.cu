@@ -399,20 +399,21 @@ int ipi_mdp_create(const int64_t* row_ptr, const int32_t* col, const double* val
     const char* env = getenv("IPI_K1_URING");
     const bool aligned = ((uintptr_t)values % 16 == 0) && ((uintptr_t)stage_cost % 16 == 0) &&
                          ((uintptr_t)col % 16 == 0);
-    // measured on C2 (scripts/uring_ab.sh, profiles/r01_uring_shapes.txt): 2 or 4 waves
-    // beat 1, 3 or 6; 10-12 warps x 3 stages beat deeper rings with fewer warps
-    int shapes[6][3] = {{12, 3, 4}, {10, 3, 2}, {11, 3, 2}, {10, 4, 2}, {8, 4, 2}, {8, 3, 2}};
+    // (warps, stages, waves, lookahead); measured on C2 (scripts/uring_ab.sh,
+    // profiles/r01_uring_shapes.txt): 2 or 4 waves beat 1, 3 or 6
+    int shapes[6][4] = {{12, 3, 4, 1}, {10, 3, 2, 1}, {11, 3, 2, 1}, {10, 4, 2, 1}, {8, 4, 2, 1}, {8, 3, 2, 1}};
     int nshape = 6;
     if (getenv("IPI_URING_WARPS") && getenv("IPI_URING_STAGES") && getenv("IPI_URING_WAVES")) {
       shapes[0][0] = atoi(getenv("IPI_URING_WARPS"));
       shapes[0][1] = atoi(getenv("IPI_URING_STAGES"));
       shapes[0][2] = atoi(getenv("IPI_URING_WAVES"));
+      shapes[0][3] = getenv("IPI_URING_AHEAD") ? atoi(getenv("IPI_URING_AHEAD")) : 1;
       nshape = 1;
     }
     const int budget = 227 * 1024 - 256;  // one CTA per SM
     bool done = false;
     for (int si = 0; si < nshape && !(env && env[0] == '0') && aligned && !done; ++si) {
-      const int NW = shapes[si][0], S = shapes[si][1], waves = shapes[si][2];
+      const int NW = shapes[si][0], S = shapes[si][1], waves = shapes[si][2], D = shapes[si][3];
       const int blocks = (int)std::min<int64_t>((int64_t)h->num_sms * waves,
                                                 std::max<int64_t>(1, (n_local + 63) / 64));
       std::vector<int64_t> hb(blocks + 1);
@@ -427,7 +428,7 @@ int ipi_mdp_create(const int64_t* row_ptr, const int32_t* col, const double* val
         if (uniform_ring_smem(64, S, NW, wbytes) > budget) continue;  // keep the window
       }
       const int smem = uniform_ring_smem(64, S, NW, wbytes);
-      if (smem > budget || !k1_uring_prepare(64, NW, S, wbytes > 0, smem)) {
+      if (smem > budget || !k1_uring_prepare(64, NW, S, D, wbytes > 0, smem)) {
         cudaGetLastError();
         continue;
       }
@@ -442,6 +443,7 @@ int ipi_mdp_create(const int64_t* row_ptr, const int32_t* col, const double* val
         p.k1_threads = NW * 32;
         p.k1_smem_bytes = smem;
         p.k1_stages = S;
+        h->uring_lookahead = D;
         p.k1_variant = 6;
         done = true;
       } else {

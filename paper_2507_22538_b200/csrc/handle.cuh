@@ -45,6 +45,7 @@ struct ipi_mdp {
       tma_stage = 0, tma_halo = -1;
   // K1 flat-row cp.async ring (variant 4): window bytes in front of the rings
   int ring_win_bytes = 0;
+  int uring_lookahead = 1;  // variant 6: V gathers issued this many steps ahead
 };
 
 namespace ipi {
@@ -90,7 +91,7 @@ int launch_bellman(ipi_mdp* h, const double* v_full, int32_t mode, int32_t* poli
 int flat_ring_smem(int K, int stages, int warps, int m, int window_bytes);
 bool k1_ring_prepare(int K, int S, int NW, bool win, int smem);
 int uniform_ring_smem(int K, int stages, int warps, int window_bytes);
-bool k1_uring_prepare(int K, int NW, int S, bool win, int smem);
+bool k1_uring_prepare(int K, int NW, int S, int D, bool win, int smem);
 
 // bellman_tma.cu
 bool k1_tma_plan(int64_t n_states_max_cta, int m, int K, int halo, int64_t n_global, int* SC,

@@ -157,8 +157,10 @@ UVARIANTS = {
                   "IPI_URING_WAVES": "1"},
     "uring8x4w2": {"IPI_K1_URING": "1", "IPI_URING_WARPS": "8", "IPI_URING_STAGES": "4",
                    "IPI_URING_WAVES": "2"},
-    "uring16x3w3": {"IPI_K1_URING": "1", "IPI_URING_WARPS": "16", "IPI_URING_STAGES": "3",
-                    "IPI_URING_WAVES": "3"},
+    "uring8x4w2d2": {"IPI_K1_URING": "1", "IPI_URING_WARPS": "8", "IPI_URING_STAGES": "4",
+                     "IPI_URING_WAVES": "2", "IPI_URING_AHEAD": "2"},
+    "uring12x4w4d2": {"IPI_K1_URING": "1", "IPI_URING_WARPS": "12", "IPI_URING_STAGES": "4",
+                      "IPI_URING_WAVES": "4", "IPI_URING_AHEAD": "2"},
     "registers": {"IPI_K1_URING": "0"},
 }
 
