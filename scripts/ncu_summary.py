@@ -56,7 +56,7 @@ def report(path, out, alg=None):
     print(json.dumps({k: d[k] for k in ("kernel", "dram_bytes_per_launch")}, indent=1))
 
 
-def launches(path, out):
+def launches(path, out, cmd="python bench.py --steps 2 --warmup 1"):
     lines = open(path).read().splitlines()
     start = next(i for i, l in enumerate(lines) if l.startswith('"ID"'))
     rows = list(csv.reader(lines[start:]))
@@ -72,7 +72,7 @@ def launches(path, out):
         agg[r[ki][:80]][1] += v
     tot = sum(v[1] for v in agg.values())
     outl = ["ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised:",
-            "compare SHARES, not absolutes) on: python bench.py --steps 2 --warmup 1 --no-cpu --no-ipi",
+            f"compare SHARES, not absolutes) on: {cmd}",
             "", f"{'kernel':80s} {'n':>4s} {'ms':>9s} {'share':>6s}"]
     for k, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1])[:20]:
         outl.append(f"{k:80s} {c:4d} {t / 1e6:9.3f} {100 * t / tot:5.1f}%")
@@ -84,4 +84,4 @@ if __name__ == "__main__":
     if sys.argv[1] == "report":
         report(sys.argv[2], sys.argv[3], sys.argv[4] if len(sys.argv) > 4 else None)
     else:
-        launches(sys.argv[2], sys.argv[3])
+        launches(sys.argv[2], sys.argv[3], *sys.argv[4:5])
