@@ -211,6 +211,7 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
   extern __shared__ double win[];
   __shared__ KShared sh;
   const uint64_t pol = policy_evict_first();
+  const uint64_t pol_first = pol, pol_last = policy_evict_last();
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int nblk = gridDim.x;
   const int64_t n = a.n;
@@ -531,7 +532,7 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
         __syncthreads();  // w rows written by group leaders, read per-thread below
         // h_0 partial in a coalesced pass (keeps dependent V0 loads out of the SpMV)
         for (int64_t i = s_lo + tid; i < s_hi; i += nthr)
-          p[0] = add_rn(p[0], mul_rn(V0[i], wl[i - s_lo]));
+          p[0] = add_rn(p[0], mul_rn(ld_hint(V0 + i, pol_last), wl[i - s_lo]));
         for (int l = 0; l <= j; ++l) {
           grid_allreduce<1>(p, a, slot, grid, sh);
           const double hlj = p[0];
@@ -539,16 +540,29 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
           const double* Vl = a.V + (int64_t)l * n;
           const double* Vn = a.V + (int64_t)(l + 1) * n;
           double q = 0.0;
-          if (l < j) {
+          // L2 reuse: V_{l+1} is read here and again as V_l by the next pass
+          // (evict-last); this is V_l's last read in the step (evict-first).
+          // w never aliases the basis: restrict + unroll batch the loads.
+          double* __restrict__ wr = wl - s_lo;
+          if (l < j && !w_shared) {  // w in global: keep it L2-resident too
+#pragma unroll 4
             for (int64_t i = s_lo + tid; i < s_hi; i += nthr) {
-              const double wi = sub_rn(wl[i - s_lo], mul_rn(hlj, Vl[i]));
-              wl[i - s_lo] = wi;
-              q = add_rn(q, mul_rn(Vn[i], wi));
+              const double wi = sub_rn(ld_hint(wr + i, pol_last), mul_rn(hlj, ld_hint(Vl + i, pol_first)));
+              st_hint(wr + i, wi, pol_last);
+              q = add_rn(q, mul_rn(ld_hint(Vn + i, pol_last), wi));
+            }
+          } else if (l < j) {
+#pragma unroll 4
+            for (int64_t i = s_lo + tid; i < s_hi; i += nthr) {
+              const double wi = sub_rn(wr[i], mul_rn(hlj, ld_hint(Vl + i, pol_first)));
+              wr[i] = wi;
+              q = add_rn(q, mul_rn(ld_hint(Vn + i, pol_last), wi));
             }
           } else {
+#pragma unroll 4
             for (int64_t i = s_lo + tid; i < s_hi; i += nthr) {
-              const double wi = sub_rn(wl[i - s_lo], mul_rn(hlj, Vl[i]));
-              wl[i - s_lo] = wi;
+              const double wi = sub_rn(wr[i], mul_rn(hlj, ld_hint(Vl + i, pol_first)));
+              wr[i] = wi;
               q = add_rn(q, mul_rn(wi, wi));
             }
           }
@@ -586,7 +600,8 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
         ++j;
         if (brk == 2) break;  // estimated convergence / invariant subspace
         double* Vnew = a.V + (int64_t)j * n;
-        for (int64_t i = s_lo + tid; i < s_hi; i += nthr) Vnew[i] = wl[i - s_lo] / hnorm;
+        for (int64_t i = s_lo + tid; i < s_hi; i += nthr)  // next SpMV input: keep in L2
+          st_hint(Vnew + i, wl[i - s_lo] / hnorm, pol_last);
         grid.sync();
       }
       if (j == 0) break;

@@ -27,6 +27,9 @@ def main():
     ap.add_argument("--solve", action="store_true")
     ap.add_argument("--scale", type=int, default=1)
     ap.add_argument("--grid", type=int, default=None)
+    ap.add_argument("--max-outer", type=int, default=5)
+    ap.add_argument("--ksp-max-it", type=int, default=None)
+    ap.add_argument("--ksp", default="gmres")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     kw = {}
@@ -47,7 +50,9 @@ def main():
         greedy_device(mdp, v, ipi.Mode.MIN, with_residual=True)
     torch.cuda.synchronize()
     if a.solve:
-        res = ipi.solve(mdp, ipi.SolveOptions(alpha=spec.alpha, tol=spec.atol, max_outer=5))
+        kw = {"ksp_max_it": a.ksp_max_it} if a.ksp_max_it else {}
+        res = ipi.solve(mdp, ipi.SolveOptions(alpha=spec.alpha, tol=spec.atol, max_outer=a.max_outer,
+                                              inner=ipi.InnerSolver(a.ksp), **kw))
         print(f"solve: {res.status.value} outer={res.outer_iterations} "
               f"inner={res.inner_iterations_total} t={res.wall_time:.3f}s "
               f"greedy={res.time_greedy:.3f} asm={res.time_assembly:.3f} inner={res.time_inner:.3f}")
