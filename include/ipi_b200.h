@@ -56,6 +56,12 @@ extern "C" {
 #define IPI_STALLED 2
 
 typedef struct ipi_mdp ipi_mdp;
+typedef struct ipi_op ipi_op;
+
+/* K3 kernel variants of a planned policy operator (ipi_op_create) */
+#define IPI_K3_GENERIC 0 /* G lanes per row through the row pointers (spmv.cu)       */
+#define IPI_K3_URING 1   /* uniform rows 9..129 (K % 4 == 0): cp.async ring, 4 rows/step */
+#define IPI_K3_FLAT 2    /* uniform rows K in {2, 4}: cp.async ring, lane = row        */
 
 /* Inner-solve report (inner.py:87-95 InnerSolveReport). */
 typedef struct {
@@ -112,6 +118,19 @@ typedef struct {
   int32_t k1_stages;       /* shared-memory ring stages (variants 2, 4, 6) */
   int32_t k1_tma_chunk_states; /* states per TMA stage (variant 2) */
 } ipi_plan;
+
+/* Plan of a policy operator (ipi_op_create): exposed for reports/tests. */
+typedef struct {
+  int64_t nnz;
+  int32_t variant;   /* IPI_K3_* */
+  int32_t row_len;   /* uniform row length K (0 = variable) */
+  int32_t halo;      /* shared-memory x window half-width, -1 = none */
+  int32_t blocks;
+  int32_t threads;
+  int32_t smem_bytes;
+  int32_t stages;
+  int32_t lanes_per_row; /* generic variant */
+} ipi_op_plan;
 
 /* Validation summary (model.py:148-194 validate; sparse.py:56-86 check). */
 typedef struct {
@@ -188,6 +207,22 @@ int ipi_apply_J(const int64_t* rp_pi, const int32_t* col_pi, const double* val_p
 int ipi_apply_J_shard(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi,
                       int64_t n_local, int64_t state0, double gamma, const double* x_full,
                       const double* b, double* y, void* stream);
+
+/* Planned policy operator J_pi = I - gamma*P_pi over a row block (PolicyOperator,
+ * sparse.py:272-295).  Rows [0, n_local) of (rp, col, val) are the states
+ * state0 .. state0+n_local-1 of an n_global-state system (state0 = 0,
+ * n_local = n_global for an unsharded operator).  Planning reads the row
+ * statistics and a sampled locality profile (one host sync); the applies
+ * below never synchronise.  The arrays are borrowed for the operator's life. */
+int ipi_op_create(const int64_t* rp, const int32_t* col, const double* val, int64_t n_local,
+                  int64_t n_global, int64_t state0, double gamma, void* stream, ipi_op** out);
+void ipi_op_destroy(ipi_op* op);
+int ipi_op_get_plan(const ipi_op* op, ipi_op_plan* out);
+/* apply (sparse.py:294-295): y = x - gamma*(P x) (b == NULL) or y = b - (x - gamma*(P x))
+ * (inner.py:220/232/276); x_full holds all n_global entries, y and b n_local. */
+int ipi_op_apply(const ipi_op* op, const double* x_full, const double* b, double* y, void* stream);
+/* spmv (sparse.py:189-215): y = P x_full. */
+int ipi_op_spmv(const ipi_op* op, const double* x_full, double* y, void* stream);
 
 /* ---- K4: policy evaluation (inner.py:163-292) ------------------------- */
 /* Jacobi preconditioner of I - gamma P_pi: inv_diag[s] = 1/(1 - gamma P_pi[s,s])

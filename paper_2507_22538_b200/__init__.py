@@ -11,7 +11,7 @@ when the CUDA library or a GPU is missing.
 from .errors import DimensionError, ResourceLimitError, ValidationError
 from .model import (MdpInstance, Mode, Partition, ROW_SUM_TOL, flatten_index, make_partition,
                     require_valid, validate)
-from .sparse import (CsrMatrix, PolicyOperator, dot, gather_policy_cost, gather_policy_matrix,
+from .sparse import (CsrMatrix, DeviceOperator, PolicyOperator, dot, gather_policy_cost, gather_policy_matrix,
                      norm, spmv)
 from .bellman import GreedyResult, bellman_residual, greedy_policy, policy_residual
 from .inner import (GMRES_RESTART, TARGET_FLOOR_SCALE, InnerSolver, InnerSolveReport,
@@ -22,7 +22,7 @@ from .fileio import FileFormatError, read_matrix, write_matrix
 __version__ = "0.1.0"
 
 __all__ = [
-    "CsrMatrix", "DimensionError", "FileFormatError", "GMRES_RESTART", "GreedyResult",
+    "CsrMatrix", "DeviceOperator", "DimensionError", "FileFormatError", "GMRES_RESTART", "GreedyResult",
     "InnerSolveReport", "InnerSolver", "MdpInstance", "Mode", "Partition", "PolicyOperator",
     "Preconditioner", "ROW_SUM_TOL", "ResourceLimitError", "STALL_WINDOW", "SolveOptions",
     "SolveResult", "SolveStatus", "TARGET_FLOOR_SCALE", "ValidationError", "bellman_residual",

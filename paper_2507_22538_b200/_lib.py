@@ -58,6 +58,15 @@ class Plan(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "pad"}
 
 
+class OpPlan(C.Structure):
+    _fields_ = [("nnz", _i64), ("variant", _i32), ("row_len", _i32), ("halo", _i32),
+                ("blocks", _i32), ("threads", _i32), ("smem_bytes", _i32), ("stages", _i32),
+                ("lanes_per_row", _i32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 class Validation(C.Structure):
     _fields_ = [("bad_row_ptr", _i64), ("bad_col_range", _i64), ("bad_col_order", _i64),
                 ("nonfinite_values", _i64), ("first_bad_prob", _i64),
@@ -87,6 +96,11 @@ _SIGS = {
     "ipi_spmv": (C.c_int, [_p, _p, _p, _i64, _i64, _p, _p, _p]),
     "ipi_apply_J": (C.c_int, [_p, _p, _p, _i64, _f64, _p, _p, _p, _p]),
     "ipi_apply_J_shard": (C.c_int, [_p, _p, _p, _i64, _i64, _f64, _p, _p, _p, _p]),
+    "ipi_op_create": (C.c_int, [_p, _p, _p, _i64, _i64, _i64, _f64, _p, C.POINTER(_p)]),
+    "ipi_op_destroy": (None, [_p]),
+    "ipi_op_get_plan": (C.c_int, [_p, C.POINTER(OpPlan)]),
+    "ipi_op_apply": (C.c_int, [_p, _p, _p, _p, _p]),
+    "ipi_op_spmv": (C.c_int, [_p, _p, _p, _p]),
     "ipi_jacobi_inv_diag": (C.c_int, [_p, _p, _p, _i64, _f64, _p, _p]),
     "ipi_inner_solve": (C.c_int, [_p, _p, _p, _i64, _f64, _p, _p, _f64, _i32, _i32, _f64, _p,
                                   C.POINTER(InnerReport), _p]),

@@ -439,21 +439,6 @@ __global__ void __launch_bounds__(kK1Threads, 2) k1_bellman_flat(K1Args a, int K
 //     m entries sequentially: no shuffles, and the policy / applied / g_pi /
 //     residual traffic becomes coalesced.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes,
-                                           uint64_t pol) {
-  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;" ::"r"(dst),
-               "l"(src), "r"(src_bytes), "l"(pol)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
 template <int K>
 struct RingLayout {
   static constexpr int kVal = 32 * K * 8;             // values of 32 rows

@@ -748,6 +748,135 @@ int ipi_apply_J_shard(const int64_t* rp_pi, const int32_t* col_pi, const double*
                      state0);
 }
 
+// ---- planned policy operator (K3) ------------------------------------------
+int ipi_op_create(const int64_t* rp, const int32_t* col, const double* val, int64_t n_local,
+                  int64_t n_global, int64_t state0, double gamma, void* stream, ipi_op** out) {
+  if (!out) return fail(IPI_EVALIDATION, "null output operator");
+  *out = nullptr;
+  if (n_local < 0 || n_global < 1 || state0 < 0 || state0 + n_local > n_global)
+    return fail(IPI_EDIMENSION, "inconsistent operator geometry");
+  ipi_op* op = new ipi_op();
+  op->rp = rp;
+  op->col = col;
+  op->val = val;
+  op->n_local = n_local;
+  op->n_global = n_global;
+  op->state0 = state0;
+  op->gamma = gamma;
+  if (n_local == 0) {
+    *out = op;
+    return IPI_OK;
+  }
+  // row statistics + sampled locality profile: the planner of an m = 1 view
+  ipi_mdp* view = nullptr;
+  int rc = ipi_mdp_create(rp, col, val, val, n_local, n_global, 1, state0, gamma, IPI_MODE_MIN,
+                          stream, &view);
+  if (rc) {
+    delete op;
+    return rc;
+  }
+  const ipi_plan pl = view->plan;
+  const int sms = view->num_sms;
+  ipi_mdp_destroy(view);
+  op->nnz = pl.nnz;
+  op->lanes = pl.lanes_per_row;
+  op->K = pl.uniform_rows ? pl.row_len_max : 0;
+  op->variant = IPI_K3_GENERIC;
+  const char* env = getenv("IPI_K3_RING");
+  const bool allow = !(env && env[0] == '0');
+  const int K = op->K;
+  const bool aligned = ((uintptr_t)val % 16 == 0) && ((uintptr_t)col % (K == 2 ? 8 : 16) == 0);
+  const int budget = 227 * 1024 - 256;
+  // (warps, stages, CTAs per SM); IPI_K3_WARPS/STAGES/WAVES force one shape
+  int shapes[4][3];
+  int nshape = 0;
+  int variant = IPI_K3_GENERIC;
+  if (K == 64) {
+    variant = IPI_K3_URING;
+    const int sh[4][3] = {{11, 3, 1}, {12, 3, 4}, {16, 3, 2}, {8, 4, 4}};
+    std::memcpy(shapes, sh, sizeof(sh));
+    nshape = 4;
+  } else if (K == 4 || K == 2) {
+    variant = IPI_K3_FLAT;
+    const int sh[4][3] = {{24, 4, 1}, {16, 4, 1}, {8, 6, 2}, {16, 4, 1}};
+    std::memcpy(shapes, sh, sizeof(sh));
+    nshape = 3;
+  }
+  if (nshape && getenv("IPI_K3_WARPS") && getenv("IPI_K3_STAGES") && getenv("IPI_K3_WAVES")) {
+    shapes[0][0] = atoi(getenv("IPI_K3_WARPS"));
+    shapes[0][1] = atoi(getenv("IPI_K3_STAGES"));
+    shapes[0][2] = atoi(getenv("IPI_K3_WAVES"));
+    nshape = 1;
+  }
+  const int align = variant == IPI_K3_FLAT ? 32 : 4;
+  for (int si = 0; si < nshape && allow && aligned && pl.uniform_rows; ++si) {
+    const int NW = shapes[si][0], S = shapes[si][1], waves = shapes[si][2];
+    const int64_t per_warp_min = variant == IPI_K3_FLAT ? 64 : 16;
+    const int blocks = (int)std::min<int64_t>((int64_t)sms * waves,
+                                              std::max<int64_t>(1, n_local / (NW * per_warp_min)));
+    const int64_t worst = (n_local + blocks - 1) / blocks + 2 * align;
+    int wbytes = 0;
+    if (pl.halo >= 0) {  // + 2: the window start is rounded down to an even index
+      const int64_t wlen = std::min<int64_t>(n_global, worst + 2 * (int64_t)pl.halo) + 2;
+      wbytes = (int)std::min<int64_t>(wlen * 8, INT32_MAX / 2);
+    }
+    int smem = variant == IPI_K3_FLAT ? k3_flat_smem(K, S, NW, wbytes) : k3_uring_smem(K, S, NW, wbytes);
+    if (smem > budget && wbytes > 0) {  // drop the window rather than the ring
+      wbytes = 0;
+      smem = variant == IPI_K3_FLAT ? k3_flat_smem(K, S, NW, 0) : k3_uring_smem(K, S, NW, 0);
+    }
+    if (smem > budget || !k3_shape_prepare(variant, K, NW, S, wbytes > 0, smem)) continue;
+    op->variant = variant;
+    op->blocks = blocks;
+    op->warps = NW;
+    op->stages = S;
+    op->smem = smem;
+    op->win_bytes = wbytes;
+    op->halo = wbytes > 0 ? pl.halo : -1;
+    op->pf = getenv("IPI_K3_PF") ? atoi(getenv("IPI_K3_PF")) : 0;
+    break;
+  }
+  *out = op;
+  return IPI_OK;
+}
+
+void ipi_op_destroy(ipi_op* op) { delete op; }
+
+int ipi_op_get_plan(const ipi_op* op, ipi_op_plan* out) {
+  if (!op || !out) return fail(IPI_EVALIDATION, "null operator");
+  out->nnz = op->nnz;
+  out->variant = op->variant;
+  out->row_len = op->K;
+  out->halo = op->halo;
+  out->blocks = op->blocks;
+  out->threads = op->warps * 32;
+  out->smem_bytes = op->smem;
+  out->stages = op->stages;
+  out->lanes_per_row = op->lanes;
+  return IPI_OK;
+}
+
+static int op_run(const ipi_op* op, const double* x_full, const double* b, int epi, double* y,
+                  void* stream) {
+  if (!op) return fail(IPI_EVALIDATION, "null operator");
+  if (op->n_local > 0 && (!x_full || !y)) return fail(IPI_EVALIDATION, "null vector");
+  if (op->variant != IPI_K3_GENERIC &&
+      ((b && (uintptr_t)b % 16 != 0) || (op->win_bytes > 0 && (uintptr_t)x_full % 16 != 0))) {
+    ipi_op generic = *op;  // b and window chunks are copied 16 bytes at a time
+    generic.variant = IPI_K3_GENERIC;
+    return op_launch(&generic, x_full, b, epi, y, (cudaStream_t)stream);
+  }
+  return op_launch(op, x_full, b, epi, y, (cudaStream_t)stream);
+}
+
+int ipi_op_apply(const ipi_op* op, const double* x_full, const double* b, double* y, void* stream) {
+  return op_run(op, x_full, b, b ? 2 : 1, y, stream);
+}
+
+int ipi_op_spmv(const ipi_op* op, const double* x_full, double* y, void* stream) {
+  return op_run(op, x_full, nullptr, 0, y, stream);
+}
+
 int ipi_jacobi_inv_diag(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi,
                         int64_t n, double gamma, double* inv_diag, void* stream) {
   if (!inv_diag) return fail(IPI_EVALIDATION, "null output");

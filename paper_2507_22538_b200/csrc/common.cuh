@@ -100,6 +100,28 @@ __device__ __forceinline__ int2 ld_stream_v2(const int* p, uint64_t pol) {
   return v;
 }
 
+// cp.async (Ampere-style async copies into shared memory): the per-warp
+// streaming rings of K1 (bellman.cu) and K3 (spmv_ring.cu).
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes,
+                                           uint64_t pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;" ::"r"(dst),
+               "l"(src), "r"(src_bytes), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Bulk L2 prefetch of a contiguous byte range (16-byte aligned, multiple of 16).
+__device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 // Register batch of P value pairs + column pairs (uniform-row fast paths).
 template <int P>
 struct Batch {

@@ -48,6 +48,22 @@ struct ipi_mdp {
   int uring_lookahead = 1;  // variant 6: V gathers issued this many steps ahead
 };
 
+// A planned policy operator (K3): borrowed P_pi rows + the kernel shape.
+struct ipi_op {
+  const int64_t* rp = nullptr;
+  const int32_t* col = nullptr;
+  const double* val = nullptr;
+  int64_t n_local = 0, n_global = 0, state0 = 0, nnz = 0;
+  double gamma = 0.0;
+  int variant = IPI_K3_GENERIC;
+  int K = 0;          // uniform row length (0 = variable)
+  int lanes = 1;      // generic variant: lanes per row
+  int halo = -1;      // x window half-width (-1 = none)
+  int win_bytes = 0;  // window bytes in front of the rings
+  int blocks = 0, warps = 0, stages = 0, smem = 0;
+  int pf = 0;         // uniform ring: L2 prefetch distance (steps)
+};
+
 namespace ipi {
 
 constexpr int kK1Threads = 512;
@@ -110,6 +126,13 @@ int policy_nnz(ipi_mdp* h, const int32_t* policy, int64_t* nnz_out, cudaStream_t
 int launch_spmv(const int64_t* rp, const int32_t* col, const double* val, int64_t rows,
                 const double* x, const double* b, double gamma, int epi, double* y,
                 int lanes, cudaStream_t st, int64_t diag_offset = 0);
+
+// spmv_ring.cu: K3 ring kernels for a planned operator
+int k3_uring_smem(int K, int stages, int warps, int window_bytes);
+int k3_flat_smem(int K, int stages, int warps, int window_bytes);
+bool k3_shape_prepare(int variant, int K, int NW, int S, bool win, int smem);
+int op_launch(const ipi_op* op, const double* x_full, const double* b, int epi, double* y,
+              cudaStream_t st);
 
 // krylov.cu
 int inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi, int64_t n,

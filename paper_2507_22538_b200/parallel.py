@@ -21,7 +21,7 @@ import torch
 
 from . import _lib
 from .model import Mode, Partition, make_partition
-from .sparse import CsrMatrix
+from .sparse import CsrMatrix, DeviceOperator
 
 __all__ = ["MdpShard", "RankContext", "ShardOps", "allgather_blocks", "host_gmres",
            "host_richardson", "rank_max", "rank_ordered_sum", "solve_sharded"]
@@ -174,7 +174,7 @@ class MdpShard:
 # tests, Givens, est_target) agree across ranks without broadcasts.  The
 # numeric phases are the rank-local kernels: K1 on the shard with the
 # all-gathered V, K2 on the local rows, and the sharded J_pi apply
-# (ipi_apply_J_shard) on the all-gathered Krylov vector.  The GMRES /
+# (DeviceOperator: ipi_op_apply) on the all-gathered Krylov vector.  The GMRES /
 # Richardson control logic below restates inner.py:216-292 exactly; it is
 # written against a tiny vector-ops interface so the CPU tests can drive it
 # with gloo and numpy stand-ins.
@@ -226,19 +226,15 @@ class ShardOps:
         _lib.check(L.ipi_gather_policy(h, _lib.ptr(policy_local), _lib.ptr(rp), _lib.ptr(col),
                                        _lib.ptr(val), _lib.ptr(g), _lib.stream_ptr()),
                    "ipi_gather_policy")
-        return (rp, col, val), g
+        # K3 planned once per policy (ring kernel for uniform rows, no sync per apply)
+        op = DeviceOperator(rp, col[:nnz.value], val[:nnz.value], sh.n_local, sh.n_global,
+                            sh.state0, sh.gamma)
+        return op, g
 
     def apply(self, P, x_local: torch.Tensor, b_local: torch.Tensor | None = None) -> torch.Tensor:
         """b - (x - gamma P x) (or x - gamma P x) on the local rows."""
         xf = self.allgather(x_local)
-        rp, col, val = P
-        y = torch.empty_like(x_local)
-        sh = self.shard
-        _lib.check(_lib.lib().ipi_apply_J_shard(
-            _lib.ptr(rp), _lib.ptr(col), _lib.ptr(val), sh.n_local, sh.state0, sh.gamma,
-            _lib.ptr(xf), _lib.ptr(b_local) if b_local is not None else None, _lib.ptr(y),
-            _lib.stream_ptr()), "ipi_apply_J_shard")
-        return y
+        return P.apply(xf, b_local.contiguous() if b_local is not None else None)
 
     def sweep(self, P, g_local, v_local):
         """g_pi + gamma * P_pi v (breakdown fallback, driver.py:190-193)."""

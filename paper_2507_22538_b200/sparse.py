@@ -215,9 +215,59 @@ def gather_policy_cost(mdp, pi):
     return _out(g, was_np)
 
 
+class DeviceOperator:
+    """A planned K3 operator (``ipi_op_create``): J = I - gamma*P over rows
+    [0, n_local) of a P_pi row block whose row r is state ``state0 + r`` of an
+    ``n_global``-state system (state0 = 0, n_local = n_global unsharded).
+    Planning syncs once (row statistics, locality profile); ``apply`` /
+    ``spmv`` never do.  Holds references to the CSR tensors it borrows."""
+
+    def __init__(self, row_ptr: torch.Tensor, col_idx: torch.Tensor, values: torch.Tensor,
+                 n_local: int, n_global: int, state0: int, gamma: float):
+        self._keep = (row_ptr, col_idx, values)
+        self.n_local, self.n_global, self.state0 = int(n_local), int(n_global), int(state0)
+        self.gamma = float(gamma)
+        h = _lib.C.c_void_p()
+        _lib.check(_lib.lib().ipi_op_create(_lib.ptr(row_ptr), _lib.ptr(col_idx), _lib.ptr(values),
+                                            self.n_local, self.n_global, self.state0, self.gamma,
+                                            _lib.stream_ptr(), _lib.C.byref(h)), "ipi_op_create")
+        self._h = h.value
+
+    def plan(self) -> dict:
+        out = _lib.OpPlan()
+        _lib.check(_lib.lib().ipi_op_get_plan(self._h, _lib.C.byref(out)), "ipi_op_get_plan")
+        return out.as_dict()
+
+    def apply(self, x_full: torch.Tensor, b: torch.Tensor | None = None,
+              out: torch.Tensor | None = None) -> torch.Tensor:
+        """x - gamma*(P x) on the rows (b - that when b is given)."""
+        y = out if out is not None else torch.empty(self.n_local, dtype=torch.float64,
+                                                    device=x_full.device)
+        _lib.check(_lib.lib().ipi_op_apply(self._h, _lib.ptr(x_full), _lib.ptr(b), _lib.ptr(y),
+                                           _lib.stream_ptr()), "ipi_op_apply")
+        return y
+
+    def spmv(self, x_full: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        y = out if out is not None else torch.empty(self.n_local, dtype=torch.float64,
+                                                    device=x_full.device)
+        _lib.check(_lib.lib().ipi_op_spmv(self._h, _lib.ptr(x_full), _lib.ptr(y),
+                                          _lib.stream_ptr()), "ipi_op_spmv")
+        return y
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                _lib.lib().ipi_op_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+
 class PolicyOperator:
     """Matrix-free I - gamma*P_pi; ``apply(x) = x - gamma*(P x)`` with that
-    exact two-step rounding (sparse.py:272-295), one fused kernel."""
+    exact two-step rounding (sparse.py:272-295), one fused kernel (K3, planned
+    on the first apply: ``DeviceOperator``)."""
 
     def __init__(self, p_pi: CsrMatrix, gamma: float):
         if p_pi.rows != p_pi.cols:
@@ -226,18 +276,20 @@ class PolicyOperator:
             raise ValueError(f"discount factor must lie in [0, 1), got {gamma}")
         self.p_pi = p_pi
         self.gamma = float(gamma)
+        self._op: DeviceOperator | None = None
 
     @property
     def n(self) -> int:
         return self.p_pi.rows
 
+    def device_operator(self) -> DeviceOperator:
+        if self._op is None:
+            p = self.p_pi
+            self._op = DeviceOperator(p.row_ptr, p.col_idx, p.values, self.n, self.n, 0, self.gamma)
+        return self._op
+
     def apply(self, x, workers=None):
         xt, was_np = _vec(x, self.n, "x")
         if tuple(xt.shape) != (self.n,):
             raise DimensionError(f"apply: vector length {tuple(xt.shape)} != {self.n}")
-        y = torch.empty_like(xt)
-        p = self.p_pi
-        _lib.check(_lib.lib().ipi_apply_J(_lib.ptr(p.row_ptr), _lib.ptr(p.col_idx),
-                                          _lib.ptr(p.values), self.n, self.gamma, _lib.ptr(xt),
-                                          None, _lib.ptr(y), _lib.stream_ptr()), "ipi_apply_J")
-        return _out(y, was_np)
+        return _out(self.device_operator().apply(xt.contiguous()), was_np)
