@@ -9,7 +9,8 @@
 // intra-CTA tree -> per-CTA partial -> every CTA sums all partials in the
 // same fixed order), so every CTA holds bit-identical scalars and runs the
 // reference's control logic (Givens, est_target tightening, caps) redundantly
-// without any broadcast.  Grid barriers are cooperative-groups grid syncs.
+// without any broadcast.  Grid barriers: a release counter + acquire spin
+// (GridBarrier, krylov.cuh) over cooperatively launched (co-resident) CTAs.
 //
 // Semantics mirrored exactly (inner.py line refs):
 //   eff = max(target, 1e-14*max(1,||b||))           :189
@@ -18,6 +19,7 @@
 //          true residual per cycle, est_target = |g_j|*(eff/rn)*0.5       :229-283
 //   back substitution with zero-pivot -> 0                                 :286-292
 // Every vector op uses separate mul/add roundings like numpy (no FMA).
+#include <cstdlib>
 #include <mutex>
 
 #include "krylov.cuh"
@@ -68,7 +70,7 @@ int inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_p
   // one 1024-thread CTA per SM (fewer for tiny systems: >= 32 rows per CTA)
   int blocks = sms;
   if ((int64_t)blocks * 32 > n) blocks = (int)std::max<int64_t>(1, n / 32);
-  const int64_t need = (int64_t)(R + 1) * n + 2 * n + 4 * (int64_t)blocks;
+  const int64_t need = (int64_t)(R + 1) * n + 2 * n + 4 * (int64_t)blocks + 8;
   // caller-owned workspace (per handle, so concurrent handles never share it)
   // or the per-device arena used by the standalone API
   double* ws = (workspace && workspace_doubles >= need) ? workspace : krylov_workspace(n, need);
@@ -85,6 +87,9 @@ int inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_p
   a.w = ws + (int64_t)(R + 1) * n;
   a.r = a.w + n;
   a.partials = a.r + n;
+  a.bar = reinterpret_cast<unsigned*>(a.partials + 4 * (int64_t)blocks);
+  IPI_CUDA_TRY(cudaMemsetAsync(a.bar, 0, 64, st));
+  a.bar_mode = getenv("IPI_K4_BARRIER") ? atoi(getenv("IPI_K4_BARRIER")) : 0;
   a.target = target;
   a.max_it = max_it;
   a.kind = kind;

@@ -55,6 +55,43 @@ struct KArgs {
   int K;         // uniform row length of P_pi (0 = variable)
   const double* invd;  // Jacobi: 1 / (1 - gamma diag(P_pi)); nullptr = identity (inner.py:113-118)
   ipi_inner_report* rep;
+  unsigned* bar;       // grid barrier counter, zeroed before every launch
+  int bar_mode;        // GridBarrier::mode (IPI_K4_BARRIER)
+};
+
+// Grid barrier for the co-resident (cooperatively launched) CTAs: one release
+// add per CTA on a monotone counter + an acquire spin by the CTA's leader.
+// Measured on B200 (scripts/micro/barrier_micro.cu, 148 x 1024 threads):
+// 2.4 us per deterministic all-reduce vs 4.1 us with cooperative-groups
+// grid.sync().  `epoch` advances in every thread so all agree on the target.
+struct GridBarrier {
+  unsigned* ctr;
+  unsigned epoch;
+  int mode;  // 0: counter + acquire spin, 1: cooperative-groups grid.sync(), 2: spin with backoff
+  __device__ __forceinline__ void arrive_and_wait(bool leader) {
+    ++epoch;
+    if (mode == 1) {
+      cg::this_grid().sync();
+      return;
+    }
+    if (leader) {
+      __threadfence();
+      asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(ctr), "r"(1u) : "memory");
+      const unsigned target = epoch * gridDim.x;
+      unsigned seen;
+      while (true) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(ctr) : "memory");
+        if (seen >= target) break;
+        if (mode == 2) __nanosleep(64);
+      }
+      __threadfence();
+    }
+  }
+  __device__ __forceinline__ void sync() {
+    __syncthreads();
+    arrive_and_wait(threadIdx.x == 0);
+    __syncthreads();
+  }
 };
 
 struct KShared {
@@ -68,7 +105,7 @@ struct KShared {
 // Two-level deterministic all-reduce of NV doubles; result in every thread.
 template <int NV>
 __device__ __forceinline__ void grid_allreduce(double (&v)[NV], const KArgs& a, int& slot,
-                                               cg::grid_group& grid, KShared& sh) {
+                                               GridBarrier& gb, KShared& sh) {
   double t[NV];
 #pragma unroll
   for (int k = 0; k < NV; ++k) t[k] = block_sum(v[k], sh.red);
@@ -77,13 +114,15 @@ __device__ __forceinline__ void grid_allreduce(double (&v)[NV], const KArgs& a, 
 #pragma unroll
     for (int k = 0; k < NV; ++k) a.partials[((int64_t)slot * nblk + blockIdx.x) * 2 + k] = t[k];
   }
-  grid.sync();
+  gb.arrive_and_wait(threadIdx.x == 0);
+  __syncthreads();
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
       double s = 0.0;
-      for (int i = lane; i < nblk; i += 32) s = add_rn(s, a.partials[((int64_t)slot * nblk + i) * 2 + k]);
+      for (int i = lane; i < nblk; i += 32)
+        s = add_rn(s, __ldcg(a.partials + ((int64_t)slot * nblk + i) * 2 + k));
       s = warp_sum(s);
       if (lane == 0) sh.bc[k] = s;
     }
@@ -207,7 +246,7 @@ __device__ __forceinline__ void spmv_rows(const KArgs& a, const double* xin, int
 // GMRES kernel does not carry the register pressure of the others.
 template <int G, int P, bool WIN, int KIND>
 __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
-  cg::grid_group grid = cg::this_grid();
+  GridBarrier gb{a.bar, 0u, a.bar_mode};
   extern __shared__ double win[];
   __shared__ KShared sh;
   const uint64_t pol = policy_evict_first();
@@ -229,6 +268,8 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
   // this CTA's slice of w: shared memory when it fits, else its global rows
   const bool w_shared = (s_hi - s_lo) <= a.own_cap;
   double* wl = w_shared ? (win + a.win_cap) : (a.w + s_lo);
+  // GMRES MGS passes on shared-memory copies of the basis slices (see below)
+  const bool staged = WIN && w_shared && 2 * (s_hi - s_lo) <= (int64_t)a.win_cap;
   int slot = 0;
 
   // ---- r = b - (x - gamma P x), ||b||, ||r|| --------------------------------
@@ -239,21 +280,21 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
     r[s] = ri;
     acc2[1] = add_rn(acc2[1], mul_rn(ri, ri));
   });
-  grid_allreduce<2>(acc2, a, slot, grid, sh);
+  grid_allreduce<2>(acc2, a, slot, gb, sh);
   const double bnorm = sqrt(acc2[0]);
   const double rr0 = acc2[1];
   double rn = sqrt(rr0);
   int brk = 0;
   // true residual r = b - A x (x complete after a grid sync); returns ||r||
   auto true_residual = [&]() -> double {
-    grid.sync();
+    gb.sync();
     double q[1] = {0.0};
     spmv_rows<G, P, WIN>(a, x, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
       const double ri = sub_rn(b[s], sub_rn(xs, mul_rn(gam, px)));
       r[s] = ri;
       q[0] = add_rn(q[0], mul_rn(ri, ri));
     });
-    grid_allreduce<1>(q, a, slot, grid, sh);
+    grid_allreduce<1>(q, a, slot, gb, sh);
     return sqrt(q[0]);
   };
   const double eff = fmax(a.target, 1e-14 * fmax(1.0, bnorm));
@@ -270,7 +311,7 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
       q[0] = add_rn(q[0], mul_rn(z, z));
     }
     if (!invd) return -1.0;  // caller reuses rn^2
-    grid_allreduce<1>(q, a, slot, grid, sh);
+    grid_allreduce<1>(q, a, slot, gb, sh);
     return q[0];
   };
 
@@ -292,7 +333,7 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
         yv[i] = ri;
         dv[i] = 0.0;
       }
-      grid.sync();
+      gb.sync();
       double p2[2] = {0.0, 0.0};
       spmv_rows<G, P, WIN>(a, yv, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
         const double u = pcv(s, sub_rn(xs, mul_rn(gam, px)));
@@ -305,7 +346,7 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
       double tau = r0nn, thq = 0.0, eta = 0.0, rho = invd ? zz : rr0, est_target = eff;
       const double r0n = r0nn;
       while (it < a.max_it) {
-        grid_allreduce<2>(p2, a, slot, grid, sh);
+        grid_allreduce<2>(p2, a, slot, gb, sh);
         const double sigma = p2[0], vn = sqrt(p2[1]);
         if (fabs(sigma) <= mul_rn(mul_rn(1e-14, r0n), vn)) { brk = 1; break; }
         const double alpha = rho / sigma;
@@ -324,7 +365,7 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
             }
           } else {
             for (int64_t i = s_lo + tid; i < s_hi; i += nthr) yv[i] = sub_rn(yv[i], mul_rn(alpha, vv[i]));
-            grid.sync();
+            gb.sync();
             spmv_rows<G, P, WIN>(a, yv, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
               const double u = pcv(s, sub_rn(xs, mul_rn(gam, px)));
               uv[s] = u;
@@ -338,10 +379,10 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
           if (tau == 0.0) { brk = 1; break; }
           if (half == 1) {
             double q1[1] = {pw[0]};
-            grid_allreduce<1>(q1, a, slot, grid, sh);
+            grid_allreduce<1>(q1, a, slot, gb, sh);
             pw[0] = q1[0];
           } else {
-            grid_allreduce<2>(pw, a, slot, grid, sh);
+            grid_allreduce<2>(pw, a, slot, gb, sh);
           }
           thq = sqrt(pw[0]) / tau;
           const double c = 1.0 / sqrt(add_rn(1.0, mul_rn(thq, thq)));
@@ -369,7 +410,7 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
           yv[i] = add_rn(wv[i], mul_rn(beta, yv[i]));
           vt[i] = add_rn(mul_rn(beta, uv[i]), mul_rn(b2, vv[i]));
         }
-        grid.sync();
+        gb.sync();
         p2[0] = p2[1] = 0.0;
         spmv_rows<G, P, WIN>(a, yv, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
           const double u = pcv(s, sub_rn(xs, mul_rn(gam, px)));
@@ -401,7 +442,7 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
       double rtn = invd ? sqrt(zz) : rn, rho = invd ? zz : rr0, est = rtn, est_target = eff;
       while (it < a.max_it) {
         if (fabs(rho) <= mul_rn(mul_rn(1e-14, rtn), est)) { brk = 1; break; }
-        grid.sync();
+        gb.sync();
         double p2[2] = {0.0, 0.0};
         spmv_rows<G, P, WIN>(a, pv, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
           const double v = pcv(s, sub_rn(xs, mul_rn(gam, px)));
@@ -409,7 +450,7 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
           p2[0] = add_rn(p2[0], mul_rn(rt[s], v));
           p2[1] = add_rn(p2[1], mul_rn(v, v));
         });
-        grid_allreduce<2>(p2, a, slot, grid, sh);
+        grid_allreduce<2>(p2, a, slot, gb, sh);
         const double sigma = p2[0];
         if (fabs(sigma) <= mul_rn(mul_rn(1e-14, rtn), sqrt(p2[1]))) { brk = 1; break; }
         const double alpha = rho / sigma;
@@ -420,19 +461,19 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
           sv[i] = sval;
           q1[0] = add_rn(q1[0], mul_rn(sval, sval));
         }
-        grid_allreduce<1>(q1, a, slot, grid, sh);
+        grid_allreduce<1>(q1, a, slot, gb, sh);
         const double s_norm = sqrt(q1[0]);
         if (s_norm <= est_target) {
           for (int64_t i = s_lo + tid; i < s_hi; i += nthr) x[i] = add_rn(x[i], mul_rn(alpha, pv[i]));
           ++it;
-          grid.sync();
+          gb.sync();
           double q[1] = {0.0};
           spmv_rows<G, P, WIN>(a, x, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
             const double ri = sub_rn(b[s], sub_rn(xs, mul_rn(gam, px)));
             r[s] = ri;
             q[0] = add_rn(q[0], mul_rn(ri, ri));
           });
-          grid_allreduce<1>(q, a, slot, grid, sh);
+          grid_allreduce<1>(q, a, slot, gb, sh);
           rn = sqrt(q[0]);
           stale = false;
           if (rn <= eff) break;
@@ -448,7 +489,7 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
           est = rtn;
           continue;
         }
-        grid.sync();
+        gb.sync();
         double p3[2] = {0.0, 0.0};
         spmv_rows<G, P, WIN>(a, sv, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
           const double t = pcv(s, sub_rn(xs, mul_rn(gam, px)));
@@ -456,7 +497,7 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
           p3[0] = add_rn(p3[0], mul_rn(t, t));
           p3[1] = add_rn(p3[1], mul_rn(t, sv[s]));
         });
-        grid_allreduce<2>(p3, a, slot, grid, sh);
+        grid_allreduce<2>(p3, a, slot, gb, sh);
         const double tt = p3[0];
         if (tt == 0.0) { brk = 1; break; }
         const double omega = p3[1] / tt;
@@ -471,7 +512,7 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
         }
         ++it;
         stale = true;
-        grid_allreduce<2>(p4, a, slot, grid, sh);
+        grid_allreduce<2>(p4, a, slot, gb, sh);
         est = sqrt(p4[0]);
         if (est <= est_target) {
           rn = true_residual();
@@ -495,14 +536,14 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
       for (int64_t i = s_lo + tid; i < s_hi; i += nthr)
         x[i] = add_rn(x[i], mul_rn(a.scale, pcv(i, r[i])));
       ++it;
-      grid.sync();
+      gb.sync();
       double acc1[1] = {0.0};
       spmv_rows<G, P, WIN>(a, x, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
         const double ri = sub_rn(b[s], sub_rn(xs, mul_rn(gam, px)));
         r[s] = ri;
         acc1[0] = add_rn(acc1[0], mul_rn(ri, ri));
       });
-      grid_allreduce<1>(acc1, a, slot, grid, sh);
+      grid_allreduce<1>(acc1, a, slot, gb, sh);
       rn = sqrt(acc1[0]);
     }
   } else {  // GMRES(30)
@@ -520,7 +561,7 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
         sh.g[0] = beta;
       }
       int j = 0;
-      grid.sync();
+      gb.sync();
       while (j < R && it < a.max_it) {
         const double* Vj = a.V + (int64_t)j * n;
         const double* V0 = a.V;
@@ -530,45 +571,88 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
         });
         ++it;
         __syncthreads();  // w rows written by group leaders, read per-thread below
-        // h_0 partial in a coalesced pass (keeps dependent V0 loads out of the SpMV)
-        for (int64_t i = s_lo + tid; i < s_hi; i += nthr)
-          p[0] = add_rn(p[0], mul_rn(ld_hint(V0 + i, pol_last), wl[i - s_lo]));
-        for (int l = 0; l <= j; ++l) {
-          grid_allreduce<1>(p, a, slot, grid, sh);
-          const double hlj = p[0];
-          if (tid == 0) sh.H[l * R + j] = hlj;
-          const double* Vl = a.V + (int64_t)l * n;
-          const double* Vn = a.V + (int64_t)(l + 1) * n;
-          double q = 0.0;
-          // L2 reuse: V_{l+1} is read here and again as V_l by the next pass
-          // (evict-last); this is V_l's last read in the step (evict-first).
-          // w never aliases the basis: restrict + unroll batch the loads.
-          double* __restrict__ wr = wl - s_lo;
-          if (l < j && !w_shared) {  // w in global: keep it L2-resident too
-#pragma unroll 4
-            for (int64_t i = s_lo + tid; i < s_hi; i += nthr) {
-              const double wi = sub_rn(ld_hint(wr + i, pol_last), mul_rn(hlj, ld_hint(Vl + i, pol_first)));
-              st_hint(wr + i, wi, pol_last);
-              q = add_rn(q, mul_rn(ld_hint(Vn + i, pol_last), wi));
+        if (staged) {
+          // MGS with the basis slices staged in shared memory (the V window is
+          // idle until the next SpMV): V_{l+1} is copied with cp.async before
+          // the all-reduce that produces h_l, so each pass costs one barrier
+          // and shared-memory arithmetic.  Same per-thread element order and
+          // roundings as the global-memory passes below (bit-identical).
+          const int64_t own_n = s_hi - s_lo;
+          const uint32_t vb_s = (uint32_t)__cvta_generic_to_shared(win);
+          auto stage = [&](int l, int buf) {
+            const double* Vs = a.V + (int64_t)l * n + s_lo;
+            const uint32_t dst = vb_s + (uint32_t)(buf * own_n * 8);
+            for (int64_t i = tid; i < own_n; i += nthr) cp_async8(dst + (uint32_t)(i * 8), Vs + i);
+            cp_async_commit();
+          };
+          stage(0, 0);
+          cp_async_wait<0>();
+          for (int64_t i = tid; i < own_n; i += nthr) p[0] = add_rn(p[0], mul_rn(win[i], wl[i]));
+          for (int l = 0; l <= j; ++l) {
+            if (l < j) stage(l + 1, (l + 1) & 1);
+            grid_allreduce<1>(p, a, slot, gb, sh);
+            const double hlj = p[0];
+            if (tid == 0) sh.H[l * R + j] = hlj;
+            if (l < j) cp_async_wait<0>();
+            const double* vl = win + (l & 1) * own_n;
+            const double* vn = win + ((l + 1) & 1) * own_n;
+            double q = 0.0;
+            if (l < j) {
+              for (int64_t i = tid; i < own_n; i += nthr) {
+                const double wi = sub_rn(wl[i], mul_rn(hlj, vl[i]));
+                wl[i] = wi;
+                q = add_rn(q, mul_rn(vn[i], wi));
+              }
+            } else {
+              for (int64_t i = tid; i < own_n; i += nthr) {
+                const double wi = sub_rn(wl[i], mul_rn(hlj, vl[i]));
+                wl[i] = wi;
+                q = add_rn(q, mul_rn(wi, wi));
+              }
             }
-          } else if (l < j) {
-#pragma unroll 4
-            for (int64_t i = s_lo + tid; i < s_hi; i += nthr) {
-              const double wi = sub_rn(wr[i], mul_rn(hlj, ld_hint(Vl + i, pol_first)));
-              wr[i] = wi;
-              q = add_rn(q, mul_rn(ld_hint(Vn + i, pol_last), wi));
-            }
-          } else {
-#pragma unroll 4
-            for (int64_t i = s_lo + tid; i < s_hi; i += nthr) {
-              const double wi = sub_rn(wr[i], mul_rn(hlj, ld_hint(Vl + i, pol_first)));
-              wr[i] = wi;
-              q = add_rn(q, mul_rn(wi, wi));
-            }
+            p[0] = q;
           }
-          p[0] = q;
+        } else {
+          // h_0 partial in a coalesced pass (keeps dependent V0 loads out of the SpMV)
+          for (int64_t i = s_lo + tid; i < s_hi; i += nthr)
+            p[0] = add_rn(p[0], mul_rn(ld_hint(V0 + i, pol_last), wl[i - s_lo]));
+          for (int l = 0; l <= j; ++l) {
+            grid_allreduce<1>(p, a, slot, gb, sh);
+            const double hlj = p[0];
+            if (tid == 0) sh.H[l * R + j] = hlj;
+            const double* Vl = a.V + (int64_t)l * n;
+            const double* Vn = a.V + (int64_t)(l + 1) * n;
+            double q = 0.0;
+            // L2 reuse: V_{l+1} is read here and again as V_l by the next pass
+            // (evict-last); this is V_l's last read in the step (evict-first).
+            // w never aliases the basis: restrict + unroll batch the loads.
+            double* __restrict__ wr = wl - s_lo;
+            if (l < j && !w_shared) {  // w in global: keep it L2-resident too
+  #pragma unroll 4
+              for (int64_t i = s_lo + tid; i < s_hi; i += nthr) {
+                const double wi = sub_rn(ld_hint(wr + i, pol_last), mul_rn(hlj, ld_hint(Vl + i, pol_first)));
+                st_hint(wr + i, wi, pol_last);
+                q = add_rn(q, mul_rn(ld_hint(Vn + i, pol_last), wi));
+              }
+            } else if (l < j) {
+  #pragma unroll 4
+              for (int64_t i = s_lo + tid; i < s_hi; i += nthr) {
+                const double wi = sub_rn(wr[i], mul_rn(hlj, ld_hint(Vl + i, pol_first)));
+                wr[i] = wi;
+                q = add_rn(q, mul_rn(ld_hint(Vn + i, pol_last), wi));
+              }
+            } else {
+  #pragma unroll 4
+              for (int64_t i = s_lo + tid; i < s_hi; i += nthr) {
+                const double wi = sub_rn(wr[i], mul_rn(hlj, ld_hint(Vl + i, pol_first)));
+                wr[i] = wi;
+                q = add_rn(q, mul_rn(wi, wi));
+              }
+            }
+            p[0] = q;
+          }
         }
-        grid_allreduce<1>(p, a, slot, grid, sh);
+        grid_allreduce<1>(p, a, slot, gb, sh);
         const double hnorm = sqrt(p[0]);
         if (tid == 0) {
           double* H = sh.H;
@@ -602,7 +686,7 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
         double* Vnew = a.V + (int64_t)j * n;
         for (int64_t i = s_lo + tid; i < s_hi; i += nthr)  // next SpMV input: keep in L2
           st_hint(Vnew + i, wl[i - s_lo] / hnorm, pol_last);
-        grid.sync();
+        gb.sync();
       }
       if (j == 0) break;
       if (tid == 0) {  // back substitution (inner.py:286-292)
@@ -620,14 +704,14 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
         for (int l = 0; l < j; ++l) t = add_rn(t, mul_rn(a.V[(int64_t)l * n + i], sh.y[l]));
         x[i] = add_rn(x[i], t);
       }
-      grid.sync();
+      gb.sync();
       double acc1[1] = {0.0};
       spmv_rows<G, P, WIN>(a, x, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
         const double ri = sub_rn(b[s], sub_rn(xs, mul_rn(gam, px)));
         r[s] = ri;
         acc1[0] = add_rn(acc1[0], mul_rn(ri, ri));
       });
-      grid_allreduce<1>(acc1, a, slot, grid, sh);
+      grid_allreduce<1>(acc1, a, slot, gb, sh);
       rn = sqrt(acc1[0]);
       const double gj = fabs(sh.g[j]);
       if (rn > eff && gj <= est_target) {

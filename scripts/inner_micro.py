@@ -42,21 +42,24 @@ def main():
         b = mdp.stage_cost[torch.arange(mdp.n, device="cuda"), pi.long()].contiguous()
         plan = mdp.plan()
         for kind in ("gmres", "richardson"):
-            for _ in range(2):
-                x = torch.zeros(mdp.n, dtype=torch.float64, device="cuda")
-                rep = _lib.InnerReport()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                h = mdp.handle()
-                e0.record()
-                rc = _lib.lib().ipi_inner_solve(_lib.ptr(p.row_ptr), _lib.ptr(p.col_idx),
-                                                _lib.ptr(p.values), mdp.n, spec.gamma, _lib.ptr(b),
-                                                _lib.ptr(x), 0.0, a.its, _lib.KSP[kind], 1.0,
-                                                _lib.C.byref(rep), _lib.stream_ptr())
-                e1.record()
-                torch.cuda.synchronize()
-                _lib.check(rc)
-            ms = e0.elapsed_time(e1)
-            print(f"{spec.name} {kind}: {rep.iterations} its, {ms / max(rep.iterations, 1):.4f} ms/it, "
+            res = {}
+            for its in (a.its // 2, a.its):  # slope: excludes planning and launch
+                for _ in range(2):
+                    x = torch.zeros(mdp.n, dtype=torch.float64, device="cuda")
+                    rep = _lib.InnerReport()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    rc = _lib.lib().ipi_inner_solve(_lib.ptr(p.row_ptr), _lib.ptr(p.col_idx),
+                                                    _lib.ptr(p.values), mdp.n, spec.gamma, _lib.ptr(b),
+                                                    _lib.ptr(x), 0.0, its, _lib.KSP[kind], 1.0, None,
+                                                    _lib.C.byref(rep), _lib.stream_ptr())
+                    e1.record()
+                    torch.cuda.synchronize()
+                    _lib.check(rc)
+                res[its] = (e0.elapsed_time(e1), rep.iterations)
+            (t0, i0), (t1, i1) = res[a.its // 2], res[a.its]
+            ms = (t1 - t0) / max(i1 - i0, 1)
+            print(f"{spec.name} {kind}: {i1} its, {ms:.4f} ms/it (slope {i0}->{i1}), "
                   f"resid {rep.final_linear_residual_2norm:.3e} plan_halo={plan['halo']}", flush=True)
         del p, mdp
         torch.cuda.empty_cache()
