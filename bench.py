@@ -17,6 +17,8 @@ gamma + per-state argmin + residual max) over every (s, a) row.  The matrix
 with V in pinned host memory and the policy/TV copied back every step.
 ``roofline`` uses the algorithmic bytes of one K1 launch (see
 DESIGN.md) over the K1 launch time measured here with CUDA events.
+``roofline_inner_spmv`` is the same for the policy-evaluation SpMV (K3,
+``PolicyOperator.apply`` on P_pi of the greedy policy of the bench's V).
 ``cpu_baseline`` times the CPU oracle (numpy restatement of greedy_policy,
 bellman.py:44-68) on a bounded sample of the same instance (rank 0, N = 1).
 ``ipi`` reports iPI time-to-tolerance (GMRES, alpha 1e-4, atol 1e-8) on the
@@ -116,12 +118,37 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic():
-    p = REPO / "profiles" / "k1_c2_ncu.json"
+def ncu_traffic(name: str = "k1_c2_ncu.json"):
+    p = REPO / "profiles" / name
     if p.exists():
         d = json.loads(p.read_text())
         return d.get("dram_bytes_per_launch"), d
     return None, None
+
+
+def inner_spmv_roofline(shard, ctx, pol, v_full, n, torch, reps=20):
+    """K3 (the policy-evaluation SpMV, J_pi = I - gamma P_pi applied to the
+    all-gathered vector) on this rank's rows of P_pi for the greedy policy of
+    the bench's V: algorithmic bytes nnz_pi*12 + 8 n_global [x, once] +
+    8 n_local [y] per launch over the CUDA-event launch time (P_pi is 805 MB
+    at C2, 6x L2: no flush needed)."""
+    from paper_2507_22538_b200.parallel import ShardOps
+    ops = ShardOps(shard, ctx)
+    op, _ = ops.gather_policy(pol)
+    y = torch.empty(shard.n_local, dtype=torch.float64, device=v_full.device)
+    for _ in range(3):
+        op.apply(v_full, out=y)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(reps)]
+    for a, b in evs:
+        a.record()
+        op.apply(v_full, out=y)
+        b.record()
+    torch.cuda.synchronize()
+    ms = statistics.median(a.elapsed_time(b) for a, b in evs)
+    plan = op.plan()
+    alg = plan["nnz"] * 12 + 8 * n + 8 * shard.n_local + (8 * (shard.n_local + 1) if plan["variant"] == 0 else 0)
+    return ms, alg, plan
 
 
 def k1_bytes(n: int, m: int, nnz: int, uniform: bool, n_v: int | None = None) -> int:
@@ -362,6 +389,22 @@ def run_ours(args):
             "algorithmic_bytes_per_launch": alg, "k1_ms": ms_k1, "peak_source": peak_src,
             "frac_of_8tbs_spec": achieved / 8000.0}
 
+    # ---- inner SpMV (K3) roofline ---------------------------------------------
+    pol_last, _, _ = shard.bellman(v_full)
+    k3_ms, k3_alg, k3_plan = inner_spmv_roofline(shard, ctx, pol_last.clone(), v_full, n, torch)
+    k3_t = torch.tensor([k3_ms], device=dev)
+    if world > 1:
+        dist.all_reduce(k3_t, op=dist.ReduceOp.MAX)
+    k3_ms = float(k3_t[0])
+    k3_ach = k3_alg / (k3_ms * 1e-3) / 1e9
+    k3_traffic, _ = ncu_traffic("k3_c2_ncu.json")
+    roof_inner = {"bound": "hbm", "achieved": k3_ach, "peak": peak, "unit": "GB/s",
+                  "frac": k3_ach / peak, "traffic": k3_traffic,
+                  "kernel": {1: "k3_uring", 2: "k3_flat"}.get(k3_plan["variant"], "spmv_kernel"),
+                  "algorithmic_bytes_per_launch": k3_alg, "k3_ms": k3_ms, "plan": k3_plan,
+                  "what": "policy-evaluation SpMV y = x - gamma*P_pi x (PolicyOperator.apply) on "
+                          "P_pi of the greedy policy, x all-gathered"}
+
     ipi_sharded = None
     if world > 1 and not args.no_ipi:
         from paper_2507_22538_b200.parallel import ShardOps, solve_sharded
@@ -418,6 +461,7 @@ def run_ours(args):
                     "d2h_bytes_per_step": d2h * world,
                     "path": "greedy_policy(mdp, pinned host V) -> pinned host policy/TV"},
             "roofline": roof,
+            "roofline_inner_spmv": roof_inner,
             "cpu_baseline": cpu,
             "gpu_launches": args.steps,
             "clocks": clk.summary(),
