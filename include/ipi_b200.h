@@ -224,6 +224,16 @@ int ipi_op_apply(const ipi_op* op, const double* x_full, const double* b, double
 /* spmv (sparse.py:189-215): y = P x_full. */
 int ipi_op_spmv(const ipi_op* op, const double* x_full, double* y, void* stream);
 
+/* ---- row-sharded inner solve: device-resident MGS (parallel.py) ------- */
+/* out[0] = <a, b> over n entries (this rank's partial; sparse.py:218-226).
+ * Deterministic (fixed grid, ordered block partials); one stream per device. */
+int ipi_dot_partial(const double* a, const double* b, int64_t n, double* out, void* stream);
+/* One MGS pass of a sharded Arnoldi step (inner.py:251-253):
+ * h = partials[0] + ... + partials[R-1] (rank order), h_out[0] = h,
+ * w -= h*v, out_partial[0] = <v_next, w> (v_next == NULL: <w, w>). */
+int ipi_mgs_pass(const double* partials, int32_t R, double* h_out, double* w, const double* v,
+                 const double* v_next, int64_t n, double* out_partial, void* stream);
+
 /* ---- K4: policy evaluation (inner.py:163-292) ------------------------- */
 /* Jacobi preconditioner of I - gamma P_pi: inv_diag[s] = 1/(1 - gamma P_pi[s,s])
  * (build_preconditioner JACOBI, inner.py:115-118). */

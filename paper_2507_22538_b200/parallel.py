@@ -49,6 +49,34 @@ class RankContext:
         return self.partition.block(self.rank)
 
 
+def _nccl() -> bool:
+    """NCCL takes the flat *_into_tensor collectives; gloo (CPU tests, or CUDA
+    tensors staged through the host) takes tensor lists."""
+    import torch.distributed as dist
+    return dist.get_backend() == "nccl"
+
+
+def gather_partials(part: torch.Tensor, world: int) -> torch.Tensor:
+    """(1,) per-rank partial -> (R,) partials of every rank, in rank order."""
+    import torch.distributed as dist
+    if world == 1 or not (dist.is_available() and dist.is_initialized()):
+        return part.reshape(1)
+    parts = torch.empty(world, dtype=part.dtype, device=part.device)
+    if _nccl():
+        dist.all_gather_into_tensor(parts, part.reshape(1).contiguous())
+    else:
+        dist.all_gather(list(parts.split(1)), part.reshape(1).contiguous())
+    return parts
+
+
+def ordered_sum(parts: torch.Tensor) -> torch.Tensor:
+    """parts[0] + parts[1] + ... in rank order (deterministic like tree_reduce)."""
+    out = parts[0:1].clone()
+    for r in range(1, parts.numel()):
+        out = out + parts[r:r + 1]
+    return out
+
+
 def allgather_blocks(local: torch.Tensor, full: torch.Tensor, partition: Partition) -> torch.Tensor:
     """Fill ``full`` (n) with every rank's block; ``local`` is this rank's.
 
@@ -63,7 +91,7 @@ def allgather_blocks(local: torch.Tensor, full: torch.Tensor, partition: Partiti
     sizes = partition.block_sizes()
     R = partition.worker_count
     if len(set(sizes)) == 1:
-        if full.device.type == "cuda":
+        if _nccl():
             dist.all_gather_into_tensor(full, local.contiguous())
         else:
             parts = list(full.split(sizes))
@@ -73,7 +101,7 @@ def allgather_blocks(local: torch.Tensor, full: torch.Tensor, partition: Partiti
     pad = torch.zeros(mx, dtype=local.dtype, device=local.device)
     pad[: local.numel()] = local
     buf = torch.empty(mx * R, dtype=local.dtype, device=local.device)
-    if buf.device.type == "cuda":
+    if _nccl():
         dist.all_gather_into_tensor(buf, pad)
     else:
         dist.all_gather(list(buf.split(mx)), pad)
@@ -89,7 +117,7 @@ def rank_ordered_sum(partial: torch.Tensor, world: int) -> torch.Tensor:
     if world == 1 or not (dist.is_available() and dist.is_initialized()):
         return partial.clone()
     parts = torch.empty((world,) + tuple(partial.shape), dtype=partial.dtype, device=partial.device)
-    if partial.device.type == "cuda":
+    if _nccl():
         dist.all_gather_into_tensor(parts, partial.contiguous())
     else:
         dist.all_gather(list(parts.unbind(0)), partial.contiguous())
@@ -182,7 +210,37 @@ class MdpShard:
 GMRES_RESTART = 30
 
 
-class ShardOps:
+class ShardVectorOps:
+    """Device-resident scalar primitives of the sharded inner solve.
+
+    Scalars stay tensors until ``to_host`` (one host sync per Arnoldi step):
+    ``dot_partial`` is this rank's share of a dot, ``gather_partials`` the
+    all-gather of the R shares, ``mgs_pass`` one modified Gram-Schmidt pass
+    (inner.py:251-253) on the gathered shares.  These defaults are torch ops
+    (CPU tests over gloo); ``ShardOps`` overrides them with CUDA kernels."""
+
+    ctx: RankContext
+
+    def dot_partial(self, a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+        return torch.dot(a, b).reshape(1)
+
+    def gather_partials(self, part: torch.Tensor) -> torch.Tensor:
+        return gather_partials(part, self.ctx.world)
+
+    def ordered_sum(self, parts: torch.Tensor) -> torch.Tensor:
+        return ordered_sum(parts)
+
+    def mgs_pass(self, parts, w, v, v_next):
+        """h = ordered_sum(parts); w -= h*v (in place); next share <v_next, w> (or <w, w>)."""
+        h = ordered_sum(parts)
+        w.sub_(h * v)
+        return h, self.dot_partial(v_next if v_next is not None else w, w)
+
+    def to_host(self, scalars) -> list[float]:
+        return torch.cat([t.reshape(1) for t in scalars]).cpu().tolist()
+
+
+class ShardOps(ShardVectorOps):
     """Device implementation of the sharded-iPI vector interface for one rank."""
 
     def __init__(self, shard: "MdpShard", ctx: RankContext):
@@ -202,6 +260,20 @@ class ShardOps:
     def max(self, x: float) -> float:
         t = torch.tensor([x], dtype=torch.float64, device=self.full.device)
         return float(rank_max(t)[0])
+
+    def dot_partial(self, a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+        out = torch.empty(1, dtype=torch.float64, device=a.device)
+        _lib.check(_lib.lib().ipi_dot_partial(_lib.ptr(a), _lib.ptr(b), a.numel(), _lib.ptr(out),
+                                              _lib.stream_ptr()), "ipi_dot_partial")
+        return out
+
+    def mgs_pass(self, parts, w, v, v_next):
+        h = torch.empty(1, dtype=torch.float64, device=w.device)
+        nxt = torch.empty(1, dtype=torch.float64, device=w.device)
+        _lib.check(_lib.lib().ipi_mgs_pass(_lib.ptr(parts), parts.numel(), _lib.ptr(h), _lib.ptr(w),
+                                           _lib.ptr(v), _lib.ptr(v_next), w.numel(), _lib.ptr(nxt),
+                                           _lib.stream_ptr()), "ipi_mgs_pass")
+        return h, nxt
 
     # -- kernels ------------------------------------------------------------
     def greedy(self, v_local: torch.Tensor):
@@ -277,10 +349,17 @@ def host_gmres(ops, P, b, theta0, eff, max_it):
         while j < R and it < max_it:
             w = ops.apply(P, V[j])
             it += 1
+            # MGS with the scalars on the device: one kernel + one all-gather of
+            # the R shares per pass, one host sync per step (the H column)
+            part = ops.dot_partial(V[0], w)
+            hs = []
             for l in range(j + 1):
-                H[l][j] = ops.dot(V[l], w)
-                w = w - H[l][j] * V[l]
-            hnorm = math.sqrt(ops.dot(w, w))
+                h, part = ops.mgs_pass(ops.gather_partials(part), w, V[l], V[l + 1] if l < j else None)
+                hs.append(h)
+            vals = ops.to_host(hs + [ops.ordered_sum(ops.gather_partials(part))])
+            for l in range(j + 1):
+                H[l][j] = vals[l]
+            hnorm = math.sqrt(vals[j + 1])
             H[j + 1][j] = hnorm
             for l in range(j):
                 t = cs[l] * H[l][j] + sn[l] * H[l + 1][j]

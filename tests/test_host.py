@@ -293,8 +293,12 @@ def test_rowblock_sharding_gloo_world2():
 # the device kernels; must reproduce the single-process oracle solve
 # ----------------------------------------------------------------------------
 
-class _CpuShardOps:
-    """Test stand-in for parallel.ShardOps: same interface, numpy oracle math."""
+from paper_2507_22538_b200.parallel import ShardVectorOps  # noqa: E402
+
+
+class _CpuShardOps(ShardVectorOps):
+    """Test stand-in for parallel.ShardOps: same interface, numpy oracle math
+    (the device-resident MGS primitives are the torch defaults)."""
 
     def __init__(self, arrays, gamma, ctx):
         import torch
