@@ -635,8 +635,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_bellman_ring(K1Args a, int win_
 
 template <int K, int S, int NW, bool WIN>
 static cudaError_t ring_attr(int smem) {
-  return cudaFuncSetAttribute(k1_bellman_ring<K, S, NW, WIN>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  return raise_smem_limit(k1_bellman_ring<K, S, NW, WIN>, smem);
 }
 
 template <int K, int S, int NW>
@@ -901,8 +900,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_bellman_uring(K1Args a, int win
 
 template <int K, int NW, int S, int D, bool WIN>
 static cudaError_t uring_attr(int smem) {
-  return cudaFuncSetAttribute(k1_bellman_uring<K, NW, S, D, WIN>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  return raise_smem_limit(k1_bellman_uring<K, NW, S, D, WIN>, smem);
 }
 
 template <int K, int NW, int S, int D>
@@ -1133,11 +1131,9 @@ static void launch_u(const K1Args& a, int K, bool win, int blocks, int smem, cud
 
 template <int G, int P>
 static cudaError_t set_smem_attr_u(int smem) {
-  cudaError_t e = cudaFuncSetAttribute(k1_bellman_deep<G, P, true>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = raise_smem_limit(k1_bellman_deep<G, P, true>, smem);
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k1_bellman_uniform<G, P, true>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  return raise_smem_limit(k1_bellman_uniform<G, P, true>, smem);
 }
 
 static cudaError_t uniform_smem(int G, int P, int smem) {
@@ -1158,8 +1154,7 @@ static void launch_g(const K1Args& a, bool win, int blocks, int smem, cudaStream
 
 template <int G>
 static cudaError_t set_smem_attr(int smem) {
-  return cudaFuncSetAttribute(k1_bellman<G, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              smem);
+  return raise_smem_limit(k1_bellman<G, true>, smem);
 }
 
 int k1_set_smem(int lanes, int smem) {
@@ -1173,7 +1168,7 @@ int k1_set_smem(int lanes, int smem) {
     default: e = set_smem_attr<32>(smem); break;
   }
   if (e != cudaSuccess) return fail(IPI_ECUDA, std::string("k1 smem attr: ") + cudaGetErrorString(e));
-  e = cudaFuncSetAttribute(k1_bellman_flat<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  e = raise_smem_limit(k1_bellman_flat<true>, smem);
   if (e != cudaSuccess) return fail(IPI_ECUDA, std::string("k1 smem attr: ") + cudaGetErrorString(e));
   for (int K = 2; K <= 256; K *= 2) {  // make every uniform instance launchable too
     int G, P;

@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k1_bellman_tma(K1TmaArgs a) {
 template <int G, bool WIN>
 static int launch_tma_t(const K1TmaArgs& a, int blocks, int smem, cudaStream_t st) {
   auto fn = k1_bellman_tma<G, WIN>;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = raise_smem_limit(fn, smem);
   if (e != cudaSuccess) return fail(IPI_ECUDA, std::string("k1 tma smem attr: ") + cudaGetErrorString(e));
   fn<<<blocks, kTmaThreads, smem, st>>>(a);
   IPI_LAUNCH_CHECK();

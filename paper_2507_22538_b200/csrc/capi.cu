@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <chrono>
 #include <cstdlib>
 #include <cmath>
@@ -20,6 +22,19 @@ void set_error(const std::string& msg) { g_err = msg; }
 int fail(int code, const std::string& msg) {
   g_err = msg;
   return code;
+}
+
+cudaError_t raise_smem_limit(const void* fn, int smem) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> limits;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  int& cur = limits[{fn, dev}];
+  if (smem <= cur) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess) cur = smem;
+  return e;
 }
 
 int pick_lanes_per_row(double mean_len) {

@@ -20,6 +20,16 @@ constexpr unsigned kFull = 0xffffffffu;
 void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);
 
+// Raise (never lower) a kernel's dynamic shared-memory limit.  The attribute is
+// per function and process-wide, so a later plan with a smaller footprint (a
+// second instance, an m = 1 operator view) must not break the launches of an
+// earlier plan that needs more.
+cudaError_t raise_smem_limit(const void* fn, int smem);
+template <class F>
+inline cudaError_t raise_smem_limit(F* fn, int smem) {
+  return raise_smem_limit(reinterpret_cast<const void*>(fn), smem);
+}
+
 #define IPI_CUDA_TRY(expr)                                                        \
   do {                                                                            \
     cudaError_t _e = (expr);                                                      \

@@ -732,7 +732,7 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
 template <int G, int P, bool WIN, int KIND>
 static int launch_inner_t(KArgs& a, int smem, int blocks, cudaStream_t st) {
   auto fn = inner_kernel<G, P, WIN, KIND>;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = raise_smem_limit(fn, smem);
   if (e != cudaSuccess) return fail(IPI_ECUDA, std::string("inner smem attr: ") + cudaGetErrorString(e));
   int per_sm = 0;
   IPI_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kInnerThreads, smem));

@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k3_flat(K3Args a, int win_bytes) {
 
 template <class F>
 static cudaError_t k3_attr(F fn, int smem) {
-  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  return raise_smem_limit(fn, smem);
 }
 
 template <int K, int NW, int S, bool WIN>

@@ -231,3 +231,18 @@ def test_unaligned_x_falls_back():
     got = host(op.apply(x))
     ref = host(x) - 0.99 * orc.spmv(rp, col, val, host(x))
     np.testing.assert_allclose(got, ref, rtol=1e-13, atol=1e-15)
+
+
+def test_operator_plan_does_not_shrink_k1_smem():
+    """Kernel smem limits are process-wide: planning an m = 1 operator view of
+    P_pi (smaller rings) must not break the instance's own K1 launches."""
+    mdp, spec = devgen.build_instance(3, grid=256)
+    v = torch.zeros(mdp.n, dtype=torch.float64, device="cuda")
+    pi, _, _ = greedy_device(mdp, v, ipi.Mode.MIN)
+    P = ipi.gather_policy_matrix(mdp, pi.long())
+    ipi.PolicyOperator(P, spec.gamma).device_operator()
+    pi2, _, _ = greedy_device(mdp, v, ipi.Mode.MIN)
+    torch.cuda.synchronize()
+    assert torch.equal(pi, pi2)
+    res = ipi.solve(mdp, ipi.SolveOptions(alpha=spec.alpha, tol=spec.atol, max_outer=2))
+    assert res.outer_iterations <= 2
