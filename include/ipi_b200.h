@@ -175,6 +175,10 @@ int ipi_mdp_create(const int64_t* row_ptr, const int32_t* col, const double* val
                    int64_t state0, double gamma, int32_t mode, void* stream, ipi_mdp** out);
 void ipi_mdp_destroy(ipi_mdp* h);
 int ipi_mdp_plan(const ipi_mdp* h, ipi_plan* out);
+/* Diagnostics: enable != 0 starts recording (smid, start ns, end ns) per K1
+ * CTA (uniform-ring kernel) of later ipi_bellman calls; enable == 0 copies up
+ * to cap words of the last launch's record to host `out` and stops. */
+int ipi_mdp_k1_trace(ipi_mdp* h, int32_t enable, uint64_t* out, int32_t cap);
 
 /* validate (model.py:148-194, sparse.py:56-86) on device. */
 int ipi_validate(ipi_mdp* h, ipi_validation* out, void* stream);

@@ -89,6 +89,7 @@ _SIGS = {
                                  C.POINTER(_p)]),
     "ipi_mdp_destroy": (None, [_p]),
     "ipi_mdp_plan": (C.c_int, [_p, C.POINTER(Plan)]),
+    "ipi_mdp_k1_trace": (C.c_int, [_p, _i32, _p, _i32]),
     "ipi_validate": (C.c_int, [_p, C.POINTER(Validation), _p]),
     "ipi_bellman": (C.c_int, [_p, _p, _i32, _p, _p, _p, _p, _p, _p]),
     "ipi_policy_nnz": (C.c_int, [_p, _p, C.POINTER(_i64), _p]),

@@ -42,7 +42,22 @@ struct K1Args {
   double* gpi;
   int32_t* lenpi;
   unsigned long long* res_bits;
+  int32_t win_async;   // uniform ring: stage the V window with cp.async
+  int32_t interleave;  // uniform ring: warps take interleaved states
+  int32_t rotate;      // uniform ring: per-CTA rotated start in the warp's state sequence
+  unsigned long long* trace;  // diagnostics: per-CTA (smid, t_start, t_end) or nullptr
 };
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned sm_id() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+  return r;
+}
 
 template <int G, bool WIN>
 __global__ void __launch_bounds__(kK1Threads) k1_bellman(K1Args a) {
@@ -715,10 +730,19 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_bellman_uring(K1Args a, int win
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double red[32];
   double* win = reinterpret_cast<double*>(smem_raw);
+  if (a.trace && threadIdx.x == 0) {
+    a.trace[3 * blockIdx.x] = sm_id();
+    a.trace[3 * blockIdx.x + 1] = global_ns();
+  }
   const int64_t s_lo = a.bounds[blockIdx.x], s_hi = a.bounds[blockIdx.x + 1];
   int w_lo = 0;
   uint32_t w_len = 0;
-  if (WIN) {
+  // the V window goes out as one cp.async group together with the first ring
+  // stages (a scalar window loop stalled every CTA wave's start)
+  if (WIN && a.win_async)
+    window_issue_async(a.v, a.state0 + s_lo - a.halo, a.state0 + s_hi + a.halo, a.n_global,
+                       smem_raw, w_lo, w_len);
+  if (WIN && !a.win_async) {  // scalar window loop (A/B: IPI_K1_WIN_ASYNC=0)
     int64_t lo = a.state0 + s_lo - a.halo;
     int64_t hi = a.state0 + s_hi + a.halo;
     lo = lo < 0 ? 0 : lo;
@@ -747,16 +771,44 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_bellman_uring(K1Args a, int win
     return __ldg(vg + c);
   };
   const int64_t ns = s_hi - s_lo;
-  const int64_t ws0 = s_lo + ns * warp / NW, ws1 = s_lo + ns * (warp + 1) / NW;
-  const int64_t r_beg = ws0 * m;
-  const int64_t nb = (ws1 - ws0) * m / 4;  // steps (m % 4 == 0)
+  // State order.  Interleaved (default): warp w takes states s_lo + w, + NW, ...
+  // so the CTA's warps stream NW consecutive states (one contiguous region per
+  // CTA).  Contiguous (IPI_K1_INTERLEAVE=0): warp w owns a contiguous state
+  // range; its NW*grid concurrent streams sit at regular strides and, for some
+  // wave counts, collide in the DRAM channel hash (0.70 vs 0.88 of HBM).
+  const bool inter = a.interleave != 0;
+  const int64_t ws0 = inter ? s_lo + warp : s_lo + ns * warp / NW;
+  const int64_t ws1 = inter ? s_hi : s_lo + ns * (warp + 1) / NW;
+  const int64_t s_step = inter ? NW : 1;  // state stride of this warp
+  const int64_t n_states = inter ? (ns > warp ? (ns - warp + NW - 1) / NW : 0) : ws1 - ws0;
+  const int spm = m >> 2;                  // steps per state (m % 4 == 0)
+  const int64_t nb = n_states * spm;
+  // Rotation (interleaved order): this warp starts at state index `rot` of its
+  // sequence and wraps, so the grid's concurrent streams do not advance in
+  // lock-step at fixed strides (IPI_K1_ROTATE=0 disables).
+  const int64_t rot = (inter && a.rotate && n_states > 0)
+                          ? (int64_t)(((uint64_t)blockIdx.x * 2654435761ull) % (uint64_t)n_states) : 0;
+  auto state_of = [&](int64_t k) -> int64_t {  // k-th state this warp processes
+    int64_t kk = k + rot;
+    if (kk >= n_states) kk -= n_states;
+    return ws0 + kk * s_step;
+  };
+  int64_t ik = 0;                          // state index of the next issue
+  int64_t irow = state_of(0) * m;          // next row to issue
+  int ist = 0;                             // steps issued in the current state
 
   // 16-byte chunk cc of row r lives at chunk cc ^ swz(r): rows of a step on disjoint banks
   // values: LDS.64 half-warp = rows {0,1} / {2,3}: flip 64 B for odd rows
   // columns: LDS.32 full warp = rows 0..3: flip 32 B * r
+  // issue() is called once per step, in step order
   auto issue = [&](int64_t i, int stg) {
     if (i < nb) {
-      const int64_t row0 = r_beg + 4 * i;
+      const int64_t row0 = irow;
+      irow += 4;
+      if (++ist == spm) {
+        ist = 0;
+        irow = state_of(++ik) * m;
+      }
       const uint32_t st = ring_s + (uint32_t)(stg * L::kStage);
       const double* vp = a.val + row0 * K;
       const int* cp = a.col + row0 * K;
@@ -791,7 +843,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_bellman_uring(K1Args a, int win
     if (has_last) x[NC] = gather(*reinterpret_cast<const int*>(st + caddr(grp, e_last)));
   };
   int t_in_state = 0;
-  int64_t s_cur = ws0;
+  int64_t kc = 0;  // state index of the step being reduced
+  int64_t s_cur = state_of(0);
   double bq = INFINITY;
   int ba = INT_MAX;
   auto compute = [&](int stg, const double (&x)[NG]) {
@@ -844,7 +897,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_bellman_uring(K1Args a, int win
         res = fmax(res, fabs(sub_rn(gather((int)(a.state0 + s)), ap)));
       }
       t_in_state = 0;
-      ++s_cur;
+      s_cur = state_of(++kc);
       bq = INFINITY;
       ba = INT_MAX;
     }
@@ -860,9 +913,13 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_bellman_uring(K1Args a, int win
     issue(i + S, stg);
     stg = stg + 1 == S ? 0 : stg + 1;
   };
-  if (nb > 0) {
 #pragma unroll 1
-    for (int q = 0; q < S; ++q) issue(q, q);
+  for (int q = 0; q < S; ++q) issue(q, q);
+  if (WIN && a.win_async) {
+    cp_async_wait<S>();  // the window group landed (this thread's copies)
+    __syncthreads();     // ... and every thread's
+  }
+  if (nb > 0) {
     double x0[NG], x1[NG], x2[NG];
 #pragma unroll
     for (int k = 0; k < NG; ++k) x0[k] = x1[k] = x2[k] = 0.0;
@@ -886,6 +943,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_bellman_uring(K1Args a, int win
     }
   }
   cp_async_wait<0>();
+  if (a.trace) {
+    __syncthreads();
+    if (threadIdx.x == 0) a.trace[3 * blockIdx.x + 2] = global_ns();
+  }
   if (a.res_bits) {
     res = warp_max(res);
     if (lane == 0) red[warp] = res;
@@ -914,6 +975,7 @@ static void uring_go(const K1Args& a, bool win, int blocks, int smem, int win_by
 // (K, warps, stages, lookahead) instances
 #define IPI_URING_SHAPES(MACRO)                                                           \
   MACRO(64, 12, 3, 1) MACRO(64, 10, 3, 1) MACRO(64, 11, 3, 1) MACRO(64, 10, 4, 1)        \
+  MACRO(64, 12, 4, 1) MACRO(64, 11, 4, 1) MACRO(64, 11, 4, 2)                            \
   MACRO(64, 8, 4, 1) MACRO(64, 8, 3, 1) MACRO(64, 10, 4, 2) MACRO(64, 8, 4, 2)           \
   MACRO(64, 8, 5, 2) MACRO(64, 12, 4, 2) MACRO(64, 6, 6, 2)
 
@@ -1232,6 +1294,10 @@ int launch_bellman(ipi_mdp* h, const double* v_full, int32_t mode, int32_t* poli
   a.gpi = g_pi;
   a.lenpi = len_pi;
   a.res_bits = res_bits;
+  a.win_async = h->k1_win_async;
+  a.interleave = h->k1_interleave;
+  a.rotate = h->k1_rotate;
+  a.trace = h->k1_trace;
   const bool win = h->plan.halo >= 0;
   const int blocks = h->plan.k1_blocks, smem = h->plan.k1_smem_bytes;
   int G = 0, P = 0;
@@ -1246,6 +1312,13 @@ int launch_bellman(ipi_mdp* h, const double* v_full, int32_t mode, int32_t* poli
     return IPI_OK;
   }
   if (h->plan.k1_variant == 6) {
+    if (a.win_async && h->ring_win_bytes > 0 && (uintptr_t)v_full % 16 != 0) {
+      // the window is staged in 16-byte cp.async chunks: realign V once
+      if (!h->vbuf) IPI_CUDA_TRY(cudaMalloc(&h->vbuf, sizeof(double) * h->n_global));
+      IPI_CUDA_TRY(cudaMemcpyAsync(h->vbuf, v_full, sizeof(double) * h->n_global,
+                                   cudaMemcpyDeviceToDevice, st));
+      a.v = h->vbuf;
+    }
     bool ok = false;
     const int K = h->plan.row_len_max, S = h->plan.k1_stages, NW = h->plan.k1_threads / 32;
     const int D = h->uring_lookahead;

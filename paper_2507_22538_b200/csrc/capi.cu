@@ -266,6 +266,9 @@ int ipi_mdp_create(const int64_t* row_ptr, const int32_t* col, const double* val
     ipi_mdp_destroy(h);
     return code;
   };
+  if (getenv("IPI_K1_WIN_ASYNC")) h->k1_win_async = atoi(getenv("IPI_K1_WIN_ASYNC")) != 0;
+  if (getenv("IPI_K1_INTERLEAVE")) h->k1_interleave = atoi(getenv("IPI_K1_INTERLEAVE")) != 0;
+  if (getenv("IPI_K1_ROTATE")) h->k1_rotate = atoi(getenv("IPI_K1_ROTATE")) != 0;
   if (cudaMallocHost(&h->host_pinned, 4096) != cudaSuccess)
     return bail(fail(IPI_ECUDA, "cudaMallocHost failed"));
   const int64_t rows = n_local * (int64_t)m;
@@ -415,8 +418,9 @@ int ipi_mdp_create(const int64_t* row_ptr, const int32_t* col, const double* val
     const bool aligned = ((uintptr_t)values % 16 == 0) && ((uintptr_t)stage_cost % 16 == 0) &&
                          ((uintptr_t)col % 16 == 0);
     // (warps, stages, waves, lookahead); measured on C2 (scripts/uring_ab.sh,
-    // profiles/r01_uring_shapes.txt): 2 or 4 waves beat 1, 3 or 6
-    int shapes[6][4] = {{12, 3, 4, 1}, {10, 3, 2, 1}, {11, 3, 2, 1}, {10, 4, 2, 1}, {8, 4, 2, 1}, {8, 3, 2, 1}};
+    // profiles/r01_uring_shapes*.txt): 8 waves (small CTAs, even tail) with the
+    // cp.async window are the most stable; 4 waves swing 0.70-0.89 across boxes
+    int shapes[6][4] = {{12, 3, 8, 1}, {12, 3, 4, 1}, {10, 3, 2, 1}, {11, 3, 2, 1}, {10, 4, 2, 1}, {8, 4, 2, 1}};
     int nshape = 6;
     if (getenv("IPI_URING_WARPS") && getenv("IPI_URING_STAGES") && getenv("IPI_URING_WAVES")) {
       shapes[0][0] = atoi(getenv("IPI_URING_WARPS"));
@@ -426,9 +430,8 @@ int ipi_mdp_create(const int64_t* row_ptr, const int32_t* col, const double* val
       nshape = 1;
     }
     const int budget = 227 * 1024 - 256;  // one CTA per SM
-    bool done = false;
-    for (int si = 0; si < nshape && !(env && env[0] == '0') && aligned && !done; ++si) {
-      const int NW = shapes[si][0], S = shapes[si][1], waves = shapes[si][2], D = shapes[si][3];
+    // install one (warps, stages, waves, lookahead) shape into the plan
+    auto install = [&](int NW, int S, int waves, int D) -> bool {
       const int blocks = (int)std::min<int64_t>((int64_t)h->num_sms * waves,
                                                 std::max<int64_t>(1, (n_local + 63) / 64));
       std::vector<int64_t> hb(blocks + 1);
@@ -437,34 +440,81 @@ int ipi_mdp_create(const int64_t* row_ptr, const int32_t* col, const double* val
       int64_t worst = 0;
       for (int c = 0; c < blocks; ++c) worst = std::max<int64_t>(worst, hb[c + 1] - hb[c]);
       int wbytes = 0;
-      if (p.halo >= 0) {
-        const int64_t wlen = std::min<int64_t>(n_global, worst + 2 * (int64_t)p.halo);
+      if (p.halo >= 0) {  // + 2: the cp.async window start is rounded down to an even index
+        const int64_t wlen = std::min<int64_t>(n_global, worst + 2 * (int64_t)p.halo) + 2;
         wbytes = (int)std::min<int64_t>(wlen * 8, INT32_MAX / 2);
-        if (uniform_ring_smem(64, S, NW, wbytes) > budget) continue;  // keep the window
+        if (uniform_ring_smem(64, S, NW, wbytes) > budget) return false;  // keep the window
       }
       const int smem = uniform_ring_smem(64, S, NW, wbytes);
       if (smem > budget || !k1_uring_prepare(64, NW, S, D, wbytes > 0, smem)) {
         cudaGetLastError();
-        continue;
+        return false;
       }
       int64_t* db = nullptr;
-      if (cudaMalloc(&db, sizeof(int64_t) * (blocks + 1)) == cudaSuccess &&
-          cudaMemcpy(db, hb.data(), sizeof(int64_t) * (blocks + 1), cudaMemcpyHostToDevice) ==
+      if (cudaMalloc(&db, sizeof(int64_t) * (blocks + 1)) != cudaSuccess ||
+          cudaMemcpy(db, hb.data(), sizeof(int64_t) * (blocks + 1), cudaMemcpyHostToDevice) !=
               cudaSuccess) {
-        cudaFree(h->k1_bounds);
-        h->k1_bounds = db;
-        h->ring_win_bytes = wbytes;
-        p.k1_blocks = blocks;
-        p.k1_threads = NW * 32;
-        p.k1_smem_bytes = smem;
-        p.k1_stages = S;
-        h->uring_lookahead = D;
-        p.k1_variant = 6;
-        done = true;
-      } else {
         if (db) cudaFree(db);
         cudaGetLastError();
+        return false;
       }
+      cudaFree(h->k1_bounds);
+      h->k1_bounds = db;
+      h->ring_win_bytes = wbytes;
+      p.k1_blocks = blocks;
+      p.k1_threads = NW * 32;
+      p.k1_smem_bytes = smem;
+      p.k1_stages = S;
+      h->uring_lookahead = D;
+      p.k1_variant = 6;
+      return true;
+    };
+    bool done = false;
+    for (int si = 0; si < nshape && !(env && env[0] == '0') && aligned && !done; ++si)
+      done = install(shapes[si][0], shapes[si][1], shapes[si][2], shapes[si][3]);
+    // Autotune the CTA count on the instance itself.  The streaming rate of the
+    // ring depends on the number of CTAs in a way that differs between B200
+    // boards (C2, 12 warps x 3 stages: 4 waves 0.70 on one box and 0.89 on
+    // another, 8 waves the reverse pattern less often; per-CTA rates are
+    // uniform within a launch, so it is not a tail effect —
+    // scripts/k1_trace.py, scripts/k1_offset.py).  For large instances time a
+    // few wave counts (one warm + one timed launch each, ~30 ms once) and keep
+    // the fastest.  IPI_K1_AUTOTUNE=0 keeps the static first choice.
+    const char* at = getenv("IPI_K1_AUTOTUNE");
+    if (done && nshape > 1 && !(at && at[0] == '0') && nnz >= (1ll << 28)) {
+      const int cand[4] = {8, 4, 6, 2};
+      double* tv = nullptr;
+      double* tap = nullptr;
+      int32_t* tpol = nullptr;
+      bool ok = cudaMalloc(&tv, sizeof(double) * n_global) == cudaSuccess &&
+                cudaMalloc(&tap, sizeof(double) * n_local) == cudaSuccess &&
+                cudaMalloc(&tpol, sizeof(int32_t) * n_local) == cudaSuccess &&
+                cudaMemsetAsync(tv, 0, sizeof(double) * n_global, st) == cudaSuccess;
+      cudaEvent_t e0 = nullptr, e1 = nullptr;
+      ok = ok && cudaEventCreate(&e0) == cudaSuccess && cudaEventCreate(&e1) == cudaSuccess;
+      float best_ms = 1e30f;
+      int best_w = -1;
+      for (int ci = 0; ok && ci < 4; ++ci) {
+        if (!install(12, 3, cand[ci], 1)) continue;
+        if (launch_bellman(h, tv, IPI_MODE_MIN, tpol, tap, nullptr, nullptr, nullptr, st)) break;
+        cudaEventRecord(e0, st);
+        if (launch_bellman(h, tv, IPI_MODE_MIN, tpol, tap, nullptr, nullptr, nullptr, st)) break;
+        cudaEventRecord(e1, st);
+        float ms = 0.f;
+        if (cudaEventSynchronize(e1) != cudaSuccess || cudaEventElapsedTime(&ms, e0, e1) != cudaSuccess) break;
+        if (ms < best_ms) {
+          best_ms = ms;
+          best_w = cand[ci];
+        }
+      }
+      cudaGetLastError();
+      if (best_w > 0) install(12, 3, best_w, 1);
+      else install(shapes[0][0], shapes[0][1], shapes[0][2], shapes[0][3]);
+      if (e0) cudaEventDestroy(e0);
+      if (e1) cudaEventDestroy(e1);
+      cudaFree(tv);
+      cudaFree(tap);
+      cudaFree(tpol);
     }
   }
   // ---- flat rows (K <= 4): cp.async ring per warp (bellman.cu) ---------------
@@ -585,8 +635,28 @@ void ipi_mdp_destroy(ipi_mdp* h) {
   cudaFree(h->d_report);
   cudaFree(h->kry);
   cudaFree(h->invd);
+  cudaFree(h->vbuf);
+  cudaFree(h->k1_trace);
   if (h->host_pinned) cudaFreeHost(h->host_pinned);
   delete h;
+}
+
+int ipi_mdp_k1_trace(ipi_mdp* h, int32_t enable, uint64_t* out, int32_t cap) {
+  if (!h) return fail(IPI_EVALIDATION, "null handle");
+  const int64_t words = 3 * (int64_t)h->plan.k1_blocks;
+  if (enable) {
+    if (!h->k1_trace) IPI_CUDA_TRY(cudaMalloc(&h->k1_trace, sizeof(uint64_t) * words));
+    IPI_CUDA_TRY(cudaMemset(h->k1_trace, 0, sizeof(uint64_t) * words));
+    return IPI_OK;
+  }
+  if (h->k1_trace && out && cap > 0) {
+    IPI_CUDA_TRY(cudaDeviceSynchronize());
+    IPI_CUDA_TRY(cudaMemcpy(out, h->k1_trace, sizeof(uint64_t) * std::min<int64_t>(words, cap),
+                            cudaMemcpyDeviceToHost));
+  }
+  cudaFree(h->k1_trace);
+  h->k1_trace = nullptr;
+  return IPI_OK;
 }
 
 int ipi_mdp_plan(const ipi_mdp* h, ipi_plan* out) {
@@ -824,8 +894,7 @@ int ipi_op_create(const int64_t* rp, const int32_t* col, const double* val, int6
     nshape = 1;
   }
   const int align = variant == IPI_K3_FLAT ? 32 : 4;
-  for (int si = 0; si < nshape && allow && aligned && pl.uniform_rows; ++si) {
-    const int NW = shapes[si][0], S = shapes[si][1], waves = shapes[si][2];
+  auto install = [&](int NW, int S, int waves) -> bool {
     const int64_t per_warp_min = variant == IPI_K3_FLAT ? 64 : 16;
     const int blocks = (int)std::min<int64_t>((int64_t)sms * waves,
                                               std::max<int64_t>(1, n_local / (NW * per_warp_min)));
@@ -840,7 +909,7 @@ int ipi_op_create(const int64_t* rp, const int32_t* col, const double* val, int6
       wbytes = 0;
       smem = variant == IPI_K3_FLAT ? k3_flat_smem(K, S, NW, 0) : k3_uring_smem(K, S, NW, 0);
     }
-    if (smem > budget || !k3_shape_prepare(variant, K, NW, S, wbytes > 0, smem)) continue;
+    if (smem > budget || !k3_shape_prepare(variant, K, NW, S, wbytes > 0, smem)) return false;
     op->variant = variant;
     op->blocks = blocks;
     op->warps = NW;
@@ -849,7 +918,54 @@ int ipi_op_create(const int64_t* rp, const int32_t* col, const double* val, int6
     op->win_bytes = wbytes;
     op->halo = wbytes > 0 ? pl.halo : -1;
     op->pf = getenv("IPI_K3_PF") ? atoi(getenv("IPI_K3_PF")) : 0;
-    break;
+    return true;
+  };
+  bool done = false;
+  for (int si = 0; si < nshape && allow && aligned && pl.uniform_rows && !done; ++si)
+    done = install(shapes[si][0], shapes[si][1], shapes[si][2]);
+  // Autotune the shape on the operator itself for large P_pi (same board
+  // sensitivity as K1, see ipi_mdp_create): one warm + one timed apply per
+  // candidate (~2 ms once per operator).  IPI_K3_AUTOTUNE=0 disables.
+  const char* at = getenv("IPI_K3_AUTOTUNE");
+  if (done && nshape > 1 && !(at && at[0] == '0') && op->nnz >= (1ll << 25)) {
+    const int cu[4][3] = {{11, 3, 1}, {12, 3, 3}, {12, 3, 6}, {12, 3, 4}};
+    const int cf[3][3] = {{24, 4, 1}, {28, 4, 1}, {16, 4, 1}};
+    const int nc = variant == IPI_K3_FLAT ? 3 : 4;
+    double* tx = nullptr;
+    double* ty = nullptr;
+    cudaStream_t st = (cudaStream_t)stream;
+    bool ok = cudaMalloc(&tx, sizeof(double) * n_global) == cudaSuccess &&
+              cudaMalloc(&ty, sizeof(double) * n_local) == cudaSuccess &&
+              cudaMemsetAsync(tx, 0, sizeof(double) * n_global, st) == cudaSuccess;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    ok = ok && cudaEventCreate(&e0) == cudaSuccess && cudaEventCreate(&e1) == cudaSuccess;
+    float best_ms = 1e30f;
+    int best = -1;
+    for (int ci = 0; ok && ci < nc; ++ci) {
+      const int* c = variant == IPI_K3_FLAT ? cf[ci] : cu[ci];
+      if (!install(c[0], c[1], c[2])) continue;
+      if (op_launch(op, tx, nullptr, 1, ty, st)) break;
+      cudaEventRecord(e0, st);
+      if (op_launch(op, tx, nullptr, 1, ty, st)) break;
+      cudaEventRecord(e1, st);
+      float ms = 0.f;
+      if (cudaEventSynchronize(e1) != cudaSuccess || cudaEventElapsedTime(&ms, e0, e1) != cudaSuccess) break;
+      if (ms < best_ms) {
+        best_ms = ms;
+        best = ci;
+      }
+    }
+    cudaGetLastError();
+    if (best >= 0) {
+      const int* c = variant == IPI_K3_FLAT ? cf[best] : cu[best];
+      install(c[0], c[1], c[2]);
+    } else {
+      install(shapes[0][0], shapes[0][1], shapes[0][2]);
+    }
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    cudaFree(tx);
+    cudaFree(ty);
   }
   *out = op;
   return IPI_OK;

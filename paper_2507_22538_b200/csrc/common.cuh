@@ -127,6 +127,27 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// Stage the window x[lo, hi) (clipped to [0, n)) into shared memory as ONE
+// cp.async commit group: 16-byte chunks, every thread's copies in flight at
+// once, the start rounded down to an even index so chunks are aligned (the
+// buffer needs 2 doubles of slack).  The caller waits for the group and
+// barriers before the first read; x must be 16-byte aligned.
+__device__ __forceinline__ void window_issue_async(const double* x, int64_t lo, int64_t hi, int64_t n,
+                                                   unsigned char* win, int& w_lo, uint32_t& w_len) {
+  lo = lo < 0 ? 0 : lo;
+  hi = hi > n ? n : hi;
+  lo &= ~(int64_t)1;
+  w_lo = (int)lo;
+  w_len = hi > lo ? (uint32_t)(hi - lo) : 0u;
+  uint64_t keep;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
+  const uint32_t win_s = (uint32_t)__cvta_generic_to_shared(win);
+  const uint32_t nch = (w_len + 1) >> 1;
+  for (uint32_t c = threadIdx.x; c < nch; c += blockDim.x)
+    cp_async16(win_s + 16 * c, x + lo + 2 * c, 2 * c + 1 < w_len ? 16u : 8u, keep);
+  cp_async_commit();
+}
+
 // Bulk L2 prefetch of a contiguous byte range (16-byte aligned, multiple of 16).
 __device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");

@@ -46,6 +46,11 @@ struct ipi_mdp {
   // K1 flat-row cp.async ring (variant 4): window bytes in front of the rings
   int ring_win_bytes = 0;
   int uring_lookahead = 1;  // variant 6: V gathers issued this many steps ahead
+  double* vbuf = nullptr;   // 16-byte-aligned copy of a misaligned V (cp.async window)
+  int k1_win_async = 1;     // variant 6: cp.async V window (IPI_K1_WIN_ASYNC=0: scalar loop)
+  int k1_interleave = 1;    // variant 6: interleaved state order (IPI_K1_INTERLEAVE=0: contiguous)
+  int k1_rotate = 1;        // variant 6: rotated per-CTA start (IPI_K1_ROTATE=0: none)
+  unsigned long long* k1_trace = nullptr;  // diagnostics (ipi_mdp_k1_trace)
 };
 
 // A planned policy operator (K3): borrowed P_pi rows + the kernel shape.

@@ -161,6 +161,10 @@ UVARIANTS = {
                      "IPI_URING_WAVES": "2", "IPI_URING_AHEAD": "2"},
     "uring12x4w4d2": {"IPI_K1_URING": "1", "IPI_URING_WARPS": "12", "IPI_URING_STAGES": "4",
                       "IPI_URING_WAVES": "4", "IPI_URING_AHEAD": "2"},
+    "uring12x4w8": {"IPI_K1_URING": "1", "IPI_URING_WARPS": "12", "IPI_URING_STAGES": "4",
+                    "IPI_URING_WAVES": "8"},
+    "uring11x4w8d2": {"IPI_K1_URING": "1", "IPI_URING_WARPS": "11", "IPI_URING_STAGES": "4",
+                      "IPI_URING_WAVES": "8", "IPI_URING_AHEAD": "2"},
     "registers": {"IPI_K1_URING": "0"},
 }
 
@@ -199,3 +203,22 @@ def test_uniform_rows_k64(monkeypatch, variant, m, n, band, maximize):
     pi_d, ap_d, rb = greedy_device(mdp, vd, mode, with_residual=True)
     want = float(np.max(np.abs(v - ap_d.cpu().numpy())))
     assert float(rb.view(torch.float64)[0]) == want
+
+
+def test_uring_misaligned_v_is_realigned():
+    """The ring's V window is staged in 16-byte cp.async chunks: a V view at an
+    odd offset goes through an aligned copy and gives the same backup."""
+    n, m, K = 6000, 32, 64
+    rp, col, val, cost = wide_instance(n, m, K, seed=5, band=400)
+    mdp = ipi.MdpInstance(n=n, m=m, gamma=0.999, stage_cost=cost,
+                          transitions=ipi.CsrMatrix(n * m, n, rp, col, val))
+    plan = mdp.plan()
+    assert plan["k1_variant"] == 6 and plan["halo"] >= 0, plan
+    v = np.random.default_rng(3).random(n)
+    buf = torch.zeros(n + 1, dtype=torch.float64, device="cuda")
+    buf[1:] = torch.as_tensor(v, device="cuda")
+    pi_a, ap_a, _ = greedy_device(mdp, buf[1:], ipi.Mode.MIN)
+    pi_b, ap_b, _ = greedy_device(mdp, torch.as_tensor(v, device="cuda"), ipi.Mode.MIN)
+    assert torch.equal(pi_a, pi_b) and torch.equal(ap_a, ap_b)
+    pi_ref, ap_ref = orc.greedy(rp, col, val, cost, 0.999, v)
+    np.testing.assert_array_equal(ap_a.cpu().numpy(), ap_ref)
