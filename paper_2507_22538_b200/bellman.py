@@ -7,6 +7,7 @@ argmin/argmax + the residual max, never materialising the n*m product.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -17,6 +18,10 @@ from .model import MdpInstance, Mode, ValidationError
 from .sparse import gather_policy_cost, gather_policy_matrix, norm, spmv
 
 __all__ = ["GreedyResult", "greedy_policy", "bellman_residual", "policy_residual"]
+
+# pinned-host-tensor path: K1 writes its outputs into the mapped host buffers
+# (IPI_ZERO_COPY=0: device outputs + D2H copies after the kernel)
+_ZERO_COPY = os.environ.get("IPI_ZERO_COPY", "1") != "0"
 
 
 @dataclass(frozen=True)
@@ -65,21 +70,30 @@ def greedy_policy(mdp: MdpInstance, v, mode: Mode | None = None, workers=None) -
 
     Output placement follows the input: numpy in -> numpy out (int64 policy,
     like bellman.py:54); CUDA tensor in -> CUDA tensors out; CPU tensor in
-    (e.g. pinned host memory) -> one H2D copy of V, one K1 launch, and D2H
-    copies of the results into pinned host tensors."""
+    (e.g. pinned host memory) -> one H2D copy of V and one K1 launch whose
+    policy / TV stores go straight to pinned host tensors (zero-copy)."""
     host_torch = isinstance(v, torch.Tensor) and v.device.type == "cpu"
     if host_torch:
         if tuple(v.shape) != (mdp.n,):
             raise ValidationError(f"cost vector length {tuple(v.shape)} does not match n = {mdp.n}")
         vt = v.to(mdp.stage_cost.device, torch.float64, non_blocking=True)
-        if not bool(torch.isfinite(vt).all()):
-            raise ValidationError("cost vector has non-finite entries")
-        pi, applied, _ = greedy_device(mdp, vt, mode or mdp.mode)
+        finite = torch.isfinite(vt).all()  # read after the one sync below
         pol_h = torch.empty(mdp.n, dtype=torch.int32, pin_memory=True)
         app_h = torch.empty(mdp.n, dtype=torch.float64, pin_memory=True)
-        pol_h.copy_(pi, non_blocking=True)
-        app_h.copy_(applied, non_blocking=True)
+        if _ZERO_COPY:
+            # K1 stores the policy / TV straight into the pinned (UVA-mapped)
+            # host buffers while it streams: the D2H transfer overlaps the kernel
+            md = _lib.MODE_MAX if (mode or mdp.mode) is Mode.MAX else _lib.MODE_MIN
+            _lib.check(_lib.lib().ipi_bellman(mdp.handle(), _lib.ptr(vt), md, pol_h.data_ptr(),
+                                              app_h.data_ptr(), None, None, None,
+                                              _lib.stream_ptr()), "ipi_bellman")
+        else:
+            pi, applied, _ = greedy_device(mdp, vt, mode or mdp.mode)
+            pol_h.copy_(pi, non_blocking=True)
+            app_h.copy_(applied, non_blocking=True)
         torch.cuda.current_stream().synchronize()
+        if not bool(finite):
+            raise ValidationError("cost vector has non-finite entries")
         return GreedyResult(policy=pol_h, applied=app_h)
     vt, was_np = _check_cost_vector(mdp, v)
     mode = mode or mdp.mode
