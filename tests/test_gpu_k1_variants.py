@@ -222,3 +222,44 @@ def test_uring_misaligned_v_is_realigned():
     assert torch.equal(pi_a, pi_b) and torch.equal(ap_a, ap_b)
     pi_ref, ap_ref = orc.greedy(rp, col, val, cost, 0.999, v)
     np.testing.assert_array_equal(ap_a.cpu().numpy(), ap_ref)
+
+
+def ragged_instance(n, m, seed, lo=0, hi=120):
+    """Variable row lengths in [lo, hi) (empty rows included when lo == 0),
+    sorted distinct columns, Dirichlet weights."""
+    rng = np.random.default_rng(seed)
+    lens = np.minimum(rng.integers(lo, hi, size=n * m), n)
+    rp = np.concatenate(([0], np.cumsum(lens))).astype(np.int64)
+    cols, vals = [], []
+    for L in lens:
+        c = np.sort(rng.choice(n, size=min(L, n), replace=False))
+        e = rng.standard_exponential(len(c))
+        cols.append(c)
+        vals.append(e / e.sum() if len(c) else e)
+    cost = rng.random((n, m))
+    return rp, np.concatenate(cols).astype(np.int64), np.concatenate(vals), cost
+
+
+@pytest.mark.parametrize("m,n,lo,hi", [(5, 3000, 0, 120), (8, 700, 1, 900), (1, 4000, 16, 64),
+                                       (3, 257, 0, 40)])
+@pytest.mark.parametrize("maximize", [False, True])
+def test_variable_rows_generic(m, n, lo, hi, maximize):
+    """Generic per-row kernel on ragged rows (empty rows included) vs the oracle."""
+    rp, col, val, cost = ragged_instance(n, m, seed=m * 100 + n, lo=lo, hi=hi)
+    gamma = 0.99
+    mode = ipi.Mode.MAX if maximize else ipi.Mode.MIN
+    mdp = ipi.MdpInstance(n=n, m=m, gamma=gamma, stage_cost=cost,
+                          transitions=ipi.CsrMatrix(n * m, n, rp, col, val), mode=mode)
+    assert mdp.plan()["k1_variant"] == 0
+    v = np.random.default_rng(2).random(n) * 50
+    res = ipi.greedy_policy(mdp, v)
+    pi_ref, ap_ref = orc.greedy(rp, col, val, cost, gamma, v, maximize)
+    gap = orc.q_gap(rp, col, val, cost, gamma, v, maximize)
+    bad = np.flatnonzero(res.policy != pi_ref)
+    assert np.all(gap[bad] < 1e-10)
+    np.testing.assert_allclose(res.applied, ap_ref, rtol=1e-13, atol=1e-13)
+    vd = torch.as_tensor(v, device="cuda")
+    pi_d, ap_d, rb = greedy_device(mdp, vd, mode, with_residual=True)
+    assert float(rb.view(torch.float64)[0]) == float(np.max(np.abs(v - ap_d.cpu().numpy())))
+    pi2, ap2, _ = greedy_device(mdp, vd, mode)  # reruns are bit-identical
+    assert torch.equal(pi_d, pi2) and torch.equal(ap_d, ap2)
