@@ -302,3 +302,60 @@ def test_k1_on_row_shards_equals_full_instance():
         assert torch.equal(app, tv_f[lo:hi])
         r_loc = float(bits.view(torch.float64)[0])
         assert r_loc == float((v[lo:hi] - tv_f[lo:hi]).abs().max())
+
+
+# ----------------------------------------------------------------------------
+# full C4 / C3 size against the C/OpenMP oracle
+# ----------------------------------------------------------------------------
+
+@pytest.mark.slow
+def test_c4_full_size_oracle_parity():
+    """BASELINE C4 (N = 20 000, ~5.7e7 nnz, variable rows): the whole iPI solve
+    against the C restatement of the reference (status, outer count, V, policy
+    outside Q-ties, residual certificate)."""
+    import os
+    from oracle import c_oracle as co
+    mdp, spec = devgen.build_instance(4)
+    rp, col, val = mdp.transitions.numpy()
+    cost = mdp.stage_cost.cpu().numpy()
+    nt = os.cpu_count()
+    res_gpu = ipi.solve(mdp, ipi.SolveOptions(alpha=spec.alpha, tol=spec.atol))
+    ref = co.solve(rp, col, val, cost, spec.gamma, tol=spec.atol, alpha=spec.alpha, nthreads=nt)
+    assert res_gpu.status.value == ref.status == "converged"
+    assert abs(res_gpu.outer_iterations - ref.outer_iterations) <= 1
+    scale = max(1.0, np.abs(ref.values).max())
+    np.testing.assert_allclose(res_gpu.values, ref.values, rtol=1e-8, atol=1e-8 * scale)
+    diff = np.flatnonzero(res_gpu.policy != ref.policy)
+    if diff.size:
+        pv = co.spmv(rp, col, val, ref.values, nthreads=nt).reshape(mdp.n, mdp.m)
+        q = np.sort(cost[diff] + spec.gamma * pv[diff], axis=1)
+        assert np.all(q[:, 1] - q[:, 0] < TIE_GAP)
+    _, _, r = co.greedy(rp, col, val, cost, spec.gamma, res_gpu.values, nthreads=nt)
+    assert r <= spec.atol
+
+
+@pytest.mark.slow
+def test_c3_full_size_backup_and_evaluation():
+    """BASELINE C3 (2048^2 states, 21 actions, 4 nnz per row) at full size: the
+    Bellman backup is bitwise the C oracle's (flat ring restates numpy's order),
+    and one policy evaluation (Richardson, fixed 50 sweeps) agrees to 1e-12."""
+    import os
+    from oracle import c_oracle as co
+    mdp, spec = devgen.build_instance(3)
+    rp, col, val = mdp.transitions.numpy()
+    cost = mdp.stage_cost.cpu().numpy()
+    nt = os.cpu_count()
+    v = np.random.default_rng(9).random(mdp.n) * 100
+    g = ipi.greedy_policy(mdp, v)
+    pi, applied, _ = co.greedy(rp, col, val, cost, spec.gamma, v, nthreads=nt)
+    assert np.array_equal(g.applied, applied)
+    assert np.array_equal(g.policy, pi)
+    p_pi = ipi.gather_policy_matrix(mdp, pi)
+    rpp, cp, vp = p_pi.numpy()
+    gp = cost[np.arange(mdp.n), pi]
+    theta, rep = ipi.inner_solve(ipi.PolicyOperator(p_pi, spec.gamma), gp, v, 0.0, 50,
+                                 kind=ipi.InnerSolver.RICHARDSON)
+    ref_t, ref_rep = co.inner_solve(rpp, cp, vp, spec.gamma, gp, v, 0.0, 50, kind="richardson",
+                                    nthreads=nt)
+    assert rep.iterations == ref_rep.iterations == 50
+    np.testing.assert_allclose(theta, ref_t, rtol=1e-12, atol=1e-12 * np.abs(ref_t).max())
