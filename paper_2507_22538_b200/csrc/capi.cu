@@ -378,8 +378,12 @@ int ipi_mdp_create(const int64_t* row_ptr, const int32_t* col, const double* val
   p.k1_variant = (p.uniform_rows && uniform_shape(p.row_len_max, &Gu, &Pu)) ? 1 : 0;
   // ---- deep-pipeline uniform kernel: one 512-thread CTA per SM ---------------
   {
+    // Default for uniform rows without a shared V window (C5: the +-65536 window
+    // does not fit): every gather is an L2 access, and the register-deep kernel
+    // beats the cp.async ring there (C5 rank proxy: 8.3 vs 11.3 ms,
+    // scripts/c5_ab.sh).  IPI_K1_DEEP=1/0 forces it on/off.
     const char* env = getenv("IPI_K1_DEEP");
-    const bool allow = env && env[0] == '1';
+    const bool allow = env ? env[0] == '1' : p.halo < 0;
     if (allow && p.k1_variant == 1 && p.row_len_max > 4 && n_local > 0) {
       const int blocks = (int)std::min<int64_t>(h->num_sms, std::max<int64_t>(1, (n_local + 15) / 16));
       std::vector<int64_t> hb(blocks + 1);
@@ -413,7 +417,8 @@ int ipi_mdp_create(const int64_t* row_ptr, const int32_t* col, const double* val
   // ---- uniform rows, K = 64: cp.async ring per warp (bellman.cu) -------------
   // Shapes (warps, stages, waves): waves > 1 splits each SM's state range over
   // several CTAs so the V window per CTA shrinks and leaves room for the rings.
-  if (p.k1_variant == 1 && p.uniform_rows && p.row_len_max == 64 && m % 4 == 0 && n_local > 0) {
+  if ((p.k1_variant == 1 || (p.k1_variant == 3 && getenv("IPI_URING_WARPS"))) && p.uniform_rows &&
+      p.row_len_max == 64 && m % 4 == 0 && n_local > 0) {
     const char* env = getenv("IPI_K1_URING");
     const bool aligned = ((uintptr_t)values % 16 == 0) && ((uintptr_t)stage_cost % 16 == 0) &&
                          ((uintptr_t)col % 16 == 0);

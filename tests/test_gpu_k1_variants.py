@@ -165,7 +165,8 @@ UVARIANTS = {
                     "IPI_URING_WAVES": "8"},
     "uring11x4w8d2": {"IPI_K1_URING": "1", "IPI_URING_WARPS": "11", "IPI_URING_STAGES": "4",
                       "IPI_URING_WAVES": "8", "IPI_URING_AHEAD": "2"},
-    "registers": {"IPI_K1_URING": "0"},
+    "registers": {"IPI_K1_URING": "0", "IPI_K1_DEEP": "0"},
+    "deep": {"IPI_K1_URING": "0", "IPI_K1_DEEP": "1"},
 }
 
 
@@ -187,7 +188,7 @@ def test_uniform_rows_k64(monkeypatch, variant, m, n, band, maximize):
     if ring and plan["k1_variant"] != 6:  # forced shape + resident V window exceed smem
         assert plan["halo"] >= 0, plan
         ring = False
-    assert plan["k1_variant"] == (6 if ring else 1), plan
+    assert plan["k1_variant"] == (6 if ring else (3 if variant == "deep" else 1)), plan
     v = np.random.default_rng(11).random(n) * 100
     res = ipi.greedy_policy(mdp, v)
     pi_ref, ap_ref = orc.greedy(rp, col, val, cost, gamma, v, maximize)
@@ -263,3 +264,22 @@ def test_variable_rows_generic(m, n, lo, hi, maximize):
     assert float(rb.view(torch.float64)[0]) == float(np.max(np.abs(v - ap_d.cpu().numpy())))
     pi2, ap2, _ = greedy_device(mdp, vd, mode)  # reruns are bit-identical
     assert torch.equal(pi_d, pi2) and torch.equal(ap_d, ap2)
+
+
+def test_no_window_uniform_rows_pick_deep_kernel():
+    """Uniform K = 64 rows whose columns span more than a window can hold (C5's
+    +-65536 locality) plan the register-deep kernel (all gathers are L2)."""
+    from paper_2507_22538_b200 import devgen
+    from paper_2507_22538_b200.generators import CONFIGS
+    spec = CONFIGS[5]
+    n = 1 << 20  # C5's generator and window on a 1M-state slice
+    rp, col, val, cost = devgen.locality(n, 8, spec.K, spec.window, 0, 0, 20000)
+    from paper_2507_22538_b200.parallel import MdpShard
+    sh = MdpShard(n, 8, spec.gamma, 0, cost, ipi.CsrMatrix(20000 * 8, n, rp, col, val))
+    plan = sh.plan()
+    assert plan["halo"] < 0 and plan["k1_variant"] == 3, plan
+    v = torch.rand(n, dtype=torch.float64, device="cuda")
+    pol, app, _ = sh.bellman(v)
+    rph, colh, valh = (t.cpu().numpy() for t in (rp, col, val))
+    pi_ref, ap_ref = orc.greedy(rph, colh, valh, cost.cpu().numpy(), spec.gamma, v.cpu().numpy())
+    np.testing.assert_allclose(app.cpu().numpy(), ap_ref, rtol=1e-13, atol=1e-13)
