@@ -1039,7 +1039,8 @@ int ipi_inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* v
   IPI_CUDA_TRY(cudaMalloc(&d_rep, sizeof(ipi_inner_report)));
   rc = inner_solve(rp_pi, col_pi, val_pi, n, gamma, b, x, target_2norm, max_it, kind,
                    richardson_scale, pl.lanes_per_row, pl.halo,
-                   pl.uniform_rows ? pl.row_len_max : 0, d_rep, st, nullptr, 0, inv_diag);
+                   pl.uniform_rows ? pl.row_len_max : 0, d_rep, st, nullptr, 0, inv_diag,
+                   12.0 * (double)nnz + 8.0 * (double)(n + 1));
   if (rc == IPI_OK && report) {
     cudaError_t e = cudaMemcpyAsync(report, d_rep, sizeof(*report), cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
@@ -1149,7 +1150,8 @@ int ipi_solve(ipi_mdp* h, const ipi_opts* o, double* v, int32_t* policy, double*
     rc = inner_solve(h->rp_pi, h->col_pi, h->val_pi, n, h->gamma, h->gpi, vnext, target, cap,
                      o->ksp_type, o->richardson_scale, h->plan.lanes_per_row, h->plan.halo,
                      h->plan.uniform_rows ? h->plan.row_len_max : 0, h->d_report, st, h->kry,
-                     h->kry_len, o->pc_type == IPI_PC_JACOBI ? h->invd : nullptr);
+                     h->kry_len, o->pc_type == IPI_PC_JACOBI ? h->invd : nullptr,
+                     (12.0 * h->plan.row_len_mean + 8.0) * (double)n);  // P_pi size estimate
     if (rc) return rc;
     if (o->ksp_type == IPI_KSP_TFQMR || o->ksp_type == IPI_KSP_BICGSTAB) {
       // these kinds can break down: read the report now (driver.py:189-193)

@@ -144,7 +144,8 @@ int inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_p
                 double gamma, const double* b, double* x, double target, int32_t max_it,
                 int32_t kind, double scale, int lanes, int halo, int uniform_K,
                 ipi_inner_report* d_report, cudaStream_t st, double* workspace = nullptr,
-                int64_t workspace_doubles = 0, const double* inv_diag = nullptr);
+                int64_t workspace_doubles = 0, const double* inv_diag = nullptr,
+                double pi_bytes = 0.0);  // bytes of P_pi (L2-residency choice; <= 0: read nnz)
 // Jacobi: inv_diag[s] = 1 / (1 - gamma * P_pi[s, s])  (inner.py:115-118)
 int jacobi_inv_diag(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi, int64_t n,
                     double gamma, double* inv_diag, cudaStream_t st);

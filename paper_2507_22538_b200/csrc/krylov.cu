@@ -58,7 +58,7 @@ int inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_p
                 double gamma, const double* b, double* x, double target, int32_t max_it,
                 int32_t kind, double scale, int lanes, int halo, int uniform_K,
                 ipi_inner_report* d_report, cudaStream_t st, double* workspace,
-                int64_t workspace_doubles, const double* inv_diag) {
+                int64_t workspace_doubles, const double* inv_diag, double pi_bytes) {
   if (kind < IPI_KSP_RICHARDSON || kind > IPI_KSP_TFQMR)
     return fail(IPI_EVALIDATION, "unknown inner solver kind " + std::to_string(kind));
   if (max_it < 1) return fail(IPI_EVALIDATION, "iteration cap must be >= 1, got " + std::to_string(max_it));
@@ -90,6 +90,23 @@ int inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_p
   a.bar = reinterpret_cast<unsigned*>(a.partials + 4 * (int64_t)blocks);
   IPI_CUDA_TRY(cudaMemsetAsync(a.bar, 0, 64, st));
   a.bar_mode = getenv("IPI_K4_BARRIER") ? atoi(getenv("IPI_K4_BARRIER")) : 0;
+  {  // L2 residency of P_pi across the solve's SpMVs (IPI_K4_KEEP overrides the fraction)
+    int l2 = 0;
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+    double bytes = pi_bytes;
+    if (bytes <= 0.0) {  // unknown: read nnz (one sync)
+      int64_t nnz_h = 0;
+      cudaMemcpyAsync(&nnz_h, rp_pi + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      bytes = 12.0 * (double)nnz_h + 8.0 * (double)(n + 1);
+    }
+    const double budget = 0.6 * (double)l2;
+    // whole P_pi when it fits; a fractional hint helped C4's SpMV (-9%) but not its
+    // MGS-bound GMRES step and slowed C3's (IPI_K4_KEEP=<fraction> to experiment)
+    double f = bytes <= budget ? 1.0 : 0.0;
+    if (getenv("IPI_K4_KEEP")) f = atof(getenv("IPI_K4_KEEP"));
+    a.keep_frac = (float)std::min(1.0, std::max(0.0, f));
+  }
   a.target = target;
   a.max_it = max_it;
   a.kind = kind;

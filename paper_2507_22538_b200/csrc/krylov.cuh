@@ -57,6 +57,7 @@ struct KArgs {
   ipi_inner_report* rep;
   unsigned* bar;       // grid barrier counter, zeroed before every launch
   int bar_mode;        // GridBarrier::mode (IPI_K4_BARRIER)
+  float keep_frac;     // fraction of P_pi accesses marked L2 evict-last (0 = evict-first)
 };
 
 // Grid barrier for the co-resident (cooperatively launched) CTAs: one release
@@ -249,8 +250,16 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
   GridBarrier gb{a.bar, 0u, a.bar_mode};
   extern __shared__ double win[];
   __shared__ KShared sh;
-  const uint64_t pol = policy_evict_first();
-  const uint64_t pol_first = pol, pol_last = policy_evict_last();
+  // P_pi is re-read by every SpMV of the solve: when it is not much larger than
+  // L2, mark that fraction of its lines evict-last so repeated SpMVs hit L2
+  // (C4: 137 MB P_pi vs 126 MB L2); large P_pi streams evict-first.
+  uint64_t pol;
+  if (a.keep_frac > 0.f)
+    asm volatile("createpolicy.fractional.L2::evict_last.L2::evict_first.b64 %0, %1;"
+                 : "=l"(pol) : "f"(a.keep_frac));
+  else
+    pol = policy_evict_first();
+  const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int nblk = gridDim.x;
   const int64_t n = a.n;
