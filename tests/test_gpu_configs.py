@@ -359,3 +359,36 @@ def test_c3_full_size_backup_and_evaluation():
                                     nthreads=nt)
     assert rep.iterations == ref_rep.iterations == 50
     np.testing.assert_allclose(theta, ref_t, rtol=1e-12, atol=1e-12 * np.abs(ref_t).max())
+
+
+@pytest.mark.slow
+def test_c5_rank_block_backup_vs_c_oracle():
+    """BASELINE C5 (16.7M states, sharded-only): rank 0's row block at R = 8
+    (2,097,152 states x 16 actions x 64 nnz = 2^31 nnz, full-length V) — the
+    per-rank Bellman backup against the C restatement of greedy_policy on the
+    same block (state0 = 0)."""
+    import os
+    from oracle import c_oracle as co
+    from paper_2507_22538_b200.model import make_partition
+    from paper_2507_22538_b200.parallel import MdpShard
+    spec = gen.CONFIGS[5]
+    lo, hi = make_partition(spec.n, 8).block(0)
+    rp, col, val, cost = devgen.locality(spec.n, spec.m, spec.K, spec.window, 0, lo, hi - lo)
+    sh = MdpShard(spec.n, spec.m, spec.gamma, lo, cost,
+                  ipi.CsrMatrix((hi - lo) * spec.m, spec.n, rp, col, val))
+    v = torch.rand(spec.n, dtype=torch.float64, device="cuda") * 10
+    pol, app, bits = sh.bellman(v)
+    pol, app = pol.cpu().numpy(), app.cpu().numpy()
+    vh = v.cpu().numpy()
+    rph, colh, valh, costh = (t.cpu().numpy() for t in (rp, col, val, cost))
+    del rp, col, val
+    torch.cuda.empty_cache()
+    nt = os.cpu_count()
+    pi, applied, res = co.greedy(rph, colh, valh, costh, spec.gamma, vh, state0=lo, nthreads=nt)
+    np.testing.assert_allclose(app, applied, rtol=1e-13, atol=1e-13)
+    diff = np.flatnonzero(pol != pi)
+    if diff.size:
+        pv = co.spmv(rph, colh, valh, vh, nthreads=nt).reshape(hi - lo, spec.m)
+        q = np.sort(costh[diff] + spec.gamma * pv[diff], axis=1)
+        assert np.all(q[:, 1] - q[:, 0] < TIE_GAP)
+    assert abs(float(bits.view(torch.float64)[0]) - res) <= 1e-13 * max(1.0, res)
