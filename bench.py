@@ -139,7 +139,7 @@ def inner_spmv_roofline(shard, ctx, pol, v_full, n, torch, reps=20):
     at C2, 6x L2: no flush needed)."""
     from paper_2507_22538_b200.parallel import ShardOps
     ops = ShardOps(shard, ctx)
-    op, _ = ops.gather_policy(pol)
+    op, _ = ops.gather_policy(pol, split=False)  # the K3 kernel alone over the gathered x
     y = torch.empty(shard.n_local, dtype=torch.float64, device=v_full.device)
     for _ in range(3):
         op.apply(v_full, out=y)

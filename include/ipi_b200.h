@@ -227,6 +227,18 @@ int ipi_op_get_plan(const ipi_op* op, ipi_op_plan* out);
 int ipi_op_apply(const ipi_op* op, const double* x_full, const double* b, double* y, void* stream);
 /* spmv (sparse.py:189-215): y = P x_full. */
 int ipi_op_spmv(const ipi_op* op, const double* x_full, double* y, void* stream);
+/* Remote half of a split apply (parallel.py, all-gather overlap): y = x_full[state0+r]
+ * - gamma*(y_partial[r] + (P x_full)[r]) (b == NULL) or b[r] - that, where
+ * y_partial is the local-column half P_loc x_local computed while V was gathered. */
+int ipi_op_apply_partial(const ipi_op* op, const double* x_full, const double* y_partial,
+                         const double* b, double* y, void* stream);
+/* Split a row block's CSR into columns in [lo, hi) (stored as col - lo) and the
+ * rest, each keeping the row's column order.  Pass 1 (col_loc == NULL): per-row
+ * counts into rp_loc[r+1] / rp_rem[r+1] (caller sets [0] = 0 and scans);
+ * pass 2: scatter.  Used per outer iteration on the rank's P_pi rows. */
+int ipi_csr_split_local(const int64_t* rp, const int32_t* col, const double* val, int64_t rows,
+                        int64_t lo, int64_t hi, int64_t* rp_loc, int32_t* col_loc, double* val_loc,
+                        int64_t* rp_rem, int32_t* col_rem, double* val_rem, void* stream);
 
 /* ---- row-sharded inner solve: device-resident MGS (parallel.py) ------- */
 /* out[0] = <a, b> over n entries (this rank's partial; sparse.py:218-226).

@@ -1013,6 +1013,24 @@ int ipi_op_spmv(const ipi_op* op, const double* x_full, double* y, void* stream)
   return op_run(op, x_full, nullptr, 0, y, stream);
 }
 
+int ipi_op_apply_partial(const ipi_op* op, const double* x_full, const double* y_partial,
+                         const double* b, double* y, void* stream) {
+  if (!op) return fail(IPI_EVALIDATION, "null operator");
+  if (op->n_local > 0 && (!x_full || !y || !y_partial)) return fail(IPI_EVALIDATION, "null vector");
+  return op_launch(op, x_full, b, b ? 5 : 4, y, (cudaStream_t)stream, y_partial);
+}
+
+int ipi_csr_split_local(const int64_t* rp, const int32_t* col, const double* val, int64_t rows,
+                        int64_t lo, int64_t hi, int64_t* rp_loc, int32_t* col_loc, double* val_loc,
+                        int64_t* rp_rem, int32_t* col_rem, double* val_rem, void* stream) {
+  if (rows < 0 || lo < 0 || hi < lo || hi > INT32_MAX) return fail(IPI_EDIMENSION, "bad split geometry");
+  if (!rp || !rp_loc || !rp_rem) return fail(IPI_EVALIDATION, "null row pointers");
+  if ((col_loc == nullptr) != (col_rem == nullptr) || (col_loc && (!val_loc || !val_rem)))
+    return fail(IPI_EVALIDATION, "split: pass 2 needs all output arrays");
+  return split_local_remote(rp, col, val, rows, (int32_t)lo, (int32_t)hi, rp_loc, col_loc, val_loc,
+                            rp_rem, col_rem, val_rem, (cudaStream_t)stream);
+}
+
 int ipi_jacobi_inv_diag(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi,
                         int64_t n, double gamma, double* inv_diag, void* stream) {
   if (!inv_diag) return fail(IPI_EVALIDATION, "null output");

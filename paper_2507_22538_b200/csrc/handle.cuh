@@ -130,14 +130,18 @@ int policy_nnz(ipi_mdp* h, const int32_t* policy, int64_t* nnz_out, cudaStream_t
 // spmv.cu
 int launch_spmv(const int64_t* rp, const int32_t* col, const double* val, int64_t rows,
                 const double* x, const double* b, double gamma, int epi, double* y,
-                int lanes, cudaStream_t st, int64_t diag_offset = 0);
+                int lanes, cudaStream_t st, int64_t diag_offset = 0,
+                const double* y_partial = nullptr);
+int split_local_remote(const int64_t* rp, const int32_t* col, const double* val, int64_t rows,
+                       int32_t lo, int32_t hi, int64_t* rp_loc, int32_t* col_loc, double* val_loc,
+                       int64_t* rp_rem, int32_t* col_rem, double* val_rem, cudaStream_t st);
 
 // spmv_ring.cu: K3 ring kernels for a planned operator
 int k3_uring_smem(int K, int stages, int warps, int window_bytes);
 int k3_flat_smem(int K, int stages, int warps, int window_bytes);
 bool k3_shape_prepare(int variant, int K, int NW, int S, bool win, int smem);
 int op_launch(const ipi_op* op, const double* x_full, const double* b, int epi, double* y,
-              cudaStream_t st);
+              cudaStream_t st, const double* y_partial = nullptr);
 
 // krylov.cu
 int inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi, int64_t n,

@@ -454,11 +454,11 @@ static bool k3_launch_epi(const ipi_op* op, const K3Args& a, cudaStream_t st) {
 
 // y = epi(P x) over the operator's rows; generic rows use spmv.cu's kernel.
 int op_launch(const ipi_op* op, const double* x_full, const double* b, int epi, double* y,
-              cudaStream_t st) {
+              cudaStream_t st, const double* y_partial) {
   if (op->n_local <= 0) return IPI_OK;
-  if (op->variant == IPI_K3_GENERIC)
+  if (op->variant == IPI_K3_GENERIC || epi >= 4)  // split halves: generic rows
     return launch_spmv(op->rp, op->col, op->val, op->n_local, x_full, b, op->gamma, epi, y,
-                       op->lanes, st, op->state0);
+                       op->lanes, st, op->state0, y_partial);
   K3Args a{op->col, op->val, op->n_local, op->state0, op->n_global, x_full, b, op->gamma, y, op->halo,
             op->pf};
   bool ok = false;

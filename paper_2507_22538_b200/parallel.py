@@ -15,6 +15,7 @@ a run at fixed R is bit-reproducible like ``tree_reduce`` (parallel.py:21-33).
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import torch
@@ -109,6 +110,75 @@ def allgather_blocks(local: torch.Tensor, full: torch.Tensor, partition: Partiti
         lo, hi = partition.block(r)
         full[lo:hi] = buf[r * mx: r * mx + (hi - lo)]
     return full
+
+
+class _Done:
+    def wait(self):
+        return None
+
+
+def allgather_blocks_async(local: torch.Tensor, full: torch.Tensor, partition: Partition):
+    """Start the all-gather of ``local`` into ``full``; returns a waitable.  With
+    NCCL the collective runs on its own stream while the caller keeps launching
+    work that does not read ``full``; ``wait()`` orders later work after it.
+    Unequal blocks fall back to the blocking path."""
+    import torch.distributed as dist
+    if (not (dist.is_available() and dist.is_initialized()) or partition.worker_count == 1
+            or len(set(partition.block_sizes())) != 1):
+        allgather_blocks(local, full, partition)
+        return _Done()
+    if _nccl():
+        return dist.all_gather_into_tensor(full, local.contiguous(), async_op=True)
+    return dist.all_gather(list(full.split(partition.block_sizes())), local.contiguous(),
+                           async_op=True)
+
+
+class SplitShardOperator:
+    """J_pi on a rank's rows with the V exchange overlapped (north star (5)):
+    the rank's P_pi rows are split into local columns (its own state block,
+    re-indexed) and remote columns (``ipi_csr_split_local``).  ``apply`` starts
+    the all-gather of x, runs the local-column SpMV on x_local while it is in
+    flight, waits, then the remote half adds its sum and forms
+    x - gamma*(P_loc x + P_rem x) (``ipi_op_apply_partial``).  Row sums are
+    (local part) + (remote part): deterministic, within 1e-13 of the unsplit
+    order."""
+
+    def __init__(self, rp, col, val, n_local: int, n_global: int, state0: int, gamma: float):
+        from .sparse import DeviceOperator
+        dev = rp.device
+        L = _lib.lib()
+        rp_loc = torch.zeros(n_local + 1, dtype=torch.int64, device=dev)
+        rp_rem = torch.zeros(n_local + 1, dtype=torch.int64, device=dev)
+        lo, hi = state0, state0 + n_local
+        _lib.check(L.ipi_csr_split_local(_lib.ptr(rp), _lib.ptr(col), _lib.ptr(val), n_local, lo, hi,
+                                         _lib.ptr(rp_loc), None, None, _lib.ptr(rp_rem), None, None,
+                                         _lib.stream_ptr()), "ipi_csr_split_local")
+        rp_loc[1:] = torch.cumsum(rp_loc[1:], 0)
+        rp_rem[1:] = torch.cumsum(rp_rem[1:], 0)
+        nl, nr = (int(x) for x in torch.stack([rp_loc[-1], rp_rem[-1]]).tolist())
+        col_loc = torch.empty(max(nl, 1), dtype=torch.int32, device=dev)
+        val_loc = torch.empty(max(nl, 1), dtype=torch.float64, device=dev)
+        col_rem = torch.empty(max(nr, 1), dtype=torch.int32, device=dev)
+        val_rem = torch.empty(max(nr, 1), dtype=torch.float64, device=dev)
+        _lib.check(L.ipi_csr_split_local(_lib.ptr(rp), _lib.ptr(col), _lib.ptr(val), n_local, lo, hi,
+                                         _lib.ptr(rp_loc), _lib.ptr(col_loc), _lib.ptr(val_loc),
+                                         _lib.ptr(rp_rem), _lib.ptr(col_rem), _lib.ptr(val_rem),
+                                         _lib.stream_ptr()), "ipi_csr_split_local")
+        self.local = DeviceOperator(rp_loc, col_loc[:nl], val_loc[:nl], n_local, n_local, 0, gamma)
+        self.remote = DeviceOperator(rp_rem, col_rem[:nr], val_rem[:nr], n_local, n_global, state0,
+                                     gamma)
+        self.n_local, self.nnz_local, self.nnz_remote = n_local, nl, nr
+
+    def plan(self) -> dict:
+        return {"split": True, "nnz_local": self.nnz_local, "nnz_remote": self.nnz_remote,
+                "local": self.local.plan(), "remote": self.remote.plan()}
+
+    def apply_overlapped(self, x_local: torch.Tensor, full: torch.Tensor, partition: Partition,
+                         b: torch.Tensor | None = None) -> torch.Tensor:
+        work = allgather_blocks_async(x_local, full, partition)
+        y_loc = self.local.spmv(x_local)          # overlaps the all-gather
+        work.wait()
+        return self.remote.apply_partial(full, y_loc, b)
 
 
 def rank_ordered_sum(partial: torch.Tensor, world: int) -> torch.Tensor:
@@ -283,7 +353,7 @@ class ShardOps(ShardVectorOps):
         res = float(bits.view(torch.float64)[0])
         return pol.clone(), app.clone(), self.max(res)
 
-    def gather_policy(self, policy_local: torch.Tensor):
+    def gather_policy(self, policy_local: torch.Tensor, split: bool | None = None):
         sh = self.shard
         h = sh.handle()
         nnz = _lib.C.c_int64()
@@ -298,15 +368,22 @@ class ShardOps(ShardVectorOps):
         _lib.check(L.ipi_gather_policy(h, _lib.ptr(policy_local), _lib.ptr(rp), _lib.ptr(col),
                                        _lib.ptr(val), _lib.ptr(g), _lib.stream_ptr()),
                    "ipi_gather_policy")
-        # K3 planned once per policy (ring kernel for uniform rows, no sync per apply)
-        op = DeviceOperator(rp, col[:nnz.value], val[:nnz.value], sh.n_local, sh.n_global,
-                            sh.state0, sh.gamma)
+        # K3 planned once per policy: with R > 1 ranks the rows are split into
+        # local / remote columns so the V all-gather overlaps the local half
+        # (IPI_SHARD_OVERLAP=0: one operator over the gathered vector)
+        if split is None:
+            split = self.ctx.world > 1 and os.environ.get("IPI_SHARD_OVERLAP", "1") != "0"
+        cls = SplitShardOperator if split else DeviceOperator
+        op = cls(rp, col[:nnz.value], val[:nnz.value], sh.n_local, sh.n_global, sh.state0, sh.gamma)
         return op, g
 
     def apply(self, P, x_local: torch.Tensor, b_local: torch.Tensor | None = None) -> torch.Tensor:
         """b - (x - gamma P x) (or x - gamma P x) on the local rows."""
+        b = b_local.contiguous() if b_local is not None else None
+        if isinstance(P, SplitShardOperator):
+            return P.apply_overlapped(x_local.contiguous(), self.full, self.ctx.partition, b)
         xf = self.allgather(x_local)
-        return P.apply(xf, b_local.contiguous() if b_local is not None else None)
+        return P.apply(xf, b)
 
     def sweep(self, P, g_local, v_local):
         """g_pi + gamma * P_pi v (breakdown fallback, driver.py:190-193)."""

@@ -247,6 +247,17 @@ class DeviceOperator:
                                            _lib.stream_ptr()), "ipi_op_apply")
         return y
 
+    def apply_partial(self, x_full: torch.Tensor, y_partial: torch.Tensor,
+                      b: torch.Tensor | None = None, out: torch.Tensor | None = None) -> torch.Tensor:
+        """x[s] - gamma*(y_partial + P x) on the rows (b - that when b is given):
+        the remote-column half of a split apply."""
+        y = out if out is not None else torch.empty(self.n_local, dtype=torch.float64,
+                                                    device=x_full.device)
+        _lib.check(_lib.lib().ipi_op_apply_partial(self._h, _lib.ptr(x_full), _lib.ptr(y_partial),
+                                                   _lib.ptr(b), _lib.ptr(y), _lib.stream_ptr()),
+                   "ipi_op_apply_partial")
+        return y
+
     def spmv(self, x_full: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         y = out if out is not None else torch.empty(self.n_local, dtype=torch.float64,
                                                     device=x_full.device)

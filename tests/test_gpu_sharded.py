@@ -32,10 +32,10 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, n, kind, q):
+def _worker(rank, world, port, n, kind, q, overlap="1"):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
-                      WORLD_SIZE=str(world))
+                      WORLD_SIZE=str(world), IPI_SHARD_OVERLAP=overlap)
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -56,14 +56,16 @@ def _worker(rank, world, port, n, kind, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kind", ["gmres", "richardson"])
-def test_two_ranks_on_device_match_persistent_solver(kind):
+@pytest.mark.parametrize("kind,n,overlap", [("gmres", 8191, "1"), ("richardson", 8191, "1"),
+                                            ("gmres", 8192, "1"), ("gmres", 8192, "0")])
+def test_two_ranks_on_device_match_persistent_solver(kind, n, overlap):
+    """n = 8191: unequal blocks (blocking gather); n = 8192: equal blocks, the
+    split operator's all-gather runs async (overlap) or the unsplit path."""
     import torch.multiprocessing as mp
-    n = 8191  # unequal blocks
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, n, kind, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, n, kind, q, overlap)) for r in range(2)]
     for p in procs:
         p.start()
     out = sorted(q.get(timeout=600) for _ in procs)
@@ -103,3 +105,28 @@ def test_mgs_kernels_match_torch(n):
     np.testing.assert_allclose(nn.item(), torch.dot(w1, w1).item(), rtol=1e-13)
     # deterministic: rerun bit-identical
     assert dev_ops.dot_partial(a, b).item() == d.item()
+
+
+@pytest.mark.parametrize("state0,n_local", [(0, 3000), (3000, 2000), (7000, 1192)])
+def test_split_operator_halves_equal_unsplit(state0, n_local):
+    """Local-column / remote-column split of a rank's P_pi rows: the two halves
+    (ipi_csr_split_local, ipi_op_apply_partial) reproduce the unsplit apply to
+    1e-13 (only the row-sum association differs)."""
+    from paper_2507_22538_b200.parallel import SplitShardOperator
+    from paper_2507_22538_b200.sparse import DeviceOperator
+    from paper_2507_22538_b200.generators import CONFIGS
+    spec = CONFIGS[2]
+    n = 8192
+    rp, col, val, cost = devgen.locality(n, 1, spec.K, 600, 0, state0, n_local)
+    x = torch.rand(n, dtype=torch.float64, device="cuda")
+    b = torch.rand(n_local, dtype=torch.float64, device="cuda")
+    whole = DeviceOperator(rp, col, val, n_local, n, state0, 0.99)
+    sp = SplitShardOperator(rp, col, val, n_local, n, state0, 0.99)
+    plan = sp.plan()
+    assert plan["nnz_local"] + plan["nnz_remote"] == n_local * spec.K
+    assert plan["nnz_remote"] > 0 or n_local == n
+    for bb in (None, b):
+        y_loc = sp.local.spmv(x[state0:state0 + n_local].contiguous())
+        got = sp.remote.apply_partial(x, y_loc, bb)
+        ref = whole.apply(x, bb)
+        torch.testing.assert_close(got, ref, rtol=1e-13, atol=1e-14)
