@@ -182,6 +182,85 @@ __global__ void validate_rows_kernel(const int64_t* rp, const int32_t* col, cons
   }
 }
 
+// Uniform rows of length K = 8*G (K % 4 == 0 and 16-byte aligned arrays: C2 /
+// C5's K = 64): G lanes per row, 8 consecutive entries per lane read with
+// 16-byte loads, 32/G rows per warp step and two steps in flight, so the
+// 26 GB validation pass streams instead of waiting per row (the warp-per-row
+// kernel above is latency-bound).  Same checks and counters; the row sum is
+// lane partials then an xor tree (1e-12 tolerance, as the warp-per-row kernel).
+template <int G>
+__global__ void __launch_bounds__(256) validate_rows_uniform_kernel(
+    const int32_t* __restrict__ col, const double* __restrict__ val, int64_t rows, int64_t ncols,
+    VAcc* acc, int structural_only) {
+  constexpr int K = 8 * G, RPW = 32 / G;
+  const int lane = threadIdx.x & 31, grp = lane / G, gl = lane % G;
+  const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t pol = policy_evict_first();
+  unsigned long long br = 0, bo = 0, nf = 0;
+  auto do_rows = [&](int64_t base) {
+    const int64_t r = base + grp;
+    const bool ok = r < rows;
+    const int64_t p0 = (ok ? r : 0) * K + 8 * gl;
+    double v[8];
+    int c[8];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double2 t = ld_stream_v2(val + p0 + 2 * q, pol);
+      v[2 * q] = t.x;
+      v[2 * q + 1] = t.y;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int2 t = ld_stream_v2(col + p0 + 2 * q, pol);
+      c[2 * q] = t.x;
+      c[2 * q + 1] = t.y;
+    }
+    // previous column of this lane's first entry: last entry of lane gl-1 in the row
+    const int prev = __shfl_up_sync(kFull, c[7], 1);
+    double sum = 0.0;
+    if (ok) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        br += (c[q] < 0 || (int64_t)c[q] >= ncols);
+        if (q > 0) bo += c[q - 1] >= c[q];
+        if (!isfinite(v[q])) nf += 1;
+        if (!structural_only && (v[q] < 0.0 || v[q] > 1.0))
+          atomicMin(&acc->first_bad_prob, (unsigned long long)(p0 + q));
+        sum = add_rn(sum, v[q]);
+      }
+      if (gl > 0) bo += prev >= c[0];
+    }
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) sum = add_rn(sum, __shfl_xor_sync(kFull, sum, off));
+    if (!structural_only && ok && gl == 0 && fabs(sum - 1.0) > 1e-12) {
+      atomicAdd(&acc->n_bad_sum, 1ull);
+      atomicMin(&acc->first_bad_sum_row, (unsigned long long)r);
+    }
+  };
+  for (int64_t base = wg * RPW; base < rows; base += 2 * nw * RPW) {
+    do_rows(base);
+    if (base + nw * RPW < rows) do_rows(base + nw * RPW);
+  }
+  for (int off = 16; off; off >>= 1) {
+    br += __shfl_xor_sync(kFull, br, off);
+    bo += __shfl_xor_sync(kFull, bo, off);
+    nf += __shfl_xor_sync(kFull, nf, off);
+  }
+  if (lane == 0) {
+    if (br) atomicAdd(&acc->bad_range, br);
+    if (bo) atomicAdd(&acc->bad_order, bo);
+    if (nf) atomicAdd(&acc->nonfinite, nf);
+  }
+}
+
+__global__ void uniform_rp_check_kernel(const int64_t* rp, int64_t rows, int64_t K,
+                                        unsigned long long* bad) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r <= rows;
+       r += (int64_t)gridDim.x * blockDim.x)
+    if (rp[r] != r * K) atomicAdd(bad, 1ull);
+}
+
 __global__ void row_sum_kernel(const int64_t* rp, const double* val, int64_t r, double* out) {
   // same summation layout as validate_rows_kernel for one row
   const int lane = threadIdx.x;
@@ -699,8 +778,25 @@ static int csr_check_impl(const int64_t* rp, const int32_t* col, const double* v
   out->nnz = last;
   out->nnz_mismatch = (last != nnz_len);
   if (out->bad_row_ptr == 0 && !out->nnz_mismatch && rows > 0 && last > 0) {
-    validate_rows_kernel<<<grid_for(rows * 32, 256, sms), 256, 0, st>>>(rp, col, val, rows, cols,
-                                                                          probs ? -1 : (long long)rows, d, probs ? 0 : 1);
+    // uniform K = 64 rows with 16-byte aligned arrays: the streaming kernel
+    bool uniform64 = last == rows * 64 && (uintptr_t)val % 16 == 0 && (uintptr_t)col % 16 == 0;
+    if (uniform64) {  // every row exactly 64 long <=> rp[r] == 64 r (checked on the device)
+      unsigned long long* flag = nullptr;
+      uniform64 = cudaMalloc(&flag, sizeof(unsigned long long)) == cudaSuccess;
+      if (uniform64) {
+        unsigned long long hflag = 0;
+        cudaMemsetAsync(flag, 0, sizeof(unsigned long long), st);
+        uniform_rp_check_kernel<<<grid_for(rows + 1, 256, sms), 256, 0, st>>>(rp, rows, 64, flag);
+        cudaMemcpyAsync(&hflag, flag, sizeof(hflag), cudaMemcpyDeviceToHost, st);
+        uniform64 = cudaStreamSynchronize(st) == cudaSuccess && hflag == 0;
+        cudaFree(flag);
+      }
+    }
+    if (uniform64)
+      validate_rows_uniform_kernel<8><<<sms * 8, 256, 0, st>>>(col, val, rows, cols, d, probs ? 0 : 1);
+    else
+      validate_rows_kernel<<<grid_for(rows * 32, 256, sms), 256, 0, st>>>(rp, col, val, rows, cols,
+                                                                            probs ? -1 : (long long)rows, d, probs ? 0 : 1);
     cudaMemcpyAsync(res, d, sizeof(VAcc), cudaMemcpyDeviceToHost, st);
     e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) {

@@ -131,3 +131,50 @@ def test_validate_messages(mutate, pattern):
 def test_csr_structure_errors(rp, col, val, pattern):
     with pytest.raises(ValueError, match=pattern):
         ipi.CsrMatrix(2, 2, np.asarray(rp), np.asarray(col), np.asarray(val))
+
+
+def _k64_instance(n=2000, m=4, seed=0):
+    from paper_2507_22538_b200.generators import random_locality_host
+    return random_locality_host(n, m, 64, 300, seed=seed)
+
+
+@pytest.mark.parametrize("kind", ["prob", "sum", "order", "range", "nan", "clean"])
+def test_validate_uniform_k64_streaming_kernel(kind):
+    """The K = 64 streaming validation kernel reports what the reference's
+    validate reports (model.py:148-194): first bad probability entry, bad row
+    sums (first five rows), and the structural CSR errors."""
+    n, m = 2000, 4
+    rp, col, val, cost = (np.array(a, copy=True) for a in _k64_instance(n, m))
+    if kind == "prob":
+        val[777] = -0.25
+        val[778] += 0.25
+        want = "entry 777 is -0.25"
+    elif kind == "sum":
+        val[64 * 5 + 3] += 1e-9           # row 5
+        val[64 * 901 + 10] *= 1.5         # row 901
+        want = "row 5 sums to"
+    elif kind == "order":
+        r0 = 64 * 42
+        col[r0 + 9], col[r0 + 10] = col[r0 + 10], col[r0 + 9]
+        want = "strictly increasing"
+    elif kind == "range":
+        col[64 * 7 + 63] = n + 5
+        want = "lie in \\[0"
+    elif kind == "nan":
+        val[4000] = np.nan
+        want = "finite"
+    else:
+        want = None
+    if kind in ("order", "range", "nan"):
+        # structural errors surface from CsrMatrix construction (sparse.py:56-86)
+        with pytest.raises((ipi.ValidationError, ValueError), match=want):
+            ipi.CsrMatrix(n * m, n, rp, col, val)
+        return
+    mdp = ipi.MdpInstance(n, m, 0.9, cost, ipi.CsrMatrix(n * m, n, rp, col, val))
+    probs = ipi.validate(mdp)
+    if want is None:
+        assert probs == []
+    else:
+        assert any(want in p for p in probs), probs
+        if kind == "sum":
+            assert "row 901" in " ".join(probs)
