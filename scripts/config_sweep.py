@@ -156,6 +156,32 @@ def main():
                                  "cores": 1, "kind": "port (numpy)",
                                  "v_rel_diff": float(np.max(np.abs(ref.values - res.values)) /
                                                      max(1.0, np.abs(ref.values).max()))}
+        if a.cpu:
+            # C/OpenMP restatement (bitwise equal to the reference's greedy_policy) on all
+            # host threads: backup throughput for every config, full solve for C1/C2/C4
+            from oracle import c_oracle as co
+            if host is None:
+                rp, col, val = mdp.transitions.numpy()
+                host = (rp, col, val, mdp.stage_cost.cpu().numpy())
+            rp, col, val, cost = host
+            nt = os.cpu_count() or 1
+            v = np.zeros(mdp.n)
+            co.greedy(rp, col, val, cost, spec.gamma, v, nthreads=nt)
+            tg = time.perf_counter()
+            co.greedy(rp, col, val, cost, spec.gamma, v, nthreads=nt)
+            tg = time.perf_counter() - tg
+            rec["cpu_c_oracle"] = {"greedy_s": tg, "backups_per_s": mdp.n * mdp.m / tg, "cores": nt,
+                                   "kind": "port (C/OpenMP)"}
+            if cfg in (1, 2, 4):
+                ts = time.perf_counter()
+                ref = co.solve(rp, col, val, cost, spec.gamma, tol=spec.atol, alpha=spec.alpha,
+                               nthreads=nt)
+                ts = time.perf_counter() - ts
+                rec["cpu_c_oracle"].update({
+                    "solve_s": ts, "status": ref.status, "outer": ref.outer_iterations,
+                    "inner": ref.inner_iterations_total,
+                    "v_rel_diff": float(np.max(np.abs(ref.values - res.values)) /
+                                        max(1.0, np.abs(ref.values).max()))})
         print(json.dumps(rec), flush=True)
         out.append(rec)
         del mdp
