@@ -191,8 +191,9 @@ __device__ __forceinline__ bool better(double q, int a, double bq, int ba, bool 
   return q < bq || (q == bq && a < ba);
 }
 
-// Block reduction of one double per thread: warp trees then warp 0 sums the
-// per-warp values in warp order.  Result valid in thread 0 only.
+// Block reduction of one double per thread: warp trees, then warp 0 reduces
+// the per-warp values with the same fixed xor tree (deterministic).  Result
+// valid in warp 0 (thread 0 is the one callers use).
 __device__ __forceinline__ double block_sum(double v, double* red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   v = warp_sum(v);
@@ -200,9 +201,9 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   if (lane == 0) red[warp] = v;
   __syncthreads();
   double t = 0.0;
-  if (threadIdx.x == 0) {
-    const int nw = blockDim.x >> 5;
-    for (int w = 0; w < nw; ++w) t = add_rn(t, red[w]);
+  if (warp == 0) {  // the per-warp values through the same fixed xor tree
+    t = lane < (int)(blockDim.x >> 5) ? red[lane] : 0.0;
+    t = warp_sum(t);
   }
   return t;
 }

@@ -102,7 +102,7 @@ struct GridBarrier {
 };
 
 struct KShared {
-  double red[32];
+  double red[64];
   double bc[4];
   double H[(R + 1) * R];
   double cs[R], sn[R], g[R + 1], y[R];
@@ -110,21 +110,36 @@ struct KShared {
 };
 
 // Two-level deterministic all-reduce of NV doubles; result in every thread.
+// Block level: warp xor trees, one shared-memory exchange for all NV values,
+// warp 0 xor tree; grid level: per-CTA partials, the grid barrier, every CTA
+// sums all partials in the same order.  Four CTA barriers per call (the
+// broadcast slot sh.bc is next written only after two barriers of the next call).
 template <int NV>
 __device__ __forceinline__ void grid_allreduce(double (&v)[NV], const KArgs& a, int& slot,
                                                GridBarrier& gb, KShared& sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double t[NV];
 #pragma unroll
-  for (int k = 0; k < NV; ++k) t[k] = block_sum(v[k], sh.red);
-  const int nblk = gridDim.x;
-  if (threadIdx.x == 0) {
+  for (int k = 0; k < NV; ++k) t[k] = warp_sum(v[k]);
+  __syncthreads();  // sh.red free (previous call's warp 0 finished reading it)
+  if (lane == 0) {
 #pragma unroll
-    for (int k = 0; k < NV; ++k) a.partials[((int64_t)slot * nblk + blockIdx.x) * 2 + k] = t[k];
+    for (int k = 0; k < NV; ++k) sh.red[k * 32 + warp] = t[k];
+  }
+  __syncthreads();
+  const int nblk = gridDim.x;
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) t[k] = warp_sum(lane < nw ? sh.red[k * 32 + lane] : 0.0);
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < NV; ++k) a.partials[((int64_t)slot * nblk + blockIdx.x) * 2 + k] = t[k];
+    }
   }
   gb.arrive_and_wait(threadIdx.x == 0);
   __syncthreads();
   if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
       double s = 0.0;
@@ -138,7 +153,6 @@ __device__ __forceinline__ void grid_allreduce(double (&v)[NV], const KArgs& a, 
 #pragma unroll
   for (int k = 0; k < NV; ++k) v[k] = sh.bc[k];
   slot ^= 1;
-  __syncthreads();
 }
 
 // Row sums of P_pi over this CTA's rows with an optional shared-memory window
