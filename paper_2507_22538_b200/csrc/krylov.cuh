@@ -170,10 +170,13 @@ __device__ __forceinline__ void spmv_rows(const KArgs& a, const double* xin, int
     lo = lo < 0 ? 0 : lo;
     hi = hi > a.n ? a.n : hi;
     __syncthreads();
-    if (hi - lo <= a.win_cap) {
+    if (hi - lo <= a.win_cap) {  // all copies in flight at once (8-byte cp.async)
       w_lo = lo;
       w_len = hi - lo;
-      for (int64_t i = threadIdx.x; i < w_len; i += blockDim.x) win[i] = xin[lo + i];
+      const uint32_t ws = (uint32_t)__cvta_generic_to_shared(win);
+      for (int64_t i = threadIdx.x; i < w_len; i += blockDim.x) cp_async8(ws + (uint32_t)(8 * i), xin + lo + i);
+      cp_async_commit();
+      cp_async_wait<0>();
     }
     __syncthreads();
   }
