@@ -72,8 +72,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_bellman(K1Args a) {
     hi = hi > a.n_global ? a.n_global : hi;
     w_lo = lo;
     w_len = hi > lo ? hi - lo : 0;
-    for (int64_t i = threadIdx.x; i < w_len; i += blockDim.x) win[i] = __ldg(a.v + lo + i);
-    __syncthreads();
+    window_load8(win, a.v, lo, w_len);
   }
   const uint64_t pol = policy_evict_first();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
@@ -188,8 +187,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_bellman_uniform(K1Args a, int K
     hi = hi > a.n_global ? a.n_global : hi;
     w_lo = lo;
     w_len = hi > lo ? hi - lo : 0;
-    for (int64_t i = threadIdx.x; i < w_len; i += blockDim.x) win[i] = __ldg(a.v + lo + i);
-    __syncthreads();
+    window_load8(win, a.v, lo, w_len);
   }
   const uint64_t pol = policy_evict_first();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
@@ -329,8 +327,7 @@ __global__ void __launch_bounds__(kK1Threads, 2) k1_bellman_flat(K1Args a, int K
     hi = hi > a.n_global ? a.n_global : hi;
     w_lo = (int)lo;
     w_len = hi > lo ? (uint32_t)(hi - lo) : 0u;
-    for (uint32_t i = threadIdx.x; i < w_len; i += blockDim.x) win[i] = __ldg(a.v + lo + i);
-    __syncthreads();
+    window_load8(win, a.v, lo, w_len);
   }
   const uint64_t pol = policy_evict_first();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
@@ -486,8 +483,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_bellman_ring(K1Args a, int win_
     hi = hi > a.n_global ? a.n_global : hi;
     w_lo = (int)lo;
     w_len = hi > lo ? (uint32_t)(hi - lo) : 0u;
-    for (uint32_t i = threadIdx.x; i < w_len; i += blockDim.x) win[i] = __ldg(a.v + lo + i);
-    __syncthreads();
+    window_load8(win, a.v, lo, w_len);
   }
   const uint64_t pol = policy_evict_first();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1023,8 +1019,7 @@ __global__ void __launch_bounds__(kK1Threads, 1) k1_bellman_deep(K1Args a, int K
     hi = hi > a.n_global ? a.n_global : hi;
     w_lo = (int)lo;
     w_len = hi > lo ? (uint32_t)(hi - lo) : 0u;
-    for (uint32_t i = threadIdx.x; i < w_len; i += blockDim.x) win[i] = __ldg(a.v + lo + i);
-    __syncthreads();
+    window_load8(win, a.v, lo, w_len);
   }
   const uint32_t win_s = (uint32_t)__cvta_generic_to_shared(win);
   const uint64_t pol = policy_evict_first();

@@ -148,6 +148,18 @@ __device__ __forceinline__ void window_issue_async(const double* x, int64_t lo, 
   cp_async_commit();
 }
 
+// Stage x[lo, lo+len) into shared memory with 8-byte cp.async (every copy in
+// flight at once; only 8-byte alignment needed), then wait and barrier.  A
+// scalar load/store loop here waits one L2 round trip per few elements and
+// stalled the start of every CTA.
+__device__ __forceinline__ void window_load8(double* win, const double* x, int64_t lo, int64_t len) {
+  const uint32_t ws = (uint32_t)__cvta_generic_to_shared(win);
+  for (int64_t i = threadIdx.x; i < len; i += blockDim.x) cp_async8(ws + (uint32_t)(8 * i), x + lo + i);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+}
+
 // Bulk L2 prefetch of a contiguous byte range (16-byte aligned, multiple of 16).
 __device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
