@@ -19,6 +19,7 @@
 // state range so the window is compact and the L1 working set is local.
 #include <cfloat>
 #include <climits>
+#include <cstdlib>
 
 #include "handle.cuh"
 
@@ -46,6 +47,7 @@ struct K1Args {
   int32_t interleave;  // uniform ring: warps take interleaved states
   int32_t rotate;      // uniform ring: per-CTA rotated start in the warp's state sequence
   unsigned long long* trace;  // diagnostics: per-CTA (smid, t_start, t_end) or nullptr
+  int32_t gen_u;              // generic rows, G = 32: loads in flight per lane (4, 8, 16)
 };
 
 __device__ __forceinline__ unsigned long long global_ns() {
@@ -59,7 +61,7 @@ __device__ __forceinline__ unsigned sm_id() {
   return r;
 }
 
-template <int G, bool WIN>
+template <int G, bool WIN, int UL = (G == 32 ? 8 : 4)>
 __global__ void __launch_bounds__(kK1Threads) k1_bellman(K1Args a) {
   extern __shared__ double win[];
   __shared__ double red[32];
@@ -100,7 +102,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_bellman(K1Args a) {
       if (act < m) {
         const int64_t p0 = __ldg(a.rp + row0 + act), p1 = __ldg(a.rp + row0 + act + 1);
         // long rows (G = 32, e.g. C4's ~570-entry rows): 8 loads in flight per lane
-        constexpr int U = G == 32 ? 8 : 4;
+        constexpr int U = UL;
         for (int64_t p = p0 + gl; p < p1; p += U * G) {
           double vv[U];
           int cc[U];
@@ -1204,6 +1206,16 @@ static cudaError_t uniform_smem(int G, int P, int smem) {
 
 template <int G>
 static void launch_g(const K1Args& a, bool win, int blocks, int smem, cudaStream_t st) {
+  if (G == 32 && a.gen_u == 4) {  // long rows, 4 loads per lane (A/B: IPI_K1_GEN_U)
+    if (win) k1_bellman<G, true, 4><<<blocks, kK1Threads, smem, st>>>(a);
+    else k1_bellman<G, false, 4><<<blocks, kK1Threads, 0, st>>>(a);
+    return;
+  }
+  if (G == 32 && a.gen_u == 16) {
+    if (win) k1_bellman<G, true, 16><<<blocks, kK1Threads, smem, st>>>(a);
+    else k1_bellman<G, false, 16><<<blocks, kK1Threads, 0, st>>>(a);
+    return;
+  }
   if (win)
     k1_bellman<G, true><<<blocks, kK1Threads, smem, st>>>(a);
   else
@@ -1212,7 +1224,10 @@ static void launch_g(const K1Args& a, bool win, int blocks, int smem, cudaStream
 
 template <int G>
 static cudaError_t set_smem_attr(int smem) {
-  return raise_smem_limit(k1_bellman<G, true>, smem);
+  cudaError_t e = raise_smem_limit(k1_bellman<G, true>, smem);
+  if (G == 32 && e == cudaSuccess) e = raise_smem_limit(k1_bellman<G, true, 4>, smem);
+  if (G == 32 && e == cudaSuccess) e = raise_smem_limit(k1_bellman<G, true, 16>, smem);
+  return e;
 }
 
 int k1_set_smem(int lanes, int smem) {
@@ -1294,6 +1309,7 @@ int launch_bellman(ipi_mdp* h, const double* v_full, int32_t mode, int32_t* poli
   a.interleave = h->k1_interleave;
   a.rotate = h->k1_rotate;
   a.trace = h->k1_trace;
+  a.gen_u = getenv("IPI_K1_GEN_U") ? atoi(getenv("IPI_K1_GEN_U")) : 8;
   const bool win = h->plan.halo >= 0;
   const int blocks = h->plan.k1_blocks, smem = h->plan.k1_smem_bytes;
   int G = 0, P = 0;

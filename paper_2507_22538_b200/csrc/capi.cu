@@ -386,7 +386,7 @@ int ipi_mdp_create(const int64_t* row_ptr, const int32_t* col, const double* val
   // whose window (own slice + 2*2^k, clipped to n_global) fits 100 KB (two
   // 512-thread CTAs per SM); use it only if it covers >= 50% of the gathers,
   // then shrink to the smallest k within 1% of that coverage.
-  const int ctas_win = 2;
+  const int ctas_win = getenv("IPI_K1_GEN_CTAS") ? std::max(1, atoi(getenv("IPI_K1_GEN_CTAS"))) : 2;
   const int nb_win = h->num_sms * ctas_win;
   const int64_t own = (n_local + nb_win - 1) / std::max(nb_win, 1);
   const int64_t cap_doubles = 100 * 1024 / 8;
@@ -600,6 +600,71 @@ int ipi_mdp_create(const int64_t* row_ptr, const int32_t* col, const double* val
       cudaFree(tap);
       cudaFree(tpol);
     }
+  }
+  // ---- generic rows: autotune the CTA count (C4: 2 CTAs/SM 0.200 ms, 8 CTAs/SM
+  // 0.154 ms; the order is not monotone, scripts/c4_ab.sh).  One warm + one
+  // timed launch per candidate; IPI_K1_GEN_CTAS forces the static choice.
+  if (p.k1_variant == 0 && p.halo >= 0 && nnz >= (1ll << 24) && n_local > 0 &&
+      !getenv("IPI_K1_GEN_CTAS") && !(getenv("IPI_K1_AUTOTUNE") && getenv("IPI_K1_AUTOTUNE")[0] == '0')) {
+    const int64_t max_blocks_g = std::max<int64_t>(1, (n_local + 15) / 16);
+    auto install_gen = [&](int ctas) -> bool {
+      const int blocks = (int)std::min<int64_t>((int64_t)h->num_sms * ctas, max_blocks_g);
+      int64_t* db = nullptr;
+      if (cudaMalloc(&db, sizeof(int64_t) * (blocks + 1)) != cudaSuccess) return false;
+      bounds_kernel<<<(blocks + 1 + 127) / 128, 128, 0, st>>>(row_ptr, n_local, m, blocks, db);
+      std::vector<int64_t> hb(blocks + 1);
+      if (cudaMemcpyAsync(hb.data(), db, sizeof(int64_t) * (blocks + 1), cudaMemcpyDeviceToHost, st) !=
+              cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess) {
+        cudaFree(db);
+        return false;
+      }
+      int64_t worst = 0;
+      for (int c2 = 0; c2 < blocks; ++c2) worst = std::max<int64_t>(worst, hb[c2 + 1] - hb[c2]);
+      const int64_t wlen = std::min<int64_t>(n_global, worst + 2 * (int64_t)p.halo);
+      const int smem = (int)(wlen * 8 + 1024);
+      if (smem > 200 * 1024 || k1_set_smem(p.lanes_per_row, smem) != IPI_OK) {
+        cudaFree(db);
+        cudaGetLastError();
+        return false;
+      }
+      cudaFree(h->k1_bounds);
+      h->k1_bounds = db;
+      p.k1_blocks = blocks;
+      p.k1_smem_bytes = smem;
+      return true;
+    };
+    const int cand[5] = {8, 2, 4, 12, 16};
+    double* tv = nullptr;
+    double* tap = nullptr;
+    int32_t* tpol = nullptr;
+    bool ok = cudaMalloc(&tv, sizeof(double) * n_global) == cudaSuccess &&
+              cudaMalloc(&tap, sizeof(double) * n_local) == cudaSuccess &&
+              cudaMalloc(&tpol, sizeof(int32_t) * n_local) == cudaSuccess &&
+              cudaMemsetAsync(tv, 0, sizeof(double) * n_global, st) == cudaSuccess;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    ok = ok && cudaEventCreate(&e0) == cudaSuccess && cudaEventCreate(&e1) == cudaSuccess;
+    float best_ms = 1e30f;
+    int best_c = -1;
+    for (int ci = 0; ok && ci < 5; ++ci) {
+      if (!install_gen(cand[ci])) continue;
+      if (launch_bellman(h, tv, IPI_MODE_MIN, tpol, tap, nullptr, nullptr, nullptr, st)) break;
+      cudaEventRecord(e0, st);
+      if (launch_bellman(h, tv, IPI_MODE_MIN, tpol, tap, nullptr, nullptr, nullptr, st)) break;
+      cudaEventRecord(e1, st);
+      float ms = 0.f;
+      if (cudaEventSynchronize(e1) != cudaSuccess || cudaEventElapsedTime(&ms, e0, e1) != cudaSuccess) break;
+      if (ms < best_ms) {
+        best_ms = ms;
+        best_c = cand[ci];
+      }
+    }
+    cudaGetLastError();
+    if (best_c > 0) install_gen(best_c);
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    cudaFree(tv);
+    cudaFree(tap);
+    cudaFree(tpol);
   }
   // ---- flat rows (K <= 4): cp.async ring per warp (bellman.cu) ---------------
   if (p.uniform_rows && p.row_len_max <= 4 && (p.row_len_max % 2) == 0 && n_local > 0) {
