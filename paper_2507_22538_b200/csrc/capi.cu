@@ -37,6 +37,60 @@ cudaError_t raise_smem_limit(const void* fn, int smem) {
   return e;
 }
 
+// Plan-time autotuning: for each candidate that `install(i)` accepts, run
+// `launch()` once warm and once timed (CUDA events on `st`) and return the
+// index of the fastest (-1 if none ran).  The kernels' streaming rate depends on
+// the CTA count in a board-dependent way, so large instances are
+// planned by measurement; callers install the winner afterwards.
+template <class Install, class Launch>
+static int autotune_pick(int ncand, Install&& install, Launch&& launch, cudaStream_t st) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) {
+    if (e0) cudaEventDestroy(e0);
+    cudaGetLastError();
+    return -1;
+  }
+  float best_ms = 1e30f;
+  int best = -1;
+  for (int i = 0; i < ncand; ++i) {
+    if (!install(i)) continue;
+    if (launch()) break;
+    cudaEventRecord(e0, st);
+    if (launch()) break;
+    cudaEventRecord(e1, st);
+    float ms = 0.f;
+    if (cudaEventSynchronize(e1) != cudaSuccess || cudaEventElapsedTime(&ms, e0, e1) != cudaSuccess) break;
+    if (ms < best_ms) {
+      best_ms = ms;
+      best = i;
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaGetLastError();
+  return best;
+}
+
+// Zeroed V plus output buffers for timing K1 candidates at plan time.
+struct K1Scratch {
+  double* v = nullptr;
+  double* applied = nullptr;
+  int32_t* policy = nullptr;
+  bool ok = false;
+  K1Scratch(int64_t n_global, int64_t n_local, cudaStream_t st) {
+    ok = cudaMalloc(&v, sizeof(double) * n_global) == cudaSuccess &&
+         cudaMalloc(&applied, sizeof(double) * n_local) == cudaSuccess &&
+         cudaMalloc(&policy, sizeof(int32_t) * n_local) == cudaSuccess &&
+         cudaMemsetAsync(v, 0, sizeof(double) * n_global, st) == cudaSuccess;
+    if (!ok) cudaGetLastError();
+  }
+  ~K1Scratch() {
+    cudaFree(v);
+    cudaFree(applied);
+    cudaFree(policy);
+  }
+};
+
 int pick_lanes_per_row(double mean_len) {
   // ~4+ elements per lane: 4 independent loads in flight per row
   if (mean_len <= 6.0) return 1;
@@ -567,38 +621,13 @@ int ipi_mdp_create(const int64_t* row_ptr, const int32_t* col, const double* val
     const char* at = getenv("IPI_K1_AUTOTUNE");
     if (done && nshape > 1 && !(at && at[0] == '0') && nnz >= (1ll << 28)) {
       const int cand[4] = {8, 4, 6, 2};
-      double* tv = nullptr;
-      double* tap = nullptr;
-      int32_t* tpol = nullptr;
-      bool ok = cudaMalloc(&tv, sizeof(double) * n_global) == cudaSuccess &&
-                cudaMalloc(&tap, sizeof(double) * n_local) == cudaSuccess &&
-                cudaMalloc(&tpol, sizeof(int32_t) * n_local) == cudaSuccess &&
-                cudaMemsetAsync(tv, 0, sizeof(double) * n_global, st) == cudaSuccess;
-      cudaEvent_t e0 = nullptr, e1 = nullptr;
-      ok = ok && cudaEventCreate(&e0) == cudaSuccess && cudaEventCreate(&e1) == cudaSuccess;
-      float best_ms = 1e30f;
-      int best_w = -1;
-      for (int ci = 0; ok && ci < 4; ++ci) {
-        if (!install(12, 3, cand[ci], 1)) continue;
-        if (launch_bellman(h, tv, IPI_MODE_MIN, tpol, tap, nullptr, nullptr, nullptr, st)) break;
-        cudaEventRecord(e0, st);
-        if (launch_bellman(h, tv, IPI_MODE_MIN, tpol, tap, nullptr, nullptr, nullptr, st)) break;
-        cudaEventRecord(e1, st);
-        float ms = 0.f;
-        if (cudaEventSynchronize(e1) != cudaSuccess || cudaEventElapsedTime(&ms, e0, e1) != cudaSuccess) break;
-        if (ms < best_ms) {
-          best_ms = ms;
-          best_w = cand[ci];
-        }
-      }
-      cudaGetLastError();
-      if (best_w > 0) install(12, 3, best_w, 1);
+      K1Scratch tmp(n_global, n_local, st);
+      const int best = !tmp.ok ? -1 : autotune_pick(
+          4, [&](int i) { return install(12, 3, cand[i], 1); },
+          [&] { return launch_bellman(h, tmp.v, IPI_MODE_MIN, tmp.policy, tmp.applied, nullptr,
+                                      nullptr, nullptr, st); }, st);
+      if (best >= 0) install(12, 3, cand[best], 1);
       else install(shapes[0][0], shapes[0][1], shapes[0][2], shapes[0][3]);
-      if (e0) cudaEventDestroy(e0);
-      if (e1) cudaEventDestroy(e1);
-      cudaFree(tv);
-      cudaFree(tap);
-      cudaFree(tpol);
     }
   }
   // ---- generic rows: autotune the CTA count (C4: 2 CTAs/SM 0.200 ms, 8 CTAs/SM
@@ -634,37 +663,12 @@ int ipi_mdp_create(const int64_t* row_ptr, const int32_t* col, const double* val
       return true;
     };
     const int cand[5] = {8, 2, 4, 12, 16};
-    double* tv = nullptr;
-    double* tap = nullptr;
-    int32_t* tpol = nullptr;
-    bool ok = cudaMalloc(&tv, sizeof(double) * n_global) == cudaSuccess &&
-              cudaMalloc(&tap, sizeof(double) * n_local) == cudaSuccess &&
-              cudaMalloc(&tpol, sizeof(int32_t) * n_local) == cudaSuccess &&
-              cudaMemsetAsync(tv, 0, sizeof(double) * n_global, st) == cudaSuccess;
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    ok = ok && cudaEventCreate(&e0) == cudaSuccess && cudaEventCreate(&e1) == cudaSuccess;
-    float best_ms = 1e30f;
-    int best_c = -1;
-    for (int ci = 0; ok && ci < 5; ++ci) {
-      if (!install_gen(cand[ci])) continue;
-      if (launch_bellman(h, tv, IPI_MODE_MIN, tpol, tap, nullptr, nullptr, nullptr, st)) break;
-      cudaEventRecord(e0, st);
-      if (launch_bellman(h, tv, IPI_MODE_MIN, tpol, tap, nullptr, nullptr, nullptr, st)) break;
-      cudaEventRecord(e1, st);
-      float ms = 0.f;
-      if (cudaEventSynchronize(e1) != cudaSuccess || cudaEventElapsedTime(&ms, e0, e1) != cudaSuccess) break;
-      if (ms < best_ms) {
-        best_ms = ms;
-        best_c = cand[ci];
-      }
-    }
-    cudaGetLastError();
-    if (best_c > 0) install_gen(best_c);
-    if (e0) cudaEventDestroy(e0);
-    if (e1) cudaEventDestroy(e1);
-    cudaFree(tv);
-    cudaFree(tap);
-    cudaFree(tpol);
+    K1Scratch tmp(n_global, n_local, st);
+    const int best = !tmp.ok ? -1 : autotune_pick(
+        5, [&](int i) { return install_gen(cand[i]); },
+        [&] { return launch_bellman(h, tmp.v, IPI_MODE_MIN, tmp.policy, tmp.applied, nullptr,
+                                    nullptr, nullptr, st); }, st);
+    if (best >= 0) install_gen(cand[best]);
   }
   // ---- flat rows (K <= 4): cp.async ring per warp (bellman.cu) ---------------
   if (p.uniform_rows && p.row_len_max <= 4 && (p.row_len_max % 2) == 0 && n_local > 0) {
@@ -1097,41 +1101,25 @@ int ipi_op_create(const int64_t* rp, const int32_t* col, const double* val, int6
     const int cu[4][3] = {{11, 3, 1}, {12, 3, 3}, {12, 3, 6}, {12, 3, 4}};
     const int cf[3][3] = {{24, 4, 1}, {28, 4, 1}, {16, 4, 1}};
     const int nc = variant == IPI_K3_FLAT ? 3 : 4;
+    cudaStream_t st = (cudaStream_t)stream;
     double* tx = nullptr;
     double* ty = nullptr;
-    cudaStream_t st = (cudaStream_t)stream;
-    bool ok = cudaMalloc(&tx, sizeof(double) * n_global) == cudaSuccess &&
-              cudaMalloc(&ty, sizeof(double) * n_local) == cudaSuccess &&
-              cudaMemsetAsync(tx, 0, sizeof(double) * n_global, st) == cudaSuccess;
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    ok = ok && cudaEventCreate(&e0) == cudaSuccess && cudaEventCreate(&e1) == cudaSuccess;
-    float best_ms = 1e30f;
-    int best = -1;
-    for (int ci = 0; ok && ci < nc; ++ci) {
-      const int* c = variant == IPI_K3_FLAT ? cf[ci] : cu[ci];
-      if (!install(c[0], c[1], c[2])) continue;
-      if (op_launch(op, tx, nullptr, 1, ty, st)) break;
-      cudaEventRecord(e0, st);
-      if (op_launch(op, tx, nullptr, 1, ty, st)) break;
-      cudaEventRecord(e1, st);
-      float ms = 0.f;
-      if (cudaEventSynchronize(e1) != cudaSuccess || cudaEventElapsedTime(&ms, e0, e1) != cudaSuccess) break;
-      if (ms < best_ms) {
-        best_ms = ms;
-        best = ci;
-      }
-    }
-    cudaGetLastError();
+    const bool ok = cudaMalloc(&tx, sizeof(double) * n_global) == cudaSuccess &&
+                    cudaMalloc(&ty, sizeof(double) * n_local) == cudaSuccess &&
+                    cudaMemsetAsync(tx, 0, sizeof(double) * n_global, st) == cudaSuccess;
+    auto shape = [&](int i) { return variant == IPI_K3_FLAT ? cf[i] : cu[i]; };
+    const int best = !ok ? -1 : autotune_pick(
+        nc, [&](int i) { const int* c = shape(i); return install(c[0], c[1], c[2]); },
+        [&] { return op_launch(op, tx, nullptr, 1, ty, st); }, st);
     if (best >= 0) {
-      const int* c = variant == IPI_K3_FLAT ? cf[best] : cu[best];
+      const int* c = shape(best);
       install(c[0], c[1], c[2]);
     } else {
       install(shapes[0][0], shapes[0][1], shapes[0][2]);
     }
-    if (e0) cudaEventDestroy(e0);
-    if (e1) cudaEventDestroy(e1);
     cudaFree(tx);
     cudaFree(ty);
+    cudaGetLastError();
   }
   *out = op;
   return IPI_OK;
