@@ -133,6 +133,39 @@ __global__ void __launch_bounds__(256) copy_rows(const int64_t* __restrict__ rp,
   }
 }
 
+// Uniform rows (length K = 4*G, 16-byte aligned arrays; C2/C5 K = 64, C3
+// K = 4): the selected row of state s starts at (s*m + pi[s])*K, so no row
+// pointers are read (for C3's 48-byte rows the random row-pointer pairs were
+// most of the DRAM traffic), and each lane moves 4 entries with 16-byte loads
+// and stores; P_pi rows land at s*K.
+template <int G>
+__global__ void __launch_bounds__(256) copy_rows_uniform(const int32_t* __restrict__ col,
+                                                         const double* __restrict__ val,
+                                                         const double* __restrict__ cost,
+                                                         const int32_t* __restrict__ pi, int64_t n,
+                                                         int m, int32_t* __restrict__ col_pi,
+                                                         double* __restrict__ val_pi,
+                                                         double* __restrict__ g_pi) {
+  constexpr int K = 4 * G, GPW = 32 / G;
+  const uint64_t pol = policy_evict_first();
+  const int lane = threadIdx.x & 31;
+  const int grp = lane / G, gl = lane % G;
+  const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwt = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t s0 = wg * GPW; s0 < n; s0 += nwt * GPW) {
+    const int64_t s = s0 + grp;
+    if (s >= n) continue;
+    const int64_t r = s * (int64_t)m + __ldg(pi + s);
+    const int64_t src = r * K + 4 * gl, dst = s * K + 4 * gl;
+    const double2 v0 = ld_stream_v2(val + src, pol), v1 = ld_stream_v2(val + src + 2, pol);
+    const int2 c0 = ld_stream_v2(col + src, pol), c1 = ld_stream_v2(col + src + 2, pol);
+    reinterpret_cast<double2*>(val_pi + dst)[0] = v0;
+    reinterpret_cast<double2*>(val_pi + dst)[1] = v1;
+    reinterpret_cast<int4*>(col_pi + dst)[0] = make_int4(c0.x, c0.y, c1.x, c1.y);
+    if (g_pi && gl == 0) g_pi[s] = __ldg(cost + r);
+  }
+}
+
 // warp per row of P_pi: the lane holding column s supplies the diagonal entry;
 // absent diagonal -> 0 -> inv_diag = 1 (CsrMatrix.diagonal, sparse.py:102-109)
 __global__ void jacobi_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
@@ -226,6 +259,29 @@ int gather_policy(ipi_mdp* h, const int32_t* policy, const int32_t* /*len_pi*/, 
   if (rc) return rc;
   const int64_t n = h->n_local;
   if (n == 0) return IPI_OK;
+  const int K = h->plan.row_len_max;
+  if (h->plan.uniform_rows && K % 4 == 0 && K >= 4 && K <= 128 && ((K / 4) & (K / 4 - 1)) == 0 &&
+      (uintptr_t)h->val % 16 == 0 && (uintptr_t)h->col % 16 == 0 && (uintptr_t)val_pi % 16 == 0 &&
+      (uintptr_t)col_pi % 16 == 0) {
+    const int Gu = K / 4, GPWu = 32 / Gu;
+    int64_t ub = ((n + GPWu - 1) / GPWu + 7) / 8;
+    if (ub > (int64_t)h->num_sms * 32) ub = (int64_t)h->num_sms * 32;
+    if (ub < 1) ub = 1;
+#define IPI_UCOPY(GG)                                                                            \
+  copy_rows_uniform<GG><<<(int)ub, 256, 0, st>>>(h->col, h->val, h->cost, policy, n, h->m, col_pi, \
+                                                 val_pi, g_pi)
+    switch (Gu) {
+      case 1: IPI_UCOPY(1); break;
+      case 2: IPI_UCOPY(2); break;
+      case 4: IPI_UCOPY(4); break;
+      case 8: IPI_UCOPY(8); break;
+      case 16: IPI_UCOPY(16); break;
+      default: IPI_UCOPY(32); break;
+    }
+#undef IPI_UCOPY
+    IPI_LAUNCH_CHECK();
+    return IPI_OK;
+  }
   const int G = h->plan.lanes_per_row;
   const int GPW = 32 / G;
   int64_t blocks = ((n + GPW - 1) / GPW + 7) / 8;
