@@ -4,6 +4,7 @@
 // thread), and per-warp cp.async rings into shared memory (K1's scheme).
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o read_bw read_bw.cu
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 template <int U>
@@ -56,8 +57,8 @@ __global__ void __launch_bounds__(1024, 1) rd_ring(const char* __restrict__ p, s
   if (acc == 1.2345) out[0] = acc;
 }
 
-int main() {
-  const size_t bytes = 16ull << 30;
+int main(int argc, char** argv) {
+  const size_t bytes = argc > 1 ? (size_t)(atof(argv[1]) * (1ull << 30)) / 65536 * 65536 : (16ull << 30);
   char* p;
   double* out;
   if (cudaMalloc(&p, bytes) != cudaSuccess) { printf("alloc failed\n"); return 1; }
