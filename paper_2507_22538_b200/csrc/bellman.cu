@@ -974,7 +974,8 @@ static void uring_go(const K1Args& a, bool win, int blocks, int smem, int win_by
 #define IPI_URING_SHAPES(MACRO)                                                           \
   MACRO(64, 12, 3, 1) MACRO(64, 10, 3, 1) MACRO(64, 11, 3, 1) MACRO(64, 10, 4, 1)        \
   MACRO(64, 12, 4, 1) MACRO(64, 11, 4, 1) MACRO(64, 11, 4, 2) MACRO(64, 16, 4, 2)        \
-  MACRO(64, 16, 3, 1) MACRO(64, 14, 4, 2) MACRO(64, 12, 5, 2)                            \
+  MACRO(64, 16, 3, 1) MACRO(64, 14, 4, 2) MACRO(64, 12, 5, 2) MACRO(64, 14, 3, 1)        \
+  MACRO(64, 15, 3, 1)                                                                    \
   MACRO(64, 8, 4, 1) MACRO(64, 8, 3, 1) MACRO(64, 10, 4, 2) MACRO(64, 8, 4, 2)           \
   MACRO(64, 8, 5, 2) MACRO(64, 12, 4, 2) MACRO(64, 6, 6, 2)
 
