@@ -135,22 +135,26 @@ def inner_spmv_roofline(shard, ctx, pol, v_full, n, torch, reps=20):
     """K3 (the policy-evaluation SpMV, J_pi = I - gamma P_pi applied to the
     all-gathered vector) on this rank's rows of P_pi for the greedy policy of
     the bench's V: algorithmic bytes nnz_pi*12 + 8 n_global [x, once] +
-    8 n_local [y] per launch over the CUDA-event launch time (P_pi is 805 MB
-    at C2, 6x L2: no flush needed)."""
+    8 n_local [y] per launch over the average launch time of back-to-back
+    launches measured with CUDA events (P_pi is 805 MB at C2, 6x L2: no flush
+    needed)."""
     from paper_2507_22538_b200.parallel import ShardOps
     ops = ShardOps(shard, ctx)
     op, _ = ops.gather_policy(pol, split=False)  # the K3 kernel alone over the gathered x
     y = torch.empty(shard.n_local, dtype=torch.float64, device=v_full.device)
     for _ in range(3):
         op.apply(v_full, out=y)
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(reps)]
-    for a, b in evs:
-        a.record()
-        op.apply(v_full, out=y)
-        b.record()
+    # one event pair around `reps` back-to-back launches: the average launch
+    # duration in a busy stream (per-launch events would also time the host's
+    # enqueue of each launch whenever the GPU drains the queue first)
     torch.cuda.synchronize()
-    ms = statistics.median(a.elapsed_time(b) for a, b in evs)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        op.apply(v_full, out=y)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / reps
     plan = op.plan()
     alg = plan["nnz"] * 12 + 8 * n + 8 * shard.n_local + (8 * (shard.n_local + 1) if plan["variant"] == 0 else 0)
     return ms, alg, plan
