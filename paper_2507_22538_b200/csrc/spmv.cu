@@ -35,11 +35,13 @@ __global__ void __launch_bounds__(256) spmv_kernel(const int64_t* __restrict__ r
     double acc = 0.0;
     if (r < rows) {
       const int64_t p0 = __ldg(rp + r), p1 = __ldg(rp + r + 1);
-      for (int64_t p = p0 + gl; p < p1; p += 4 * G) {
-        double vv[4];
-        int cc[4];
+      // long rows (G = 32: C4's ~570-entry P_pi rows): 8 loads in flight per lane
+      constexpr int U = G == 32 ? 8 : 4;
+      for (int64_t p = p0 + gl; p < p1; p += U * G) {
+        double vv[U];
+        int cc[U];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < U; ++u) {
           const int64_t q = p + (int64_t)u * G;
           if (q < p1) {
             vv[u] = ld_stream(val + q, pol);
@@ -49,11 +51,11 @@ __global__ void __launch_bounds__(256) spmv_kernel(const int64_t* __restrict__ r
             cc[u] = -1;
           }
         }
-        double xx[4];
+        double xx[U];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) xx[u] = cc[u] >= 0 ? __ldg(x + cc[u]) : 0.0;
+        for (int u = 0; u < U; ++u) xx[u] = cc[u] >= 0 ? __ldg(x + cc[u]) : 0.0;
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < U; ++u)
           if (cc[u] >= 0) acc = add_rn(acc, mul_rn(vv[u], xx[u]));
       }
     }
