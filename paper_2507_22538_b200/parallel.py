@@ -306,8 +306,12 @@ class ShardVectorOps:
         w.sub_(h * v)
         return h, self.dot_partial(v_next if v_next is not None else w, w)
 
+    def gather_sum(self, part: torch.Tensor) -> torch.Tensor:
+        """Per-rank shares (k,) -> their rank-ordered sum (k,), on every rank."""
+        return rank_ordered_sum(part.reshape(-1), self.ctx.world)
+
     def to_host(self, scalars) -> list[float]:
-        return torch.cat([t.reshape(1) for t in scalars]).cpu().tolist()
+        return torch.cat([t.reshape(-1) for t in scalars]).cpu().tolist()
 
 
 class ShardOps(ShardVectorOps):
@@ -404,8 +408,15 @@ def host_richardson(ops, P, b, theta0, eff, max_it, scale):
     return theta, it, rn, False
 
 
-def host_gmres(ops, P, b, theta0, eff, max_it):
-    """Restarted GMRES(30) with MGS and Givens (inner.py:229-292) on sharded vectors."""
+def host_gmres(ops, P, b, theta0, eff, max_it, ortho: str = "mgs"):
+    """Restarted GMRES(30) with Givens (inner.py:229-292) on sharded vectors.
+
+    ``ortho="mgs"`` restates the reference's modified Gram-Schmidt: j+2
+    cross-rank reductions per Arnoldi step.  ``ortho="cgs2"`` orthogonalises
+    with two classical Gram-Schmidt sweeps (batched dots and one fused update
+    per sweep): three reductions per step whatever j — the option SURVEY §8(e)
+    names for multi-GPU runs, where each reduction is an all-gather.  Same
+    stopping logic; Hessenberg entries differ from MGS at rounding level."""
     x = theta0.clone() if hasattr(theta0, "clone") else theta0.copy()
     it = 0
     r = ops.apply(P, x, b)
@@ -416,7 +427,12 @@ def host_gmres(ops, P, b, theta0, eff, max_it):
         beta = math.sqrt(ops.dot(r, r))
         if beta == 0.0 or not math.isfinite(beta):
             break
-        V = [r / beta]
+        if ortho == "cgs2":
+            Vm = torch.empty((R + 1,) + tuple(r.shape), dtype=r.dtype, device=r.device)
+            Vm[0] = r / beta
+            V = [Vm[0]]
+        else:
+            V = [r / beta]
         H = [[0.0] * R for _ in range(R + 1)]
         cs = [0.0] * R
         sn = [0.0] * R
@@ -426,14 +442,24 @@ def host_gmres(ops, P, b, theta0, eff, max_it):
         while j < R and it < max_it:
             w = ops.apply(P, V[j])
             it += 1
-            # MGS with the scalars on the device: one kernel + one all-gather of
-            # the R shares per pass, one host sync per step (the H column)
-            part = ops.dot_partial(V[0], w)
-            hs = []
-            for l in range(j + 1):
-                h, part = ops.mgs_pass(ops.gather_partials(part), w, V[l], V[l + 1] if l < j else None)
-                hs.append(h)
-            vals = ops.to_host(hs + [ops.ordered_sum(ops.gather_partials(part))])
+            if ortho == "cgs2":
+                # two classical sweeps: batched shares <V_l, w>, one reduction,
+                # one update w -= V^T c; then ||w||: three reductions per step
+                Vj = Vm[: j + 1]
+                c1 = ops.gather_sum(torch.mv(Vj, w))
+                w = w - torch.mv(Vj.t(), c1)
+                c2 = ops.gather_sum(torch.mv(Vj, w))
+                w = w - torch.mv(Vj.t(), c2)
+                vals = ops.to_host([c1 + c2, ops.gather_sum(torch.dot(w, w).reshape(1))])
+            else:
+                # MGS with the scalars on the device: one kernel + one all-gather of
+                # the R shares per pass, one host sync per step (the H column)
+                part = ops.dot_partial(V[0], w)
+                hs = []
+                for l in range(j + 1):
+                    h, part = ops.mgs_pass(ops.gather_partials(part), w, V[l], V[l + 1] if l < j else None)
+                    hs.append(h)
+                vals = ops.to_host(hs + [ops.ordered_sum(ops.gather_partials(part))])
             for l in range(j + 1):
                 H[l][j] = vals[l]
             hnorm = math.sqrt(vals[j + 1])
@@ -453,7 +479,11 @@ def host_gmres(ops, P, b, theta0, eff, max_it):
             j += 1
             if abs(g[j]) <= est_target or hnorm == 0.0:
                 break
-            V.append(w / hnorm)
+            if ortho == "cgs2":
+                torch.div(w, hnorm, out=Vm[j])
+                V.append(Vm[j])
+            else:
+                V.append(w / hnorm)
         if j == 0:
             break
         y = [0.0] * j
@@ -473,14 +503,20 @@ def host_gmres(ops, P, b, theta0, eff, max_it):
     return x, it, rn, False
 
 
-def solve_sharded(ops, opts, n_global: int, v0_local=None):
+def solve_sharded(ops, opts, n_global: int, v0_local=None, ortho: str | None = None):
     """Algorithm 1 (driver.py:109-209) across ranks; returns a SolveResult whose
-    values/policy are the gathered full vectors (on every rank)."""
+    values/policy are the gathered full vectors (on every rank).  GMRES
+    orthogonalisation: ``ortho`` or IPI_SHARD_ORTHO, default MGS on one rank
+    (the reference's arithmetic) and CGS2 across ranks (3 reductions per step)."""
     import time
     from .driver import STALL_WINDOW, SolveResult, SolveStatus
     from .inner import InnerSolver
     if opts.inner not in (InnerSolver.GMRES, InnerSolver.RICHARDSON):
         raise NotImplementedError("the sharded path runs GMRES and Richardson inner solves")
+    if ortho is None:
+        ortho = os.environ.get("IPI_SHARD_ORTHO", "cgs2" if ops.ctx.world > 1 else "mgs")
+    if ortho not in ("mgs", "cgs2"):
+        raise ValueError(f"unknown orthogonalisation {ortho!r}; expected 'mgs' or 'cgs2'")
     t0 = time.perf_counter()
     v = v0_local
     if v is None:
@@ -514,7 +550,7 @@ def solve_sharded(ops, opts, n_global: int, v0_local=None):
         bn = math.sqrt(ops.dot(g, g))
         eff = max(target, 1e-14 * max(1.0, bn))          # inner.py:189
         if opts.inner is InnerSolver.GMRES:
-            v, its, _, _ = host_gmres(ops, P, g, v, eff, cap)
+            v, its, _, _ = host_gmres(ops, P, g, v, eff, cap, ortho=ortho)
         else:
             v, its, _, _ = host_richardson(ops, P, g, v, eff, cap, opts.richardson_scale)
         inner_total += its

@@ -32,10 +32,10 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, n, kind, q, overlap="1"):
+def _worker(rank, world, port, n, kind, q, overlap="1", ortho="cgs2"):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
-                      WORLD_SIZE=str(world), IPI_SHARD_OVERLAP=overlap)
+                      WORLD_SIZE=str(world), IPI_SHARD_OVERLAP=overlap, IPI_SHARD_ORTHO=ortho)
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -56,16 +56,19 @@ def _worker(rank, world, port, n, kind, q, overlap="1"):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kind,n,overlap", [("gmres", 8191, "1"), ("richardson", 8191, "1"),
-                                            ("gmres", 8192, "1"), ("gmres", 8192, "0")])
-def test_two_ranks_on_device_match_persistent_solver(kind, n, overlap):
+@pytest.mark.parametrize("kind,n,overlap,ortho", [("gmres", 8191, "1", "cgs2"),
+                                                  ("richardson", 8191, "1", "cgs2"),
+                                                  ("gmres", 8192, "1", "cgs2"),
+                                                  ("gmres", 8192, "0", "mgs")])
+def test_two_ranks_on_device_match_persistent_solver(kind, n, overlap, ortho):
     """n = 8191: unequal blocks (blocking gather); n = 8192: equal blocks, the
     split operator's all-gather runs async (overlap) or the unsplit path."""
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, n, kind, q, overlap)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, n, kind, q, overlap, ortho))
+             for r in range(2)]
     for p in procs:
         p.start()
     out = sorted(q.get(timeout=600) for _ in procs)

@@ -351,7 +351,7 @@ class _CpuShardOps(ShardVectorOps):
         return b_local - y if b_local is not None else y
 
 
-def _sharded_solve_worker(rank, world, port, kind, q):
+def _sharded_solve_worker(rank, world, port, kind, q, ortho=None):
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -363,21 +363,22 @@ def _sharded_solve_worker(rank, world, port, kind, q):
         ops = _CpuShardOps(arrays, 0.95, ctx)
         lo, hi = ctx.block
         res = solve_sharded(ops, ipi.SolveOptions(inner=ipi.InnerSolver.from_name(kind)), 61,
-                            torch.zeros(hi - lo, dtype=torch.float64))
+                            torch.zeros(hi - lo, dtype=torch.float64), ortho=ortho)
         q.put((rank, res.status.value, res.outer_iterations, res.values.tolist(),
                res.policy.tolist(), res.residual_history))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kind", ["gmres", "richardson"])
-def test_sharded_ipi_gloo_world2_matches_oracle(kind):
+@pytest.mark.parametrize("kind,ortho", [("gmres", "mgs"), ("gmres", "cgs2"), ("richardson", None)])
+def test_sharded_ipi_gloo_world2_matches_oracle(kind, ortho):
     import torch.multiprocessing as mp
     from oracle import mdp_oracle as orc
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_sharded_solve_worker, args=(r, 2, port, kind, q)) for r in range(2)]
+    procs = [ctx.Process(target=_sharded_solve_worker, args=(r, 2, port, kind, q, ortho))
+             for r in range(2)]
     for p in procs:
         p.start()
     out = sorted(q.get(timeout=180) for _ in procs)
