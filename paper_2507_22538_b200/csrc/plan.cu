@@ -373,10 +373,12 @@ static int plan_uniform_ring(PlanCtx& c) {
     // the fastest.  IPI_K1_AUTOTUNE=0 keeps the static first choice.
     const char* at = getenv("IPI_K1_AUTOTUNE");
     if (done && nshape > 1 && !(at && at[0] == '0') && nnz >= (1ll << 28)) {
-      const int cand[4] = {8, 4, 6, 2};
+      // the rate also varies between processes on one board (fresh physical
+      // placement of the CSR), so a broader set of wave counts is timed
+      const int cand[8] = {8, 6, 4, 2, 10, 12, 3, 5};
       K1Scratch tmp(n_global, n_local, st);
       const int best = !tmp.ok ? -1 : autotune_pick(
-          4, [&](int i) { return install(12, 3, cand[i], 1); },
+          8, [&](int i) { return install(12, 3, cand[i], 1); },
           [&] { return launch_bellman(h, tmp.v, IPI_MODE_MIN, tmp.policy, tmp.applied, nullptr,
                                       nullptr, nullptr, st); }, st);
       if (best >= 0) install(12, 3, cand[best], 1);
