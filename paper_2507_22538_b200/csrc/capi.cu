@@ -606,9 +606,10 @@ int ipi_op_create(const int64_t* rp, const int32_t* col, const double* val, int6
   // candidate (~2 ms once per operator).  IPI_K3_AUTOTUNE=0 disables.
   const char* at = getenv("IPI_K3_AUTOTUNE");
   if (done && nshape > 1 && !(at && at[0] == '0') && op->nnz >= (1ll << 25)) {
-    const int cu[4][3] = {{11, 3, 1}, {12, 3, 3}, {12, 3, 6}, {12, 3, 4}};
-    const int cf[3][3] = {{24, 4, 1}, {28, 4, 1}, {16, 4, 1}};
-    const int nc = variant == IPI_K3_FLAT ? 3 : 4;
+    const int cu[8][3] = {{11, 3, 1}, {12, 3, 3}, {12, 3, 6}, {12, 3, 4},
+                          {12, 3, 2}, {10, 3, 1}, {12, 3, 8}, {11, 3, 2}};
+    const int cf[4][3] = {{24, 4, 1}, {28, 4, 1}, {16, 4, 1}, {16, 4, 2}};
+    const int nc = variant == IPI_K3_FLAT ? 4 : 8;
     cudaStream_t st = (cudaStream_t)stream;
     double* tx = nullptr;
     double* ty = nullptr;
