@@ -221,6 +221,9 @@ int ipi_apply_J_shard(const int64_t* rp_pi, const int32_t* col_pi, const double*
 int ipi_op_create(const int64_t* rp, const int32_t* col, const double* val, int64_t n_local,
                   int64_t n_global, int64_t state0, double gamma, void* stream, ipi_op** out);
 void ipi_op_destroy(ipi_op* op);
+/* Diagnostics: per-CTA (smid, start ns, end ns) of the ring kernels' later launches
+ * (enable != 0 starts recording; enable == 0 copies up to cap words to host and stops). */
+int ipi_op_trace(ipi_op* op, int32_t enable, uint64_t* out, int32_t cap);
 int ipi_op_get_plan(const ipi_op* op, ipi_op_plan* out);
 /* apply (sparse.py:294-295): y = x - gamma*(P x) (b == NULL) or y = b - (x - gamma*(P x))
  * (inner.py:220/232/276); x_full holds all n_global entries, y and b n_local. */

@@ -99,6 +99,7 @@ _SIGS = {
     "ipi_apply_J_shard": (C.c_int, [_p, _p, _p, _i64, _i64, _f64, _p, _p, _p, _p]),
     "ipi_op_create": (C.c_int, [_p, _p, _p, _i64, _i64, _i64, _f64, _p, C.POINTER(_p)]),
     "ipi_op_destroy": (None, [_p]),
+    "ipi_op_trace": (C.c_int, [_p, _i32, _p, _i32]),
     "ipi_op_get_plan": (C.c_int, [_p, C.POINTER(OpPlan)]),
     "ipi_op_apply": (C.c_int, [_p, _p, _p, _p, _p]),
     "ipi_op_spmv": (C.c_int, [_p, _p, _p, _p]),

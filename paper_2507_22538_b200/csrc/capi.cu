@@ -634,7 +634,28 @@ int ipi_op_create(const int64_t* rp, const int32_t* col, const double* val, int6
   return IPI_OK;
 }
 
-void ipi_op_destroy(ipi_op* op) { delete op; }
+void ipi_op_destroy(ipi_op* op) {
+  if (op) cudaFree(op->trace);
+  delete op;
+}
+
+int ipi_op_trace(ipi_op* op, int32_t enable, uint64_t* out, int32_t cap) {
+  if (!op) return fail(IPI_EVALIDATION, "null operator");
+  const int64_t words = 3 * (int64_t)std::max(op->blocks, 1);
+  if (enable) {
+    if (!op->trace) IPI_CUDA_TRY(cudaMalloc(&op->trace, sizeof(uint64_t) * words));
+    IPI_CUDA_TRY(cudaMemset(op->trace, 0, sizeof(uint64_t) * words));
+    return IPI_OK;
+  }
+  if (op->trace && out && cap > 0) {
+    IPI_CUDA_TRY(cudaDeviceSynchronize());
+    IPI_CUDA_TRY(cudaMemcpy(out, op->trace, sizeof(uint64_t) * std::min<int64_t>(words, cap),
+                            cudaMemcpyDeviceToHost));
+  }
+  cudaFree(op->trace);
+  op->trace = nullptr;
+  return IPI_OK;
+}
 
 int ipi_op_get_plan(const ipi_op* op, ipi_op_plan* out) {
   if (!op || !out) return fail(IPI_EVALIDATION, "null operator");

@@ -67,6 +67,7 @@ struct ipi_op {
   int win_bytes = 0;  // window bytes in front of the rings
   int blocks = 0, warps = 0, stages = 0, smem = 0;
   int pf = 0;         // uniform ring: L2 prefetch distance (steps)
+  unsigned long long* trace = nullptr;  // diagnostics (ipi_op_trace)
 };
 
 namespace ipi {

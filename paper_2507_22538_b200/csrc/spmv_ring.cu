@@ -43,7 +43,28 @@ struct K3Args {
   double* y;
   int halo;
   int pf;  // uniform ring: L2 bulk prefetch distance in steps beyond the ring (0 = off)
+  unsigned long long* trace;  // diagnostics: per-CTA (smid, start ns, end ns) or nullptr
 };
+
+__device__ __forceinline__ unsigned long long k3_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void k3_trace_begin(const K3Args& a) {
+  if (a.trace && threadIdx.x == 0) {
+    unsigned r;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+    a.trace[3 * blockIdx.x] = r;
+    a.trace[3 * blockIdx.x + 1] = k3_ns();
+  }
+}
+__device__ __forceinline__ void k3_trace_end(const K3Args& a) {
+  if (a.trace) {
+    __syncthreads();
+    if (threadIdx.x == 0) a.trace[3 * blockIdx.x + 2] = k3_ns();
+  }
+}
 
 template <int EPI>
 __device__ __forceinline__ double k3_epi(double px, double xd, double bb, double gamma) {
@@ -105,6 +126,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k3_uring(K3Args a, int win_bytes) 
   using L = K3URing<K>;
   constexpr bool NEED_B = EPI >= 2, NEED_XD = EPI == 1 || EPI == 2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  k3_trace_begin(a);
   double* win = reinterpret_cast<double*>(smem_raw);
   const int64_t r_lo = k3_split(a.rows, blockIdx.x, gridDim.x, 4);
   const int64_t r_hi = k3_split(a.rows, blockIdx.x + 1, gridDim.x, 4);
@@ -239,6 +261,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k3_uring(K3Args a, int win_bytes) 
     }
   }
   cp_async_wait<0>();
+  k3_trace_end(a);
 }
 
 // ---------------------------------------------------------------------------
@@ -263,6 +286,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k3_flat(K3Args a, int win_bytes) {
   using L = K3Flat<K>;
   constexpr bool NEED_B = EPI >= 2, NEED_XD = EPI == 1 || EPI == 2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  k3_trace_begin(a);
   double* win = reinterpret_cast<double*>(smem_raw);
   const int64_t r_lo = k3_split(a.rows, blockIdx.x, gridDim.x, 32);
   const int64_t r_hi = k3_split(a.rows, blockIdx.x + 1, gridDim.x, 32);
@@ -376,6 +400,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k3_flat(K3Args a, int win_bytes) {
     }
   }
   cp_async_wait<0>();
+  k3_trace_end(a);
 }
 
 // ---------------------------------------------------------------------------
@@ -460,7 +485,7 @@ int op_launch(const ipi_op* op, const double* x_full, const double* b, int epi, 
     return launch_spmv(op->rp, op->col, op->val, op->n_local, x_full, b, op->gamma, epi, y,
                        op->lanes, st, op->state0, y_partial);
   K3Args a{op->col, op->val, op->n_local, op->state0, op->n_global, x_full, b, op->gamma, y, op->halo,
-            op->pf};
+            op->pf, op->trace};
   bool ok = false;
   switch (epi) {
     case 0: ok = k3_launch_epi<0>(op, a, st); break;
