@@ -253,6 +253,11 @@ int ipi_dot_partial(const double* a, const double* b, int64_t n, double* out, vo
 int ipi_mgs_pass(const double* partials, int32_t R, double* h_out, double* w, const double* v,
                  const double* v_next, int64_t n, double* out_partial, void* stream);
 
+/* Min / max column index of a CSR block's nnz entries (the V range a
+ * row-sharded rank's rows read; parallel.py uses it to pick a halo exchange
+ * instead of the all-gather when column locality allows).  One sync. */
+int ipi_col_range(const int32_t* col, int64_t nnz, int64_t* cmin, int64_t* cmax, void* stream);
+
 /* ---- K4: policy evaluation (inner.py:163-292) ------------------------- */
 /* Jacobi preconditioner of I - gamma P_pi: inv_diag[s] = 1/(1 - gamma P_pi[s,s])
  * (build_preconditioner JACOBI, inner.py:115-118). */

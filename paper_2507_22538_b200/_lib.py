@@ -105,6 +105,7 @@ _SIGS = {
     "ipi_op_spmv": (C.c_int, [_p, _p, _p, _p]),
     "ipi_op_apply_partial": (C.c_int, [_p, _p, _p, _p, _p, _p]),
     "ipi_csr_split_local": (C.c_int, [_p, _p, _p, _i64, _i64, _i64, _p, _p, _p, _p, _p, _p, _p]),
+    "ipi_col_range": (C.c_int, [_p, _i64, C.POINTER(_i64), C.POINTER(_i64), _p]),
     "ipi_dot_partial": (C.c_int, [_p, _p, _i64, _p, _p]),
     "ipi_mgs_pass": (C.c_int, [_p, _i32, _p, _p, _p, _p, _i64, _p, _p]),
     "ipi_jacobi_inv_diag": (C.c_int, [_p, _p, _p, _i64, _f64, _p, _p]),

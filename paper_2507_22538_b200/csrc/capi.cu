@@ -189,6 +189,25 @@ __global__ void uniform_rp_check_kernel(const int64_t* rp, int64_t rows, int64_t
     if (rp[r] != r * K) atomicAdd(bad, 1ull);
 }
 
+// min / max column index of a CSR block (the V range a row-sharded rank reads)
+__global__ void col_range_kernel(const int32_t* __restrict__ col, int64_t nnz, int* out) {
+  int lo = INT32_MAX, hi = INT32_MIN;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnz;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = col[i];
+    lo = c < lo ? c : lo;
+    hi = c > hi ? c : hi;
+  }
+  for (int off = 16; off; off >>= 1) {
+    lo = min(lo, __shfl_xor_sync(kFull, lo, off));
+    hi = max(hi, __shfl_xor_sync(kFull, hi, off));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(out, lo);
+    atomicMax(out + 1, hi);
+  }
+}
+
 __global__ void row_sum_kernel(const int64_t* rp, const double* val, int64_t r, double* out) {
   // same summation layout as validate_rows_kernel for one row
   const int lane = threadIdx.x;
@@ -708,6 +727,31 @@ int ipi_csr_split_local(const int64_t* rp, const int32_t* col, const double* val
     return fail(IPI_EVALIDATION, "split: pass 2 needs all output arrays");
   return split_local_remote(rp, col, val, rows, (int32_t)lo, (int32_t)hi, rp_loc, col_loc, val_loc,
                             rp_rem, col_rem, val_rem, (cudaStream_t)stream);
+}
+
+int ipi_col_range(const int32_t* col, int64_t nnz, int64_t* cmin, int64_t* cmax, void* stream) {
+  if (!cmin || !cmax) return fail(IPI_EVALIDATION, "null output");
+  *cmin = 0;
+  *cmax = -1;
+  if (nnz <= 0) return IPI_OK;
+  if (!col) return fail(IPI_EVALIDATION, "null columns");
+  cudaStream_t st = (cudaStream_t)stream;
+  int* d = nullptr;
+  IPI_CUDA_TRY(cudaMalloc(&d, 2 * sizeof(int)));
+  const int init[2] = {INT32_MAX, INT32_MIN};
+  cudaMemcpyAsync(d, init, sizeof(init), cudaMemcpyHostToDevice, st);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  col_range_kernel<<<grid_for(nnz, 256, sms), 256, 0, st>>>(col, nnz, d);
+  int h[2];
+  cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, st);
+  const cudaError_t e = cudaStreamSynchronize(st);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(IPI_ECUDA, std::string("col range: ") + cudaGetErrorString(e));
+  *cmin = h[0];
+  *cmax = h[1];
+  return IPI_OK;
 }
 
 int ipi_jacobi_inv_diag(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi,

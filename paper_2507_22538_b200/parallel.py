@@ -133,6 +133,88 @@ def allgather_blocks_async(local: torch.Tensor, full: torch.Tensor, partition: P
                            async_op=True)
 
 
+class _Staged:
+    """Waitable for gloo P2P on device tensors: receives land in host buffers
+    and are copied into place after the waits."""
+
+    def __init__(self, works, copies):
+        self.works, self.copies = works, copies
+
+    def wait(self):
+        for w in self.works:
+            w.wait()
+        for dst, src in self.copies:
+            dst.copy_(src)
+
+
+class HaloExchange:
+    """Point-to-point V exchange for row blocks whose columns stay near the
+    block (north star (5): "or by halo exchange when column locality allows").
+
+    Every rank publishes the global column range its rows read
+    (``ipi_col_range``); rank r then receives from each rank q the part of q's
+    block inside r's range and sends q the part of its own block inside q's
+    range.  Enabled when every rank's range spans at most ``frac`` of the
+    states (``IPI_HALO_FRAC``, default 0.5); otherwise the all-gather is the
+    cheaper exchange (C2 / C5: 10% uniform columns make every range full).
+    Entries of ``full`` outside the rank's range are never read by its kernels."""
+
+    def __init__(self, partition: Partition, rank: int, world: int, need: tuple[int, int],
+                 n_global: int, device):
+        import torch.distributed as dist
+        self.partition, self.rank, self.world = partition, rank, world
+        mine = torch.tensor([int(need[0]), int(need[1])], dtype=torch.int64, device=device)
+        if world > 1 and dist.is_available() and dist.is_initialized():
+            allr = torch.empty((world, 2), dtype=torch.int64, device=device)
+            if _nccl():
+                dist.all_gather_into_tensor(allr, mine)
+            else:
+                dist.all_gather(list(allr.unbind(0)), mine)
+            self.ranges = [tuple(r) for r in allr.cpu().tolist()]
+        else:
+            self.ranges = [(int(need[0]), int(need[1]))]
+        frac = float(os.environ.get("IPI_HALO_FRAC", "0.5"))
+        widest = max(max(0, hi - lo + 1) for lo, hi in self.ranges)
+        self.enabled = world > 1 and widest <= frac * n_global
+        lo_me, hi_me = partition.block(rank)
+        self.lo, self.hi = lo_me, hi_me
+        self.recv, self.send = [], []  # (peer, a, b): global slice [a, b)
+        for q in range(world if self.enabled else 0):
+            if q == rank:
+                continue
+            lq, hq = partition.block(q)
+            nlo, nhi = self.ranges[rank]
+            a, b = max(lq, nlo), min(hq, nhi + 1)
+            if a < b:
+                self.recv.append((q, a, b))
+            qlo, qhi = self.ranges[q]
+            a, b = max(lo_me, qlo), min(hi_me, qhi + 1)
+            if a < b:
+                self.send.append((q, a, b))
+
+    def bytes_received(self) -> int:
+        return 8 * sum(b - a for _, a, b in self.recv)
+
+    def exchange_async(self, local: torch.Tensor, full: torch.Tensor):
+        import torch.distributed as dist
+        full[self.lo:self.hi].copy_(local)
+        if _nccl():
+            ops = [dist.P2POp(dist.isend, local[a - self.lo:b - self.lo].contiguous(), q)
+                   for q, a, b in self.send]
+            ops += [dist.P2POp(dist.irecv, full[a:b], q) for q, a, b in self.recv]
+            works = dist.batch_isend_irecv(ops) if ops else []
+            return _Staged(works, [])
+        # gloo: host-staged point-to-point
+        works, copies = [], []
+        for q, a, b in self.send:
+            works.append(dist.isend(local[a - self.lo:b - self.lo].detach().cpu().contiguous(), q))
+        for q, a, b in self.recv:
+            buf = torch.empty(b - a, dtype=full.dtype)
+            works.append(dist.irecv(buf, q))
+            copies.append((full[a:b], buf))
+        return _Staged(works, copies)
+
+
 class SplitShardOperator:
     """J_pi on a rank's rows with the V exchange overlapped (north star (5)):
     the rank's P_pi rows are split into local columns (its own state block,
@@ -174,8 +256,9 @@ class SplitShardOperator:
                 "local": self.local.plan(), "remote": self.remote.plan()}
 
     def apply_overlapped(self, x_local: torch.Tensor, full: torch.Tensor, partition: Partition,
-                         b: torch.Tensor | None = None) -> torch.Tensor:
-        work = allgather_blocks_async(x_local, full, partition)
+                         b: torch.Tensor | None = None, exchange_async=None) -> torch.Tensor:
+        work = (exchange_async(x_local, full) if exchange_async is not None
+                else allgather_blocks_async(x_local, full, partition))
         y_loc = self.local.spmv(x_local)          # overlaps the all-gather
         work.wait()
         return self.remote.apply_partial(full, y_loc, b)
@@ -322,6 +405,28 @@ class ShardOps(ShardVectorOps):
         self.ctx = ctx
         dev = shard.stage_cost.device
         self.full = torch.empty(shard.n_global, dtype=torch.float64, device=dev)
+        # V exchange for the SpMVs: halo (point-to-point) when the ranks' column
+        # ranges are narrow, else the all-gather (collective: every rank builds this)
+        t = shard.transitions
+        cmin, cmax = _lib.C.c_int64(), _lib.C.c_int64()
+        _lib.check(_lib.lib().ipi_col_range(_lib.ptr(t.col_idx), int(t.col_idx.numel()),
+                                            _lib.C.byref(cmin), _lib.C.byref(cmax),
+                                            _lib.stream_ptr()), "ipi_col_range")
+        lo, hi = ctx.block
+        need = (min(cmin.value, lo), max(cmax.value, hi - 1)) if cmax.value >= 0 else (lo, hi - 1)
+        self.halo = HaloExchange(ctx.partition, ctx.rank, ctx.world, need, shard.n_global, dev)
+
+    def exchange_async(self, local: torch.Tensor, full: torch.Tensor):
+        if self.halo.enabled:
+            return self.halo.exchange_async(local.contiguous(), full)
+        return allgather_blocks_async(local.contiguous(), full, self.ctx.partition)
+
+    def exchange(self, local: torch.Tensor) -> torch.Tensor:
+        """V for this rank's SpMVs: every entry its rows can read is current."""
+        if self.halo.enabled:
+            self.halo.exchange_async(local.contiguous(), self.full).wait()
+            return self.full
+        return self.allgather(local)
 
     # -- collectives ------------------------------------------------------
     def allgather(self, local: torch.Tensor) -> torch.Tensor:
@@ -352,7 +457,7 @@ class ShardOps(ShardVectorOps):
     # -- kernels ------------------------------------------------------------
     def greedy(self, v_local: torch.Tensor):
         """K1 on the shard: (policy_local int32, applied_local, global ||v - Tv||_inf)."""
-        vf = self.allgather(v_local)
+        vf = self.exchange(v_local)
         pol, app, bits = self.shard.bellman(vf)
         res = float(bits.view(torch.float64)[0])
         return pol.clone(), app.clone(), self.max(res)
@@ -385,8 +490,9 @@ class ShardOps(ShardVectorOps):
         """b - (x - gamma P x) (or x - gamma P x) on the local rows."""
         b = b_local.contiguous() if b_local is not None else None
         if isinstance(P, SplitShardOperator):
-            return P.apply_overlapped(x_local.contiguous(), self.full, self.ctx.partition, b)
-        xf = self.allgather(x_local)
+            return P.apply_overlapped(x_local.contiguous(), self.full, self.ctx.partition, b,
+                                      exchange_async=self.exchange_async)
+        xf = self.exchange(x_local)
         return P.apply(xf, b)
 
     def sweep(self, P, g_local, v_local):

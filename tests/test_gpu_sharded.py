@@ -133,3 +133,57 @@ def test_split_operator_halves_equal_unsplit(state0, n_local):
         got = sp.remote.apply_partial(x, y_loc, bb)
         ref = whole.apply(x, bb)
         torch.testing.assert_close(got, ref, rtol=1e-13, atol=1e-14)
+
+
+
+def _sis_worker(rank, world, port, q, halo_frac):
+    """C4-shaped (SIS, variable rows with banded columns) sharded solve; with
+    IPI_HALO_FRAC = 1 the V exchange is point-to-point halos, not all-gathers."""
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), IPI_HALO_FRAC=halo_frac)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2507_22538_b200.parallel import MdpShard, RankContext, ShardOps, solve_sharded
+        mdp, spec = devgen.build_instance(4, population=2000)
+        n, m = mdp.n, mdp.m
+        ctx = RankContext.from_env(n)
+        lo, hi = ctx.block
+        rp, col, val = mdp.transitions.row_ptr, mdp.transitions.col_idx, mdp.transitions.values
+        a, b = int(rp[lo * m]), int(rp[hi * m])
+        sub = ipi.CsrMatrix((hi - lo) * m, n, (rp[lo * m:hi * m + 1] - a).clone(),
+                            col[a:b].clone(), val[a:b].clone())
+        shard = MdpShard(n, m, spec.gamma, lo, mdp.stage_cost[lo:hi].clone(), sub)
+        ops = ShardOps(shard, ctx)
+        res = solve_sharded(ops, ipi.SolveOptions(alpha=spec.alpha, tol=spec.atol), n)
+        q.put((rank, ops.halo.enabled, ops.halo.bytes_received(), res.status.value,
+               res.outer_iterations, res.values.tolist(), res.policy.tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("halo_frac", ["1.0", "0.0"])
+def test_two_ranks_sis_halo_exchange(halo_frac):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sis_worker, args=(r, 2, port, q, halo_frac)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    (_, en0, b0, st0, k0, v0, p0), (_, en1, b1, st1, k1, v1, p1) = out
+    assert en0 == en1 == (halo_frac == "1.0")
+    if en0:  # a halo, not the other rank's whole block
+        assert 0 < b0 < 8 * 1001 and 0 < b1 < 8 * 1001
+    assert (st0, k0, p0) == (st1, k1, p1) and v0 == v1
+    mdp, spec = devgen.build_instance(4, population=2000)
+    ref = ipi.solve(mdp, ipi.SolveOptions(alpha=spec.alpha, tol=spec.atol))
+    assert st0 == ref.status.value
+    assert abs(k0 - ref.outer_iterations) <= 1
+    np.testing.assert_allclose(v0, ref.values, rtol=1e-8, atol=1e-8 * np.abs(ref.values).max())
+    np.testing.assert_array_equal(p0, ref.policy)

@@ -422,3 +422,47 @@ def test_creator_argument_errors_before_device():
         mf.createTransitionProbabilityTensor(2, 1, lambda s, a: ([0, 0], [0.5, 0.5]))
     with pytest.raises(ipi.ValidationError, match="negative"):
         mf.createTransitionProbabilityTensor(2, 1, lambda s, a: ([0, 1], [1.5, -0.5]))
+
+
+# ----------------------------------------------------------------------------
+# halo (point-to-point) V exchange over gloo, world size 3, CPU tensors
+# ----------------------------------------------------------------------------
+
+def _halo_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2507_22538_b200.model import make_partition
+        from paper_2507_22538_b200.parallel import HaloExchange
+        n = 100
+        part = make_partition(n, world)
+        lo, hi = part.block(rank)
+        need = (max(0, lo - 7), min(n - 1, hi - 1 + 11))  # asymmetric halo
+        os.environ["IPI_HALO_FRAC"] = "0.9"
+        hx = HaloExchange(part, rank, world, need, n, torch.device("cpu"))
+        ref = torch.arange(n, dtype=torch.float64) * 1.5 + 2.0
+        full = torch.full((n,), float("nan"), dtype=torch.float64)
+        hx.exchange_async(ref[lo:hi].clone(), full).wait()
+        ok = bool(torch.equal(full[need[0]:need[1] + 1], ref[need[0]:need[1] + 1]))
+        q.put((rank, hx.enabled, ok, hx.bytes_received()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_halo_exchange_gloo_world3():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_halo_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(enabled and ok for _, enabled, ok, _ in out), out
+    # the middle rank receives both halos (7 + 11 entries), the outer ranks one each
+    assert [b // 8 for *_, b in out] == [11, 18, 7]
