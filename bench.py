@@ -438,7 +438,7 @@ def run_ours(args):
         ipi_sharded = {"time_to_tol_s": float(tt[0]), "status": res_sh.status.value,
                        "outer": res_sh.outer_iterations, "inner": res_sh.inner_iterations_total,
                        "final_residual": res_sh.residual_history[-1],
-                       "driver": "parallel.solve_sharded (host-driven phases, NCCL)"}
+                       "driver": "parallel.solve_sharded (host-driven phases, %s)" % dist.get_backend()}
     out = None
     if rank == 0:
         cpu = None
