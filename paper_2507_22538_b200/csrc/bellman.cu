@@ -1324,6 +1324,8 @@ int launch_bellman(ipi_mdp* h, const double* v_full, int32_t mode, int32_t* poli
     IPI_LAUNCH_CHECK();
     return IPI_OK;
   }
+  if (h->plan.k1_variant == 9)
+    return launch_bellman_tiled(h, v_full, mode, policy, applied, g_pi, len_pi, res_bits, st);
   if (h->plan.k1_variant == 6) {
     if (a.win_async && h->ring_win_bytes > 0 && (uintptr_t)v_full % 16 != 0) {
       // the window is staged in 16-byte cp.async chunks: realign V once

@@ -317,6 +317,7 @@ void ipi_mdp_destroy(ipi_mdp* h) {
   cudaFree(h->invd);
   cudaFree(h->vbuf);
   cudaFree(h->k1_trace);
+  k1_tiled_free(h);
   if (h->host_pinned) cudaFreeHost(h->host_pinned);
   delete h;
 }

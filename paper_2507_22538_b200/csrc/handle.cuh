@@ -51,6 +51,14 @@ struct ipi_mdp {
   int k1_interleave = 1;    // variant 6: interleaved state order (IPI_K1_INTERLEAVE=0: contiguous)
   int k1_rotate = 1;        // variant 6: rotated per-CTA start (IPI_K1_ROTATE=0: none)
   unsigned long long* k1_trace = nullptr;  // diagnostics (ipi_mdp_k1_trace)
+  // variant 9: column-tiled layout of the shard (bellman_tiled.cu)
+  double* tl_val = nullptr;
+  uint32_t* tl_key = nullptr;
+  int32_t* tl_farcol = nullptr;
+  int64_t* tl_farbase = nullptr;
+  int32_t* tl_meta = nullptr;
+  int64_t tl_nblocks = 0, tl_wt = 0;
+  int tl_bs = 0, tl_T = 0;
 };
 
 // A planned policy operator (K3): borrowed P_pi rows + the kernel shape.
@@ -114,6 +122,14 @@ int flat_ring_smem(int K, int stages, int warps, int m, int window_bytes);
 bool k1_ring_prepare(int K, int S, int NW, bool win, int smem);
 int uniform_ring_smem(int K, int stages, int warps, int window_bytes);
 bool k1_uring_prepare(int K, int NW, int S, int D, bool win, int smem);
+
+// bellman_tiled.cu: column-tiled K1 for window-less uniform rows (variant 9)
+int k1_tiled_build(ipi_mdp* h, int64_t wt, cudaStream_t st);
+void k1_tiled_free(ipi_mdp* h);
+int k1_tiled_smem(const ipi_mdp* h);
+int launch_bellman_tiled(ipi_mdp* h, const double* v_full, int32_t mode, int32_t* policy,
+                         double* applied, double* g_pi, int32_t* len_pi,
+                         unsigned long long* res_bits, cudaStream_t st);
 
 // bellman_tma.cu
 bool k1_tma_plan(int64_t n_states_max_cta, int m, int K, int halo, int64_t n_global, int* SC,

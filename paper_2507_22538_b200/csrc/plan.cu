@@ -571,11 +571,58 @@ static int plan_tma(PlanCtx& c) {
   return IPI_OK;
 }
 
+// window-less uniform rows (C5): column-tiled layout.  Opt-in experiment
+// (IPI_K1_TILED=1 forces it, =2 lets the planner time it against the
+// register-deep kernel): correct, but 16.7 vs 8.0 ms on a C5 rank block — the
+// ~3.8-entry row pieces per tile cost a segmented scan each.
+static int plan_tiled(PlanCtx& c) {
+  ipi_mdp* h = c.h;
+  cudaStream_t st = c.st;
+  ipi_plan& p = h->plan;
+  const char* env = getenv("IPI_K1_TILED");
+  if (!env || (env[0] != '1' && env[0] != '2')) return IPI_OK;
+  const bool force = env[0] == '1';
+  if (p.k1_variant != 3 || !p.uniform_rows || p.halo >= 0 || (!force && p.nnz < (1ll << 26)))
+    return IPI_OK;
+  // near half-width: the smallest 2^k covering >= 85% of the sampled gathers
+  double cum[41];
+  cum[0] = 0.0;
+  for (int b = 0; b < 40; ++b) cum[b + 1] = cum[b] + (double)c.hst[8 + b];
+  int k = 0;
+  while (k < 30 && cum[40] > 0 && cum[std::min(k, 39) + 1] / cum[40] < 0.85) ++k;
+  const int64_t wt = std::min<int64_t>(1ll << k, h->n_global);
+  int rc = k1_tiled_build(h, wt, st);
+  if (rc) return rc;
+  if (h->tl_nblocks == 0) return IPI_OK;
+  int best = 0;
+  if (!force) {  // time deep (0) vs tiled (1) on the instance
+    K1Scratch tmp(h->n_global, h->n_local, st);
+    const int saved = p.k1_variant;
+    best = !tmp.ok ? -1 : autotune_pick(
+        2, [&](int i) { p.k1_variant = i == 0 ? saved : 9; return true; },
+        [&] { return launch_bellman(h, tmp.v, IPI_MODE_MIN, tmp.policy, tmp.applied, nullptr,
+                                    nullptr, nullptr, st); }, st);
+    p.k1_variant = saved;
+  } else {
+    best = 1;
+  }
+  if (best == 1) {
+    p.k1_variant = 9;
+    p.k1_blocks = (int32_t)std::min<int64_t>(h->tl_nblocks, h->num_sms);
+    p.k1_threads = 16 * 32;
+    p.k1_smem_bytes = k1_tiled_smem(h);
+  } else {
+    k1_tiled_free(h);
+  }
+  return IPI_OK;
+}
+
 int plan_instance(ipi_mdp* h, cudaStream_t st) {
   PlanCtx c{h, st, h->n_local * (int64_t)h->m, {}};
   int rc = plan_row_stats(c);
   if (!rc) rc = plan_window_and_grid(c);
   if (!rc) rc = plan_deep(c);
+  if (!rc) rc = plan_tiled(c);
   if (!rc) rc = plan_uniform_ring(c);
   if (!rc) rc = plan_generic_autotune(c);
   if (!rc) rc = plan_flat_ring(c);
