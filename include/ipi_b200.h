@@ -130,6 +130,7 @@ typedef struct {
   int32_t smem_bytes;
   int32_t stages;
   int32_t lanes_per_row; /* generic variant */
+  int32_t interleave;    /* uniform ring: warps take interleaved 4-row steps */
 } ipi_op_plan;
 
 /* Validation summary (model.py:148-194 validate; sparse.py:56-86 check). */

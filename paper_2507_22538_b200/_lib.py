@@ -61,7 +61,7 @@ class Plan(C.Structure):
 class OpPlan(C.Structure):
     _fields_ = [("nnz", _i64), ("variant", _i32), ("row_len", _i32), ("halo", _i32),
                 ("blocks", _i32), ("threads", _i32), ("smem_bytes", _i32), ("stages", _i32),
-                ("lanes_per_row", _i32)]
+                ("lanes_per_row", _i32), ("interleave", _i32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

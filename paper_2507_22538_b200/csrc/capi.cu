@@ -592,14 +592,20 @@ int ipi_op_create(const int64_t* rp, const int32_t* col, const double* val, int6
     nshape = 1;
   }
   const int align = variant == IPI_K3_FLAT ? 32 : 4;
-  auto install = [&](int NW, int S, int waves) -> bool {
+  // nowin: no x window — gathers go through L1/L2 (x is L2-resident) and the
+  // warps interleave 4-row steps so each CTA reads one contiguous stream; on
+  // C2 this beats the windowed shapes (0.81 vs 0.72 of HBM: no window staging
+  // before the first row, fewer concurrent DRAM streams).
+  auto install = [&](int NW, int S, int waves, bool nowin = false, int ilv = -1) -> bool {
     const int64_t per_warp_min = variant == IPI_K3_FLAT ? 64 : 16;
     const int blocks = (int)std::min<int64_t>((int64_t)sms * waves,
                                               std::max<int64_t>(1, n_local / (NW * per_warp_min)));
     const int64_t worst = (n_local + blocks - 1) / blocks + 2 * align;
     int wbytes = 0;
-    if (pl.halo >= 0) {  // + 2: the window start is rounded down to an even index
-      const int64_t wlen = std::min<int64_t>(n_global, worst + 2 * (int64_t)pl.halo) + 2;
+    int halo = nowin ? -1 : pl.halo;
+    if (halo >= 0 && getenv("IPI_K3_HALO")) halo = std::min(halo, std::max(-1, atoi(getenv("IPI_K3_HALO"))));
+    if (halo >= 0) {  // + 2: the window start is rounded down to an even index
+      const int64_t wlen = std::min<int64_t>(n_global, worst + 2 * (int64_t)halo) + 2;
       wbytes = (int)std::min<int64_t>(wlen * 8, INT32_MAX / 2);
     }
     int smem = variant == IPI_K3_FLAT ? k3_flat_smem(K, S, NW, wbytes) : k3_uring_smem(K, S, NW, wbytes);
@@ -614,22 +620,26 @@ int ipi_op_create(const int64_t* rp, const int32_t* col, const double* val, int6
     op->stages = S;
     op->smem = smem;
     op->win_bytes = wbytes;
-    op->halo = wbytes > 0 ? pl.halo : -1;
+    op->halo = wbytes > 0 ? halo : -1;
     op->pf = getenv("IPI_K3_PF") ? atoi(getenv("IPI_K3_PF")) : 0;
+    op->interleave = ilv >= 0 ? ilv : wbytes == 0;
+    if (getenv("IPI_K3_INTERLEAVE")) op->interleave = atoi(getenv("IPI_K3_INTERLEAVE")) != 0;
     return true;
   };
   bool done = false;
   for (int si = 0; si < nshape && allow && aligned && pl.uniform_rows && !done; ++si)
     done = install(shapes[si][0], shapes[si][1], shapes[si][2]);
   // Autotune the shape on the operator itself for large P_pi (same board
-  // sensitivity as K1, see ipi_mdp_create): one warm + one timed apply per
-  // candidate (~2 ms once per operator).  IPI_K3_AUTOTUNE=0 disables.
+  // sensitivity as K1, see ipi_mdp_create): one warm + three timed applies per
+  // candidate (~6 ms once per operator).  IPI_K3_AUTOTUNE=0 disables.
   const char* at = getenv("IPI_K3_AUTOTUNE");
   if (done && nshape > 1 && !(at && at[0] == '0') && op->nnz >= (1ll << 25)) {
-    const int cu[8][3] = {{11, 3, 1}, {12, 3, 3}, {12, 3, 6}, {12, 3, 4},
-                          {12, 3, 2}, {10, 3, 1}, {12, 3, 8}, {11, 3, 2}};
-    const int cf[4][3] = {{24, 4, 1}, {28, 4, 1}, {16, 4, 1}, {16, 4, 2}};
-    const int nc = variant == IPI_K3_FLAT ? 4 : 8;
+    // (warps, stages, CTAs per SM, no window, interleaved warps)
+    const int cu[11][5] = {{12, 3, 1, 1, 1}, {11, 3, 1, 1, 1}, {10, 3, 2, 1, 1}, {10, 4, 1, 1, 1},
+                           {12, 3, 3, 1, 0}, {12, 3, 4, 1, 0}, {11, 3, 1, 0, 0}, {12, 3, 3, 0, 0},
+                           {12, 3, 6, 0, 0}, {12, 3, 4, 0, 0}, {12, 3, 2, 0, 0}};
+    const int cf[4][5] = {{24, 4, 1, 0, 0}, {28, 4, 1, 0, 0}, {16, 4, 1, 0, 0}, {16, 4, 2, 0, 0}};
+    const int nc = variant == IPI_K3_FLAT ? 4 : 11;
     cudaStream_t st = (cudaStream_t)stream;
     double* tx = nullptr;
     double* ty = nullptr;
@@ -638,11 +648,11 @@ int ipi_op_create(const int64_t* rp, const int32_t* col, const double* val, int6
                     cudaMemsetAsync(tx, 0, sizeof(double) * n_global, st) == cudaSuccess;
     auto shape = [&](int i) { return variant == IPI_K3_FLAT ? cf[i] : cu[i]; };
     const int best = !ok ? -1 : autotune_pick(
-        nc, [&](int i) { const int* c = shape(i); return install(c[0], c[1], c[2]); },
-        [&] { return op_launch(op, tx, nullptr, 1, ty, st); }, st);
+        nc, [&](int i) { const int* c = shape(i); return install(c[0], c[1], c[2], c[3] != 0, c[4]); },
+        [&] { return op_launch(op, tx, nullptr, 1, ty, st); }, st, 3);
     if (best >= 0) {
       const int* c = shape(best);
-      install(c[0], c[1], c[2]);
+      install(c[0], c[1], c[2], c[3] != 0, c[4]);
     } else {
       install(shapes[0][0], shapes[0][1], shapes[0][2]);
     }
@@ -688,6 +698,7 @@ int ipi_op_get_plan(const ipi_op* op, ipi_op_plan* out) {
   out->smem_bytes = op->smem;
   out->stages = op->stages;
   out->lanes_per_row = op->lanes;
+  out->interleave = op->interleave;
   return IPI_OK;
 }
 

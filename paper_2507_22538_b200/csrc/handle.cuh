@@ -75,6 +75,7 @@ struct ipi_op {
   int win_bytes = 0;  // window bytes in front of the rings
   int blocks = 0, warps = 0, stages = 0, smem = 0;
   int pf = 0;         // uniform ring: L2 prefetch distance (steps)
+  int interleave = 0; // uniform ring: warps interleave 4-row steps (one stream per CTA)
   unsigned long long* trace = nullptr;  // diagnostics (ipi_op_trace)
 };
 

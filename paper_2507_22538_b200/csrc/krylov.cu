@@ -90,6 +90,7 @@ int inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_p
   a.bar = reinterpret_cast<unsigned*>(a.partials + 4 * (int64_t)blocks);
   IPI_CUDA_TRY(cudaMemsetAsync(a.bar, 0, 64, st));
   a.bar_mode = getenv("IPI_K4_BARRIER") ? atoi(getenv("IPI_K4_BARRIER")) : 0;
+  a.xwin = getenv("IPI_K4_XWIN") ? atoi(getenv("IPI_K4_XWIN")) != 0 : 1;
   {  // L2 residency of P_pi across the solve's SpMVs (IPI_K4_KEEP overrides the fraction)
     int l2 = 0;
     cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);

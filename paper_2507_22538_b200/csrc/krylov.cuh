@@ -58,6 +58,7 @@ struct KArgs {
   unsigned* bar;       // grid barrier counter, zeroed before every launch
   int bar_mode;        // GridBarrier::mode (IPI_K4_BARRIER)
   float keep_frac;     // fraction of P_pi accesses marked L2 evict-last (0 = evict-first)
+  int xwin;            // stage the SpMV input window (else the window space only holds MGS slices)
 };
 
 // Grid barrier for the co-resident (cooperatively launched) CTAs: one release
@@ -170,7 +171,7 @@ __device__ __forceinline__ void spmv_rows(const KArgs& a, const double* xin, int
     lo = lo < 0 ? 0 : lo;
     hi = hi > a.n ? a.n : hi;
     __syncthreads();
-    if (hi - lo <= a.win_cap) {  // all copies in flight at once (8-byte cp.async)
+    if (a.xwin && hi - lo <= a.win_cap) {  // all copies in flight at once (8-byte cp.async)
       w_lo = lo;
       w_len = hi - lo;
       const uint32_t ws = (uint32_t)__cvta_generic_to_shared(win);

@@ -12,12 +12,13 @@ inline int grid_for(int64_t work, int threads, int sms) {
 }
 
 // Plan-time autotuning: for each candidate that `install(i)` accepts, run
-// `launch()` once warm and once timed (CUDA events on `st`) and return the
+// `launch()` once warm and `reps` times timed (CUDA events on `st`) and return the
 // index of the fastest (-1 if none ran).  The kernels' streaming rate depends on
 // the CTA count in a board-dependent way, so large instances are
 // planned by measurement; callers install the winner afterwards.
 template <class Install, class Launch>
-inline int autotune_pick(int ncand, Install&& install, Launch&& launch, cudaStream_t st) {
+inline int autotune_pick(int ncand, Install&& install, Launch&& launch, cudaStream_t st,
+                         int reps = 1) {
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) {
     if (e0) cudaEventDestroy(e0);
@@ -30,7 +31,9 @@ inline int autotune_pick(int ncand, Install&& install, Launch&& launch, cudaStre
     if (!install(i)) continue;
     if (launch()) break;
     cudaEventRecord(e0, st);
-    if (launch()) break;
+    bool bad = false;
+    for (int r = 0; r < reps && !bad; ++r) bad = launch() != 0;
+    if (bad) break;
     cudaEventRecord(e1, st);
     float ms = 0.f;
     if (cudaEventSynchronize(e1) != cudaSuccess || cudaEventElapsedTime(&ms, e0, e1) != cudaSuccess) break;

@@ -44,6 +44,7 @@ struct K3Args {
   int halo;
   int pf;  // uniform ring: L2 bulk prefetch distance in steps beyond the ring (0 = off)
   unsigned long long* trace;  // diagnostics: per-CTA (smid, start ns, end ns) or nullptr
+  int interleave;  // uniform ring: warp w takes 4-row steps w, w+NW, ... of its CTA (else a contiguous range)
 };
 
 __device__ __forceinline__ unsigned long long k3_ns() {
@@ -147,13 +148,24 @@ __global__ void __launch_bounds__(NW * 32, 1) k3_uring(K3Args a, int win_bytes) 
     return __ldg(xg + c);
   };
   const int64_t nr = r_hi - r_lo;
-  const int64_t w0 = r_lo + (nr * warp / NW) / 4 * 4;
-  const int64_t w1 = warp + 1 == NW ? r_hi : r_lo + (nr * (warp + 1) / NW) / 4 * 4;
-  const int64_t nb = (w1 - w0 + 3) >> 2;
+  // rows of step i: [w0 + 4*rs*i, +4) clipped to w1
+  int64_t w0, w1, nb, rs;
+  if (a.interleave) {  // the CTA's warps read one contiguous stream
+    const int64_t groups = (nr + 3) >> 2;
+    w0 = r_lo + 4 * warp;
+    w1 = r_hi;
+    nb = groups > warp ? (groups - warp + NW - 1) / NW : 0;
+    rs = NW;
+  } else {
+    w0 = r_lo + (nr * warp / NW) / 4 * 4;
+    w1 = warp + 1 == NW ? r_hi : r_lo + (nr * (warp + 1) / NW) / 4 * 4;
+    nb = (w1 - w0 + 3) >> 2;
+    rs = 1;
+  }
 
   auto issue = [&](int64_t i, int stg) {
     if (i < nb) {
-      const int64_t row0 = w0 + 4 * i;
+      const int64_t row0 = w0 + 4 * rs * i;
       const int64_t left = w1 - row0;
       const int nrow = left < 4 ? (int)left : 4;
       const uint32_t st = ring_s + (uint32_t)(stg * L::kStage);
@@ -172,7 +184,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k3_uring(K3Args a, int win_bytes) 
         cp_async16(st + L::kVal + r * K * 4 + 16 * (cc ^ (r << 1)), ok ? cp + 4 * c : cp, ok ? 16 : 0, pol);
       }
       if (a.pf > 0 && lane < 2 && i + a.pf < nb) {  // DRAM -> L2 ahead of the ring
-        const int64_t rp0 = row0 + 4 * (int64_t)a.pf;
+        const int64_t rp0 = row0 + 4 * rs * (int64_t)a.pf;
         const int64_t lp = w1 - rp0;
         const int np = lp < 4 ? (int)lp : 4;
         if (lane == 0) l2_prefetch(a.val + rp0 * K, (uint32_t)(np * K * 8));
@@ -201,7 +213,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k3_uring(K3Args a, int win_bytes) 
     for (int k = 0; k < NC; ++k) x[k] = gather(*reinterpret_cast<const int*>(st + caddr(grp, 1 + j + 8 * k)));
     if (has_last) x[NC] = gather(*reinterpret_cast<const int*>(st + caddr(grp, e_last)));
     if (NEED_XD && j == 0) {
-      const int64_t row = w0 + 4 * i + grp;
+      const int64_t row = w0 + 4 * rs * i + grp;
       if (row < w1) x[NC + 1] = gather((int)(a.state0 + row));
     }
   };
@@ -217,7 +229,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k3_uring(K3Args a, int win_bytes) 
     r = add_rn(r, __shfl_xor_sync(kFull, r, 4));
     __syncwarp();
     if (j == 0) {
-      const int64_t row = w0 + 4 * i + grp;
+      const int64_t row = w0 + 4 * rs * i + grp;
       if (row < w1) {
         const double* t = tb + (grp << 3);
 #pragma unroll
@@ -407,7 +419,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k3_flat(K3Args a, int win_bytes) {
 // instances and dispatch
 // ---------------------------------------------------------------------------
 // (warps, stages) shapes with an instance
-#define IPI_K3U_SHAPES(M) M(64, 12, 3) M(64, 16, 3) M(64, 8, 4) M(64, 10, 3) M(64, 14, 3) M(64, 15, 3) M(64, 11, 3) M(64, 13, 3)
+#define IPI_K3U_SHAPES(M) M(64, 12, 3) M(64, 16, 3) M(64, 8, 4) M(64, 10, 3) M(64, 14, 3) M(64, 15, 3) M(64, 11, 3) M(64, 13, 3) M(64, 12, 4) M(64, 13, 4) M(64, 10, 4)
 #define IPI_K3F_SHAPES(M) M(4, 16, 4) M(4, 8, 6) M(4, 24, 4) M(4, 28, 4) M(4, 20, 5) M(2, 16, 4) M(2, 24, 4)
 
 template <class F>
@@ -485,7 +497,7 @@ int op_launch(const ipi_op* op, const double* x_full, const double* b, int epi, 
     return launch_spmv(op->rp, op->col, op->val, op->n_local, x_full, b, op->gamma, epi, y,
                        op->lanes, st, op->state0, y_partial);
   K3Args a{op->col, op->val, op->n_local, op->state0, op->n_global, x_full, b, op->gamma, y, op->halo,
-            op->pf, op->trace};
+            op->pf, op->trace, op->interleave};
   bool ok = false;
   switch (epi) {
     case 0: ok = k3_launch_epi<0>(op, a, st); break;

@@ -57,7 +57,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="2,3,4")
     ap.add_argument("--reps", type=int, default=30)
-    ap.add_argument("--shapes", default="", help="warps:stages:waves[:l2_prefetch_steps] list to force, ';'-separated")
+    ap.add_argument("--shapes", default="", help="warps:stages:waves[:l2_prefetch_steps[:halo_cap[:interleave]]] list to force, ';'-separated")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     for cfg in [int(c) for c in a.configs.split(",")]:
@@ -77,6 +77,10 @@ def main():
             env = {"IPI_K3_WARPS": parts[0], "IPI_K3_STAGES": parts[1], "IPI_K3_WAVES": parts[2]}
             if len(parts) > 3:
                 env["IPI_K3_PF"] = parts[3]
+            if len(parts) > 4:
+                env["IPI_K3_HALO"] = parts[4]
+            if len(parts) > 5:
+                env["IPI_K3_INTERLEAVE"] = parts[5]
             variants.append((f"shape{sh}", env))
         variants.append(("generic", {"IPI_K3_RING": "0"}))
         for name, env in variants:

@@ -61,7 +61,8 @@ def host(t):
 
 @pytest.fixture
 def env_guard():
-    keys = ("IPI_K3_RING", "IPI_K3_WARPS", "IPI_K3_STAGES", "IPI_K3_WAVES")
+    keys = ("IPI_K3_RING", "IPI_K3_WARPS", "IPI_K3_STAGES", "IPI_K3_WAVES", "IPI_K3_HALO",
+            "IPI_K3_INTERLEAVE")
     saved = {k: os.environ.get(k) for k in keys}
     yield os.environ
     for k, v in saved.items():
@@ -125,6 +126,21 @@ def test_uring_forced_shapes(shape, env_guard):
     op = check_bitwise(rp, col, val, 0.999, expect=1)
     p = op.plan()
     assert (p["threads"] // 32, p["stages"]) == shape[:2]
+
+
+@pytest.mark.parametrize("shape", [(12, 3, 1), (10, 3, 2), (10, 4, 1), (12, 4, 1), (13, 4, 1)])
+@pytest.mark.parametrize("halo,ilv", [(-1, 1), (-1, 0), (100, 1), (300, 0)])
+@pytest.mark.parametrize("n", [4099, 30001])
+def test_uring_window_and_interleave(shape, halo, ilv, n, env_guard):
+    """No-window / capped-window rings with contiguous or interleaved warp rows
+    (the autotuner's candidates): still bitwise, shards included."""
+    env_guard["IPI_K3_WARPS"], env_guard["IPI_K3_STAGES"], env_guard["IPI_K3_WAVES"] = map(str, shape)
+    env_guard["IPI_K3_HALO"], env_guard["IPI_K3_INTERLEAVE"] = str(halo), str(ilv)
+    rp, col, val = band_rows(n, 64, seed=n + halo)
+    op = check_bitwise(rp, col, val, 0.999, expect=1)
+    p = op.plan()
+    assert p["interleave"] == ilv and (p["halo"] == -1) == (halo == -1), p
+    check_bitwise(rp, col, val, 0.999, n_local=n // 3 + 1, state0=n // 3, expect=1)
 
 
 def test_uring_shard_rows(env_guard):
