@@ -331,7 +331,8 @@ static int plan_uniform_ring(PlanCtx& c) {
       int64_t worst = 0;
       for (int c = 0; c < blocks; ++c) worst = std::max<int64_t>(worst, hb[c + 1] - hb[c]);
       int wbytes = 0;
-      if (p.halo >= 0) {  // + 2: the cp.async window start is rounded down to an even index
+      const bool nowin = getenv("IPI_K1_NOWIN") && atoi(getenv("IPI_K1_NOWIN")) != 0;
+      if (p.halo >= 0 && !nowin) {  // + 2: the cp.async window start is rounded down to an even index
         const int64_t wlen = std::min<int64_t>(n_global, worst + 2 * (int64_t)p.halo) + 2;
         wbytes = (int)std::min<int64_t>(wlen * 8, INT32_MAX / 2);
         if (uniform_ring_smem(64, S, NW, wbytes) > budget) return false;  // keep the window
