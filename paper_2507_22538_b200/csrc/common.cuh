@@ -63,11 +63,14 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
 }
 
 // Coherent (non-.nc) load with an L2 eviction hint, for data written earlier in
-// the same kernel.  Not volatile: the compiler may batch these ahead of
-// unrelated stores (callers never load an address they stored in the same pass).
+// the same kernel (Krylov basis, w).  Volatile with a memory clobber: a plain
+// asm without one is a pure function of its operands to the compiler, which
+// may then hoist it above the barrier or the stores that produce the data (it
+// did, in a 384-thread K4 build: GMRES diverged until this was added; the
+// committed 1024-thread kernels measured the same before and after).
 __device__ __forceinline__ double ld_hint(const double* p, uint64_t pol) {
   double v;
-  asm("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol) : "memory");
   return v;
 }
 
