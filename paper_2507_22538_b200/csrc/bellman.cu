@@ -1040,7 +1040,8 @@ __global__ void __launch_bounds__(kK1Threads, 1) k1_bellman_deep(K1Args a, int K
       const uint32_t off = (uint32_t)(c - w_lo);
       if (off < w_len) {
         double x;
-        asm("ld.shared.f64 %0, [%1];" : "=d"(x) : "r"(win_s + off * 8u));
+        // volatile: the window is filled in this kernel (ordered by the barrier)
+        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(x) : "r"(win_s + off * 8u));
         return x;
       }
     }
