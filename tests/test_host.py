@@ -42,6 +42,29 @@ def test_library_exports_every_declared_symbol():
     assert set(declared) <= exported
 
 
+@pytest.mark.parametrize("cname,pyname", [
+    ("ipi_inner_report", "InnerReport"), ("ipi_opts", "Opts"), ("ipi_stats", "Stats"),
+    ("ipi_plan", "Plan"), ("ipi_op_plan", "OpPlan"), ("ipi_validation", "Validation"),
+    ("ipi_csr_report", "CsrReport")])
+def test_ctypes_structs_match_the_header(cname, pyname, tmp_path):
+    """The ctypes mirrors in _lib.py have the C header's size and field offsets
+    (compiled with gcc against include/ipi_b200.h)."""
+    cls = getattr(_lib, pyname)
+    fields = [f[0] for f in cls._fields_]
+    prog = ["#include <stdio.h>", "#include <stddef.h>", '#include "ipi_b200.h"', "int main(void) {",
+            f'  printf("%zu\\n", sizeof({cname}));']
+    prog += [f'  printf("%zu\\n", offsetof({cname}, {f}));' for f in fields]
+    prog += ["  return 0;", "}"]
+    src = tmp_path / "abi.c"
+    src.write_text("\n".join(prog) + "\n")
+    exe = tmp_path / "abi"
+    subprocess.run(["gcc", "-I", str(REPO / "include"), str(src), "-o", str(exe)], check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True,
+                                          check=True).stdout.split()]
+    assert got[0] == __import__("ctypes").sizeof(cls), (cname, got[0])
+    assert got[1:] == [getattr(cls, f).offset for f in fields], cname
+
+
 def test_library_is_sm100a_only():
     out = subprocess.run(["cuobjdump", "--list-elf", str(_lib.LIB_PATH)], capture_output=True,
                          text=True).stdout
