@@ -624,6 +624,7 @@ int ipi_op_create(const int64_t* rp, const int32_t* col, const double* val, int6
     op->pf = getenv("IPI_K3_PF") ? atoi(getenv("IPI_K3_PF")) : 0;
     op->interleave = ilv >= 0 ? ilv : wbytes == 0;
     if (getenv("IPI_K3_INTERLEAVE")) op->interleave = atoi(getenv("IPI_K3_INTERLEAVE")) != 0;
+    if (variant != IPI_K3_URING) op->interleave = 0;  // the flat kernel has one row order
     return true;
   };
   bool done = false;
