@@ -29,29 +29,29 @@ namespace ipi {
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
+// one arena per device (the standalone ipi_inner_solve; handles own theirs)
 static std::mutex g_ws_mu;
-static double* g_ws = nullptr;
-static int64_t g_ws_len = 0;
-static int g_ws_dev = -1;
+static double* g_ws[64] = {};
+static int64_t g_ws_len[64] = {};
 
 double* krylov_workspace(int64_t /*n*/, int64_t doubles_needed) {
   std::lock_guard<std::mutex> lk(g_ws_mu);
   int dev = 0;
-  cudaGetDevice(&dev);
-  if (g_ws && g_ws_dev == dev && g_ws_len >= doubles_needed) return g_ws;
-  if (g_ws) {
-    cudaDeviceSynchronize();
-    cudaFree(g_ws);
-    g_ws = nullptr;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  if (g_ws[dev] && g_ws_len[dev] >= doubles_needed) return g_ws[dev];
+  if (g_ws[dev]) {
+    cudaDeviceSynchronize();  // the arena may still be in use by queued solves
+    cudaFree(g_ws[dev]);
+    g_ws[dev] = nullptr;
+    g_ws_len[dev] = 0;
   }
-  if (cudaMalloc(&g_ws, sizeof(double) * doubles_needed) != cudaSuccess) {
-    g_ws = nullptr;
-    g_ws_len = 0;
+  if (cudaMalloc(&g_ws[dev], sizeof(double) * doubles_needed) != cudaSuccess) {
+    g_ws[dev] = nullptr;
+    cudaGetLastError();
     return nullptr;
   }
-  g_ws_len = doubles_needed;
-  g_ws_dev = dev;
-  return g_ws;
+  g_ws_len[dev] = doubles_needed;
+  return g_ws[dev];
 }
 
 int inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi, int64_t n,
