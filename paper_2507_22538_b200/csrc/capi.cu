@@ -641,25 +641,47 @@ int ipi_op_create(const int64_t* rp, const int32_t* col, const double* val, int6
                            {12, 3, 6, 0, 0}, {12, 3, 4, 0, 0}, {12, 3, 2, 0, 0}};
     const int cf[4][5] = {{24, 4, 1, 0, 0}, {28, 4, 1, 0, 0}, {16, 4, 1, 0, 0}, {16, 4, 2, 0, 0}};
     const int nc = variant == IPI_K3_FLAT ? 4 : 11;
-    cudaStream_t st = (cudaStream_t)stream;
-    double* tx = nullptr;
-    double* ty = nullptr;
-    const bool ok = cudaMalloc(&tx, sizeof(double) * n_global) == cudaSuccess &&
-                    cudaMalloc(&ty, sizeof(double) * n_local) == cudaSuccess &&
-                    cudaMemsetAsync(tx, 0, sizeof(double) * n_global, st) == cudaSuccess;
     auto shape = [&](int i) { return variant == IPI_K3_FLAT ? cf[i] : cu[i]; };
-    const int best = !ok ? -1 : autotune_pick(
-        nc, [&](int i) { const int* c = shape(i); return install(c[0], c[1], c[2], c[3] != 0, c[4]); },
-        [&] { return op_launch(op, tx, nullptr, 1, ty, st); }, st, 3);
+    // The pick is cached per (device, geometry, halo) for the process: the
+    // sharded driver re-plans P_pi every outer iteration with the same shape
+    // (IPI_K3_AUTOTUNE_CACHE=0 re-times every operator).
+    static std::mutex tune_mu;
+    static std::map<std::vector<int64_t>, int> tune_cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const std::vector<int64_t> key = {dev, variant, K, n_local, n_global, state0, op->nnz, pl.halo};
+    const char* cenv = getenv("IPI_K3_AUTOTUNE_CACHE");
+    const bool use_cache = !(cenv && cenv[0] == '0');
+    int best = -1;
+    if (use_cache) {
+      std::lock_guard<std::mutex> lk(tune_mu);
+      auto it = tune_cache.find(key);
+      if (it != tune_cache.end()) best = it->second;
+    }
+    if (best < 0) {
+      cudaStream_t st = (cudaStream_t)stream;
+      double* tx = nullptr;
+      double* ty = nullptr;
+      const bool ok = cudaMalloc(&tx, sizeof(double) * n_global) == cudaSuccess &&
+                      cudaMalloc(&ty, sizeof(double) * n_local) == cudaSuccess &&
+                      cudaMemsetAsync(tx, 0, sizeof(double) * n_global, st) == cudaSuccess;
+      best = !ok ? -1 : autotune_pick(
+          nc, [&](int i) { const int* c = shape(i); return install(c[0], c[1], c[2], c[3] != 0, c[4]); },
+          [&] { return op_launch(op, tx, nullptr, 1, ty, st); }, st, 3);
+      cudaFree(tx);
+      cudaFree(ty);
+      cudaGetLastError();
+      if (best >= 0 && use_cache) {
+        std::lock_guard<std::mutex> lk(tune_mu);
+        tune_cache[key] = best;
+      }
+    }
+    bool installed = false;
     if (best >= 0) {
       const int* c = shape(best);
-      install(c[0], c[1], c[2], c[3] != 0, c[4]);
-    } else {
-      install(shapes[0][0], shapes[0][1], shapes[0][2]);
+      installed = install(c[0], c[1], c[2], c[3] != 0, c[4]);
     }
-    cudaFree(tx);
-    cudaFree(ty);
-    cudaGetLastError();
+    if (!installed) install(shapes[0][0], shapes[0][1], shapes[0][2]);
   }
   *out = op;
   return IPI_OK;
