@@ -28,7 +28,7 @@
 namespace ipi {
 
 constexpr int kTileW = 8192;  // columns per V tile (64 KB)
-constexpr int kTiledNW = 16;  // warps per CTA (transform and backup)
+constexpr int kTiledNW = 32;  // warps per CTA (transform and backup)
 
 struct TiledArgs {
   const double* tv;
