@@ -27,19 +27,29 @@
 
 namespace ipi {
 
-constexpr int kTileW = 8192;  // columns per V tile (64 KB)
-constexpr int kTiledNW = 32;  // warps per CTA (transform and backup)
+constexpr int kTileW = 8192;   // columns per V tile (64 KB)
+constexpr int kTiledNW = 32;   // warps per CTA (transform and backup)
+constexpr int kTiledNT = kTiledNW * 32;
+#ifndef IPI_TILED_UN
+#define IPI_TILED_UN 12
+#endif
+#ifndef IPI_TILED_UF
+#define IPI_TILED_UF 8
+#endif
+constexpr int kTiledUN = IPI_TILED_UN;  // JDS steps in flight per warp (near tiles)
+constexpr int kTiledUF = IPI_TILED_UF;  // (far list: one more dependent load per step)
 
 struct TiledArgs {
   const double* tv;
-  const uint32_t* tk;
+  const uint16_t* tk;
   const int32_t* tfc;
   const int64_t* far_base;
-  const int32_t* meta;  // per block: (T + 1) x (NW + 1) split offsets, relative to the block's entries
+  const int32_t* meta;  // per block: split table (T + 1) x (NW + 1), then uint16 counts (T + 1) x NT
   const double* cost;
   const double* v;
   int64_t n_local, n_global, state0;
   int32_t m, K, bs, T;  // states per block, max tiles per block
+  int32_t rpl;          // rows per thread (consecutive block rows)
   int64_t wt;           // near half-width
   int64_t nblocks;
   double gamma;
@@ -51,6 +61,10 @@ struct TiledArgs {
   unsigned long long* res_bits;
 };
 
+__host__ __device__ __forceinline__ int64_t tiled_meta_stride(int T) {
+  return (int64_t)(T + 1) * (kTiledNW + 1) + (int64_t)(T + 1) * (kTiledNT / 2);
+}
+
 __device__ __forceinline__ void block_span(const TiledArgs& a, int64_t b, int64_t& s0, int64_t& s1,
                                            int64_t& cs, int64_t& ce) {
   s0 = b * a.bs;
@@ -61,164 +75,206 @@ __device__ __forceinline__ void block_span(const TiledArgs& a, int64_t b, int64_
   ce = ce > a.n_global ? a.n_global : ce;
 }
 
+__device__ __forceinline__ int tile_of(int64_t c, int64_t cs, int64_t ce, int T) {
+  return (c >= cs && c < ce) ? (int)((c - cs) / kTileW) : T;
+}
+
 // ---- plan-time transform ------------------------------------------------------
-// pass 1: per (warp, tile) counts -> split offsets (meta) and the block's far count
-__global__ void __launch_bounds__(kTiledNW * 32) tiled_count_kernel(const int32_t* __restrict__ col,
-                                                                    TiledArgs a, int32_t* meta,
-                                                                    int64_t* far_count) {
-  extern __shared__ int tcnt[];  // [NW][T + 1]
+// Layout per block of bs states: thread t of the CTA owns rows [t*rpl, t*rpl+rpl)
+// of the block.  For every tile (and the far list, tile T) each warp's entries
+// form one jagged-diagonal segment: step k holds entry k of every lane that has
+// more than k entries in the tile, in lane order, so a warp-wide load at step k
+// is contiguous.  A lane's entries in a tile are in (row, column) order; the
+// 16-bit key is (row_in_thread << 13 | column_in_tile).
+//
+// pass 1: per (tile, thread) counts and per (tile, warp) split offsets
+__global__ void __launch_bounds__(kTiledNT) tiled_count_kernel(const int32_t* __restrict__ col,
+                                                               TiledArgs a, int32_t* meta,
+                                                               int64_t* far_count) {
+  extern __shared__ __align__(16) unsigned char tsm_raw[];
+  uint16_t* cnt = reinterpret_cast<uint16_t*>(tsm_raw);  // [T + 1][NT]
   const int T1 = a.T + 1;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int* wtot = reinterpret_cast<int*>(tsm_raw + (size_t)T1 * kTiledNT * 2);  // [T + 1][NW]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t b = blockIdx.x;
   int64_t s0, s1, cs, ce;
   block_span(a, b, s0, s1, cs, ce);
-  for (int i = threadIdx.x; i < kTiledNW * T1; i += blockDim.x) tcnt[i] = 0;
+  for (int i = tid; i < T1 * kTiledNT; i += blockDim.x) cnt[i] = 0;
   __syncthreads();
-  const int64_t r0 = s0 * a.m, nr = (s1 - s0) * a.m;
-  const int64_t w0 = r0 + nr * warp / kTiledNW, w1 = r0 + nr * (warp + 1) / kTiledNW;
-  for (int64_t e = w0 * a.K + lane; e < w1 * a.K; e += 32) {
-    const int64_t c = col[e];
-    const int t = (c >= cs && c < ce) ? (int)((c - cs) / kTileW) : a.T;
-    atomicAdd(&tcnt[warp * T1 + t], 1);
+  const int nrows = (int)((s1 - s0) * a.m);
+  const int q0 = tid * a.rpl, q1 = min(nrows, q0 + a.rpl);
+  for (int q = q0; q < q1; ++q) {
+    const int64_t e0 = (s0 * a.m + q) * (int64_t)a.K;
+    for (int k = 0; k < a.K; ++k) ++cnt[tile_of(col[e0 + k], cs, ce, a.T) * kTiledNT + tid];
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int32_t* mb = meta + b * (int64_t)T1 * (kTiledNW + 1);
+  int32_t* mb = meta + b * tiled_meta_stride(a.T);
+  uint16_t* cg = reinterpret_cast<uint16_t*>(mb + (int64_t)T1 * (kTiledNW + 1));
+  for (int t = 0; t < T1; ++t) {
+    const int c = cnt[t * kTiledNT + tid];
+    cg[t * kTiledNT + tid] = (uint16_t)c;
+    const int s = __reduce_add_sync(kFull, c);
+    if (lane == 0) wtot[t * kTiledNW + warp] = s;
+  }
+  __syncthreads();
+  if (tid == 0) {
     int off = 0;
     for (int t = 0; t < T1; ++t) {
       for (int w = 0; w < kTiledNW; ++w) {
         mb[t * (kTiledNW + 1) + w] = off;
-        off += tcnt[w * T1 + t];
+        off += wtot[t * kTiledNW + w];
       }
       mb[t * (kTiledNW + 1) + kTiledNW] = off;
     }
-    int far = 0;
-    for (int w = 0; w < kTiledNW; ++w) far += tcnt[w * T1 + a.T];
-    far_count[b] = far;
+    far_count[b] = off - mb[a.T * (kTiledNW + 1)];
   }
 }
 
-// pass 2: stable scatter in (tile, warp, row, column) order
-__global__ void __launch_bounds__(kTiledNW * 32) tiled_scatter_kernel(
+// pass 2: every thread walks its own rows; entry j of a lane in tile t goes to
+// split(t, warp) + sum_l min(cnt_l, j) + #{l < lane : cnt_l > j}.
+__global__ void __launch_bounds__(kTiledNT) tiled_scatter_kernel(
     const int32_t* __restrict__ col, const double* __restrict__ val, TiledArgs a, double* tv,
-    uint32_t* tk, int32_t* tfc) {
-  extern __shared__ int tcur[];  // [NW][T + 1] cursors
+    uint16_t* tk, int32_t* tfc) {
+  extern __shared__ __align__(16) unsigned char tsm_raw[];
   const int T1 = a.T + 1;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint16_t* cnt = reinterpret_cast<uint16_t*>(tsm_raw);  // [T + 1][NT]
+  uint16_t* cur = cnt + (size_t)T1 * kTiledNT;           // [T + 1][NT]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t b = blockIdx.x;
   int64_t s0, s1, cs, ce;
   block_span(a, b, s0, s1, cs, ce);
-  const int32_t* mb = a.meta + b * (int64_t)T1 * (kTiledNW + 1);
-  for (int t = lane; t < T1; t += 32) tcur[warp * T1 + t] = mb[t * (kTiledNW + 1) + warp];
-  __syncwarp();
-  const int64_t r0 = s0 * a.m, nr = (s1 - s0) * a.m;
-  const int64_t w0 = r0 + nr * warp / kTiledNW, w1 = r0 + nr * (warp + 1) / kTiledNW;
-  const int64_t ebase = r0 * a.K;       // the block's first entry
+  const int32_t* mb = a.meta + b * tiled_meta_stride(a.T);
+  const uint16_t* cg = reinterpret_cast<const uint16_t*>(mb + (int64_t)T1 * (kTiledNW + 1));
+  for (int i = tid; i < T1 * kTiledNT; i += blockDim.x) {
+    cnt[i] = cg[i];
+    cur[i] = 0;
+  }
+  __syncthreads();
+  const int nrows = (int)((s1 - s0) * a.m);
+  const int q0 = tid * a.rpl, q1 = min(nrows, q0 + a.rpl);
+  const int64_t ebase = s0 * a.m * (int64_t)a.K;
   const int far0 = mb[a.T * (kTiledNW + 1)];
   const int64_t fbase = a.far_base[b];
-  const unsigned lt = (1u << lane) - 1u;
-  for (int64_t r = w0; r < w1; ++r) {
-    const uint32_t rib = (uint32_t)(r - r0);
-    for (int64_t e0 = r * a.K; e0 < (r + 1) * a.K; e0 += 32) {
-      const int64_t e = e0 + lane;
-      const bool act = e < (r + 1) * a.K;
-      const unsigned am = __ballot_sync(kFull, act);
-      if (!act) continue;
-      const int64_t c = col[e];
-      const bool near = c >= cs && c < ce;
-      const int t = near ? (int)((c - cs) / kTileW) : a.T;
-      const unsigned peers = __match_any_sync(am, t);
-      const int rank = __popc(peers & lt);
-      const int pos = tcur[warp * T1 + t] + rank;
-      tv[ebase + pos] = val[e];
-      if (near) {
-        tk[ebase + pos] = (rib << 13) | (uint32_t)(c - cs - (int64_t)t * kTileW);
+  for (int q = q0; q < q1; ++q) {
+    const int64_t e0 = (s0 * a.m + q) * (int64_t)a.K;
+    for (int k = 0; k < a.K; ++k) {
+      const int64_t c = col[e0 + k];
+      const int t = tile_of(c, cs, ce, a.T);
+      const int j = cur[t * kTiledNT + tid]++;
+      const uint16_t* cw = cnt + t * kTiledNT + warp * 32;
+      int off = 0;
+      for (int l = 0; l < 32; ++l) {
+        const int cl = cw[l];
+        off += cl < j ? cl : j;
+        off += (l < lane && cl > j) ? 1 : 0;
+      }
+      const int pos = mb[t * (kTiledNW + 1) + warp] + off;
+      tv[ebase + pos] = val[e0 + k];
+      const uint32_t tag = (uint32_t)(q - q0) << 13;
+      if (t < a.T) {
+        tk[ebase + pos] = (uint16_t)(tag | (uint32_t)(c - cs - (int64_t)t * kTileW));
       } else {
-        tk[ebase + pos] = rib << 13;
+        tk[ebase + pos] = (uint16_t)tag;
         tfc[fbase + (pos - far0)] = (int32_t)c;
       }
-      __syncwarp(am);
-      if (rank == 0) tcur[warp * T1 + t] += __popc(peers);
-      __syncwarp(am);
     }
   }
 }
 
 // ---- the backup ----------------------------------------------------------------
-template <bool FAR>
-__device__ __forceinline__ void tiled_segment(const TiledArgs& a, int64_t ebase, int e_lo, int e_hi,
-                                              const double* vt, int64_t far_off, double* acc) {
-  constexpr int U = 8;  // 32-entry chunks in flight per warp (loads issued before any reduction)
-  const int lane = threadIdx.x & 31;
-  for (int c0 = e_lo; c0 < e_hi; c0 += 32 * U) {
-    uint32_t key[U];
-    double vv[U], x[U];
+// Read-only loads with an L2 hint: the entry streams are evict-first, the far
+// V gathers evict-last, so the 10% uniform columns find V in L2 more often.
+__device__ __forceinline__ uint32_t ldg_u16_hint(const uint16_t* p, uint64_t pol) {
+  unsigned short v;
+  asm("ld.global.nc.L2::cache_hint.u16 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ldg_f64_hint(const double* p, uint64_t pol) {
+  double v;
+  asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int32_t ldg_s32_hint(const int32_t* p, uint64_t pol) {
+  int32_t v;
+  asm("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
+// One warp walks its jagged-diagonal segment of tile t, kTiledU steps in flight,
+// branch-free: lanes past their count re-load the segment's first entry and add
+// 0.0.  Each product goes straight into its row's shared-memory sum (rows are
+// thread-private), so a row's sum is one sequential left-to-right sum over its
+// near entries in column order, then its far entries — deterministic, 1e-13
+// relative to numpy's reduceat like the register kernels.
+template <bool FAR, int kTiledU>
+__device__ __forceinline__ void tiled_segment(const TiledArgs& a, int64_t ebase, int seg, int cnt,
+                                              const double* vt, int64_t far_off, double* rs,
+                                              uint64_t pol_s, uint64_t pol_v) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const int maxc = __reduce_max_sync(kFull, (unsigned)cnt);
+  const uint16_t* __restrict__ tkw = a.tk + ebase + seg;
+  const double* __restrict__ tvw = a.tv + ebase + seg;
+  const int32_t* __restrict__ fcw = FAR ? a.tfc + far_off : nullptr;
+  double* rst = rs + tid;
+  int off = 0;
+  for (int k0 = 0; k0 < maxc; k0 += kTiledU) {
+    uint32_t key[kTiledU];
+    int32_t fcol[kTiledU];
+    double vv[kTiledU];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int e = c0 + 32 * u + lane;
-      key[u] = 0xffffffffu;
-      vv[u] = 0.0;
-      if (e < e_hi) {
-        key[u] = __ldg(a.tk + ebase + e);
-        vv[u] = __ldg(a.tv + ebase + e);
-      }
+    for (int u = 0; u < kTiledU; ++u) {
+      const bool act = k0 + u < cnt;
+      const unsigned bal = __ballot_sync(kFull, act);
+      const int o = act ? off + __popc(bal & lt) : 0;
+      off += __popc(bal);
+      key[u] = ldg_u16_hint(tkw + o, pol_s);
+      vv[u] = ldg_f64_hint(tvw + o, pol_s);
+      if (FAR) fcol[u] = ldg_s32_hint(fcw + o, pol_s);
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int e = c0 + 32 * u + lane;
-      x[u] = 0.0;
-      if (e < e_hi) x[u] = FAR ? __ldg(a.v + __ldg(a.tfc + far_off + (e - e_lo))) : vt[key[u] & 8191u];
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {  // chunks in order: deterministic row partials
-      const int e = c0 + 32 * u + lane;
-      const bool act = e < e_hi;
-      double p = act ? mul_rn(vv[u], x[u]) : 0.0;
-      const uint32_t row = key[u] >> 13;
-      // segmented inclusive scan over the chunk (rows are sorted within it)
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const double o = __shfl_up_sync(kFull, p, d);
-        const uint32_t orow = __shfl_up_sync(kFull, row, d);
-        if (lane >= d && orow == row) p = add_rn(o, p);
-      }
-      const uint32_t nrow = __shfl_down_sync(kFull, row, 1);
-      if (act && (lane == 31 || e + 1 >= e_hi || nrow != row)) acc[row] = add_rn(acc[row], p);
+    for (int u = 0; u < kTiledU; ++u) {
+      const double x = FAR ? ldg_f64_hint(a.v + fcol[u], pol_v) : vt[key[u] & 8191u];
+      const double p = k0 + u < cnt ? mul_rn(vv[u], x) : 0.0;
+      double* d = rst + (key[u] >> 13) * kTiledNT;
+      *d = add_rn(*d, p);
     }
   }
 }
 
-__global__ void __launch_bounds__(kTiledNW * 32, 1) k1_bellman_tiled(TiledArgs a) {
+__global__ void __launch_bounds__(kTiledNT, 1) k1_bellman_tiled(TiledArgs a) {
   extern __shared__ __align__(16) double tsm[];
   __shared__ double red[32];
-  double* vt = tsm;                       // 2 x kTileW
-  double* acc = tsm + 2 * kTileW;         // bs * m row sums
-  int32_t* sp = reinterpret_cast<int32_t*>(acc + (int64_t)a.bs * a.m);  // splits of the block
+  double* vt = tsm;                        // 2 x kTileW
+  double* rs = tsm + 2 * kTileW;           // [rpl][NT] row sums (row q = tid * rpl + r)
+  int32_t* sp = reinterpret_cast<int32_t*>(rs + (int64_t)a.rpl * kTiledNT);  // splits of the block
   const int T1 = a.T + 1;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool mx = a.maximize != 0;
   const uint32_t vt_s = (uint32_t)__cvta_generic_to_shared(vt);
+  const uint64_t pol_s = policy_evict_first(), pol_v = policy_evict_last();
   double res = 0.0;
   for (int64_t b = blockIdx.x; b < a.nblocks; b += gridDim.x) {
     int64_t s0, s1, cs, ce;
     block_span(a, b, s0, s1, cs, ce);
-    const int nrows = (int)((s1 - s0) * a.m);
     const int64_t ebase = s0 * a.m * (int64_t)a.K;
     const int nt = (int)((ce - cs + kTileW - 1) / kTileW);
     __syncthreads();  // previous block fully consumed
-    for (int i = threadIdx.x; i < nrows; i += blockDim.x) acc[i] = 0.0;
-    const int32_t* mb = a.meta + b * (int64_t)T1 * (kTiledNW + 1);
-    for (int i = threadIdx.x; i < T1 * (kTiledNW + 1); i += blockDim.x) sp[i] = mb[i];
+    for (int i = tid; i < a.rpl * kTiledNT; i += blockDim.x) rs[i] = 0.0;
+    const int32_t* mb = a.meta + b * tiled_meta_stride(a.T);
+    const uint16_t* cg = reinterpret_cast<const uint16_t*>(mb + (int64_t)T1 * (kTiledNW + 1));
+    for (int i = tid; i < T1 * (kTiledNW + 1); i += blockDim.x) sp[i] = mb[i];
     auto issue_tile = [&](int t) {
       const int64_t c0 = cs + (int64_t)t * kTileW;
       const int64_t len = ce - c0 < kTileW ? ce - c0 : kTileW;
       const uint32_t dst = vt_s + (uint32_t)((t & 1) * kTileW * 8);
-      for (int64_t i = threadIdx.x; i < len; i += blockDim.x) cp_async8(dst + (uint32_t)(8 * i), a.v + c0 + i);
+      for (int64_t i = tid; i < len; i += blockDim.x) cp_async8(dst + (uint32_t)(8 * i), a.v + c0 + i);
       cp_async_commit();
     };
     if (nt > 0) issue_tile(0);
     __syncthreads();
     for (int t = 0; t < nt; ++t) {
+      const int c = __ldg(cg + t * kTiledNT + tid);
       if (t + 1 < nt) {
         issue_tile(t + 1);
         cp_async_wait<1>();
@@ -226,13 +282,13 @@ __global__ void __launch_bounds__(kTiledNW * 32, 1) k1_bellman_tiled(TiledArgs a
         cp_async_wait<0>();
       }
       __syncthreads();  // tile t staged by every thread
-      tiled_segment<false>(a, ebase, sp[t * (kTiledNW + 1) + warp], sp[t * (kTiledNW + 1) + warp + 1],
-                           vt + (t & 1) * kTileW, 0, acc);
+      tiled_segment<false, kTiledUN>(a, ebase, sp[t * (kTiledNW + 1) + warp], c, vt + (t & 1) * kTileW, 0, rs, pol_s, pol_v);
       __syncthreads();  // tile t consumed before its buffer is refilled
     }
-    const int f_lo = sp[a.T * (kTiledNW + 1) + warp], f_hi = sp[a.T * (kTiledNW + 1) + warp + 1];
+    const int f_lo = sp[a.T * (kTiledNW + 1) + warp];
     const int far0 = sp[a.T * (kTiledNW + 1)];
-    tiled_segment<true>(a, ebase, f_lo, f_hi, nullptr, a.far_base[b] + (f_lo - far0), acc);
+    tiled_segment<true, kTiledUF>(a, ebase, f_lo, __ldg(cg + a.T * kTiledNT + tid), nullptr,
+                        a.far_base[b] + (f_lo - far0), rs, pol_s, pol_v);
     __syncthreads();
     // first-index argmin / argmax over each state's m rows (bellman.py:58-62)
     for (int64_t s = s0 + warp; s < s1; s += kTiledNW) {
@@ -240,9 +296,10 @@ __global__ void __launch_bounds__(kTiledNW * 32, 1) k1_bellman_tiled(TiledArgs a
       double bq = mx ? -INFINITY : INFINITY;
       int ba = INT_MAX;
       for (int act = lane; act < a.m; act += 32) {
-        const double q = add_rn(__ldg(a.cost + row0 + act), mul_rn(a.gamma, acc[(s - s0) * a.m + act]));
-        if (better(q, act, bq, ba, mx)) {
-          bq = q;
+        const int q = (int)((s - s0) * a.m + act);
+        const double q_sa = add_rn(__ldg(a.cost + row0 + act), mul_rn(a.gamma, rs[(q % a.rpl) * kTiledNT + q / a.rpl]));
+        if (better(q_sa, act, bq, ba, mx)) {
+          bq = q_sa;
           ba = act;
         }
       }
@@ -292,6 +349,7 @@ static TiledArgs tiled_args(const ipi_mdp* h) {
   a.K = h->plan.row_len_max;
   a.bs = h->tl_bs;
   a.T = h->tl_T;
+  a.rpl = (h->tl_bs * h->m + kTiledNT - 1) / kTiledNT;
   a.wt = h->tl_wt;
   a.nblocks = h->tl_nblocks;
   a.gamma = h->gamma;
@@ -299,7 +357,8 @@ static TiledArgs tiled_args(const ipi_mdp* h) {
 }
 
 int k1_tiled_smem(const ipi_mdp* h) {
-  return (2 * kTileW + h->tl_bs * h->m) * 8 + (h->tl_T + 1) * (kTiledNW + 1) * 4;
+  const int rpl = (h->tl_bs * h->m + kTiledNT - 1) / kTiledNT;
+  return (2 * kTileW + rpl * kTiledNT) * 8 + (h->tl_T + 1) * (kTiledNW + 1) * 4;
 }
 
 // Build the tiled layout for h (uniform rows, m * bs <= 8192).  Returns IPI_OK
@@ -309,25 +368,33 @@ int k1_tiled_build(ipi_mdp* h, int64_t wt, cudaStream_t st) {
   if (!h->plan.uniform_rows || K <= 0 || m > 8192 || h->n_local <= 0) return IPI_OK;
   int bs = 8192 / m;
   bs = bs > 512 ? 512 : bs;
+  const int rpl = (bs * m + kTiledNT - 1) / kTiledNT;  // <= 8: a 3-bit row tag
+  if (rpl * K >= 65536) return IPI_OK;                  // uint16 per-(tile, thread) counts
   const int64_t nblocks = (h->n_local + bs - 1) / bs;
   const int T = (int)((bs + 2 * wt + kTileW - 1) / kTileW);
-  if (T > 64) return IPI_OK;
+  if (T > 48) return IPI_OK;
   const int64_t nnz = h->plan.nnz;
   size_t fr = 0, tot = 0;
   cudaMemGetInfo(&fr, &tot);
-  const double need = 12.0 * nnz + 4.0 * nnz * 0.25 + 1e8;
+  const double need = 10.0 * nnz + 4.0 * nnz * 0.25 + 1e8;
   if (need > 0.9 * (double)fr) return IPI_OK;
+  const int cnt_smem = (T + 1) * kTiledNT * 2 + (T + 1) * kTiledNW * 4;
+  const int sct_smem = (T + 1) * kTiledNT * 4;
+  if (raise_smem_limit(tiled_count_kernel, cnt_smem) != cudaSuccess ||
+      raise_smem_limit(tiled_scatter_kernel, sct_smem) != cudaSuccess) {
+    cudaGetLastError();
+    return IPI_OK;
+  }
   h->tl_bs = bs;
   h->tl_T = T;
   h->tl_wt = wt;
   IPI_CUDA_TRY(cudaMalloc(&h->tl_val, sizeof(double) * nnz));
-  IPI_CUDA_TRY(cudaMalloc(&h->tl_key, sizeof(uint32_t) * nnz));
-  IPI_CUDA_TRY(cudaMalloc(&h->tl_meta, sizeof(int32_t) * nblocks * (T + 1) * (kTiledNW + 1)));
+  IPI_CUDA_TRY(cudaMalloc(&h->tl_key, sizeof(uint16_t) * nnz));
+  IPI_CUDA_TRY(cudaMalloc(&h->tl_meta, sizeof(int32_t) * nblocks * tiled_meta_stride(T)));
   IPI_CUDA_TRY(cudaMalloc(&h->tl_farbase, sizeof(int64_t) * (nblocks + 1)));
   h->tl_nblocks = nblocks;
   TiledArgs a = tiled_args(h);
-  const int cnt_smem = kTiledNW * (T + 1) * 4;
-  tiled_count_kernel<<<(int)nblocks, kTiledNW * 32, cnt_smem, st>>>(h->col, a, h->tl_meta, h->tl_farbase);
+  tiled_count_kernel<<<(int)nblocks, kTiledNT, cnt_smem, st>>>(h->col, a, h->tl_meta, h->tl_farbase);
   IPI_LAUNCH_CHECK();
   // exclusive prefix of the per-block far counts (host: nblocks values)
   std::vector<int64_t> fc(nblocks);
@@ -339,8 +406,8 @@ int k1_tiled_build(ipi_mdp* h, int64_t wt, cudaStream_t st) {
   IPI_CUDA_TRY(cudaMemcpyAsync(h->tl_farbase, fb.data(), sizeof(int64_t) * (nblocks + 1), cudaMemcpyHostToDevice, st));
   IPI_CUDA_TRY(cudaMalloc(&h->tl_farcol, sizeof(int32_t) * (fb[nblocks] > 0 ? fb[nblocks] : 1)));
   a = tiled_args(h);
-  tiled_scatter_kernel<<<(int)nblocks, kTiledNW * 32, cnt_smem, st>>>(h->col, h->val, a, h->tl_val,
-                                                                       h->tl_key, h->tl_farcol);
+  tiled_scatter_kernel<<<(int)nblocks, kTiledNT, sct_smem, st>>>(h->col, h->val, a, h->tl_val,
+                                                                  h->tl_key, h->tl_farcol);
   IPI_LAUNCH_CHECK();
   IPI_CUDA_TRY(cudaStreamSynchronize(st));
   const int smem = k1_tiled_smem(h);
@@ -377,7 +444,7 @@ int launch_bellman_tiled(ipi_mdp* h, const double* v_full, int32_t mode, int32_t
   a.lenpi = len_pi;
   a.res_bits = res_bits;
   const int grid = (int)std::min<int64_t>(h->tl_nblocks, (int64_t)h->num_sms);
-  k1_bellman_tiled<<<grid, kTiledNW * 32, k1_tiled_smem(h), st>>>(a);
+  k1_bellman_tiled<<<grid, kTiledNT, k1_tiled_smem(h), st>>>(a);
   IPI_LAUNCH_CHECK();
   return IPI_OK;
 }

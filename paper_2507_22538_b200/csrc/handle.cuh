@@ -53,7 +53,7 @@ struct ipi_mdp {
   unsigned long long* k1_trace = nullptr;  // diagnostics (ipi_mdp_k1_trace)
   // variant 9: column-tiled layout of the shard (bellman_tiled.cu)
   double* tl_val = nullptr;
-  uint32_t* tl_key = nullptr;
+  uint16_t* tl_key = nullptr;
   int32_t* tl_farcol = nullptr;
   int64_t* tl_farbase = nullptr;
   int32_t* tl_meta = nullptr;

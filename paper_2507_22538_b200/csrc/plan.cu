@@ -610,7 +610,7 @@ static int plan_tiled(PlanCtx& c) {
   if (best == 1) {
     p.k1_variant = 9;
     p.k1_blocks = (int32_t)std::min<int64_t>(h->tl_nblocks, h->num_sms);
-    p.k1_threads = 16 * 32;
+    p.k1_threads = 1024;
     p.k1_smem_bytes = k1_tiled_smem(h);
   } else {
     k1_tiled_free(h);
