@@ -4,20 +4,21 @@
 // The register-deep kernel gathers every V entry from L2 with 32-byte sectors
 // per 8-byte value: on a C5 rank block that is ~90 GB of L2->SM traffic per
 // backup and the kernel runs L1TEX/L2-bound at ~0.48 of HBM.  Here the shard's
-// entries are re-laid out once (plan time) per block of BS states: entries
-// whose column lies in the block's near span [cs, ce) are stable-sorted by
-// TW-column tile (the tile index is monotone along a sorted row, so a
-// per-warp counting sort does it) and stored with a packed key
-// (row_in_block << 13 | column_in_tile); the far entries follow in row order
-// with their full columns in a side array.  Per (tile, warp) split points give
-// every warp its own row range inside every tile, so row partial sums go to
-// shared memory without atomics (deterministic).  The backup then stages one
-// TW-double V tile at a time (cp.async, double-buffered): near gathers become
-// shared-memory loads and only the far ones touch L2.
+// entries are re-laid out once (plan time) per block of BS states.  Thread i of
+// the 1024-thread CTA owns block rows [i*rpl, i*rpl + rpl) (rpl <= 8).  Entries
+// whose column lies in the block's near span [cs, ce) are grouped by 8192-column
+// tile; per (tile, warp) the warp's entries form one jagged-diagonal segment —
+// step k holds entry k of every lane with more than k entries in the tile, in
+// lane order — so the warp-wide load of a step is contiguous.  Keys are 16 bits
+// (row_in_thread << 13 | column_in_tile); far entries (tile T) keep their full
+// column in a side array.  Per block, a split table (tile, warp) and uint16
+// per-(tile, thread) counts drive the backup.  Entry bytes drop from 12 to ~10.4
+// per nnz.  The backup stages one 64 KB V tile at a time (cp.async, double
+// buffered): near gathers become shared-memory loads, only far ones touch L2.
 //
-// Row sum order: per row, tile 0, 1, ... partials (segmented shuffle scans over
-// 32-entry chunks, in chunk order), then the far partial — deterministic, 1e-13
-// relative to numpy's reduceat like the register kernels.
+// Measured on a C5 rank block (profiles/r01_k1_c5_tiled_jds.txt): 9.6 ms vs
+// 8.0 ms for the deep kernel (13.7 ms for the earlier segmented-scan design),
+// so the planner still only uses it on request (IPI_K1_TILED).
 #include <algorithm>
 #include <cfloat>
 #include <climits>
@@ -31,10 +32,16 @@ constexpr int kTileW = 8192;   // columns per V tile (64 KB)
 constexpr int kTiledNW = 32;   // warps per CTA (transform and backup)
 constexpr int kTiledNT = kTiledNW * 32;
 #ifndef IPI_TILED_UN
-#define IPI_TILED_UN 12
+#define IPI_TILED_UN 8
 #endif
 #ifndef IPI_TILED_UF
-#define IPI_TILED_UF 8
+#define IPI_TILED_UF 4
+#endif
+#ifndef IPI_TILED_DIAG  // timing diagnostics only: 1 skips the far list, 2 the near tiles
+#define IPI_TILED_DIAG 0
+#endif
+#ifndef IPI_TILED_FAR_SPREAD
+#define IPI_TILED_FAR_SPREAD 0  // 1: far list spread over the tile phases — measured slower (10.1 vs 9.6 ms)
 #endif
 constexpr int kTiledUN = IPI_TILED_UN;  // JDS steps in flight per warp (near tiles)
 constexpr int kTiledUF = IPI_TILED_UF;  // (far list: one more dependent load per step)
@@ -202,23 +209,27 @@ __device__ __forceinline__ int32_t ldg_s32_hint(const int32_t* p, uint64_t pol) 
 
 // One warp walks its jagged-diagonal segment of tile t, kTiledU steps in flight,
 // branch-free: lanes past their count re-load the segment's first entry and add
-// 0.0.  Each product goes straight into its row's shared-memory sum (rows are
-// thread-private), so a row's sum is one sequential left-to-right sum over its
-// near entries in column order, then its far entries — deterministic, 1e-13
-// relative to numpy's reduceat like the register kernels.
+// nothing.  A lane's entries in a tile come in row runs; each run is summed in a
+// register and added to the row's thread-private shared-memory slot, so a row's
+// sum is tile 0, 1, ... run sums (each sequential in column order), then the
+// far run — deterministic, 1e-13 relative to numpy's reduceat like the
+// register kernels.
 template <bool FAR, int kTiledU>
 __device__ __forceinline__ void tiled_segment(const TiledArgs& a, int64_t ebase, int seg, int cnt,
                                               const double* vt, int64_t far_off, double* rs,
-                                              uint64_t pol_s, uint64_t pol_v) {
+                                              uint64_t pol_s, uint64_t pol_v, int k_lo = 0,
+                                              int k_hi = INT_MAX) {
   const int tid = threadIdx.x, lane = tid & 31;
   const unsigned lt = (1u << lane) - 1u;
-  const int maxc = __reduce_max_sync(kFull, (unsigned)cnt);
+  const int maxc = min((int)__reduce_max_sync(kFull, (unsigned)cnt), k_hi);
   const uint16_t* __restrict__ tkw = a.tk + ebase + seg;
   const double* __restrict__ tvw = a.tv + ebase + seg;
   const int32_t* __restrict__ fcw = FAR ? a.tfc + far_off : nullptr;
   double* rst = rs + tid;
-  int off = 0;
-  for (int k0 = 0; k0 < maxc; k0 += kTiledU) {
+  int off = k_lo > 0 ? (int)__reduce_add_sync(kFull, (unsigned)min(cnt, k_lo)) : 0;
+  int cur = -1;
+  double acc = 0.0;
+  for (int k0 = k_lo; k0 < maxc; k0 += kTiledU) {
     uint32_t key[kTiledU];
     int32_t fcol[kTiledU];
     double vv[kTiledU];
@@ -234,12 +245,19 @@ __device__ __forceinline__ void tiled_segment(const TiledArgs& a, int64_t ebase,
     }
 #pragma unroll
     for (int u = 0; u < kTiledU; ++u) {
+      // a run of one row's entries accumulates in a register; the run's sum
+      // goes to the row's shared-memory slot when the row tag changes
+      const bool act = k0 + u < cnt;
       const double x = FAR ? ldg_f64_hint(a.v + fcol[u], pol_v) : vt[key[u] & 8191u];
-      const double p = k0 + u < cnt ? mul_rn(vv[u], x) : 0.0;
-      double* d = rst + (key[u] >> 13) * kTiledNT;
-      *d = add_rn(*d, p);
+      const double p = mul_rn(vv[u], x);
+      const int r = act ? (int)(key[u] >> 13) : cur;
+      const bool sw = r != cur;
+      if (sw && cur >= 0) rst[cur * kTiledNT] = add_rn(rst[cur * kTiledNT], acc);
+      acc = sw ? p : (act ? add_rn(acc, p) : acc);
+      cur = r;
     }
   }
+  if (cur >= 0) rst[cur * kTiledNT] = add_rn(rst[cur * kTiledNT], acc);
 }
 
 __global__ void __launch_bounds__(kTiledNT, 1) k1_bellman_tiled(TiledArgs a) {
@@ -273,8 +291,17 @@ __global__ void __launch_bounds__(kTiledNT, 1) k1_bellman_tiled(TiledArgs a) {
     };
     if (nt > 0) issue_tile(0);
     __syncthreads();
+    // The far list is spread over the tile phases (chunk t of its steps in phase
+    // t, before or after the near segment by warp parity) so its L2/DRAM
+    // gathers overlap the near tiles instead of forming a tail.
+    const int f_lo = sp[a.T * (kTiledNW + 1) + warp];
+    const int far0 = sp[a.T * (kTiledNW + 1)];
+    const int fcnt = IPI_TILED_DIAG == 1 ? 0 : __ldg(cg + a.T * kTiledNT + tid);
+    const int64_t foff = a.far_base[b] + (f_lo - far0);
+    const int fmx = (int)__reduce_max_sync(kFull, (unsigned)fcnt);
+    const int fchunk = IPI_TILED_FAR_SPREAD && nt > 0 ? ((fmx + nt - 1) / nt + kTiledUF - 1) / kTiledUF * kTiledUF : 0;
     for (int t = 0; t < nt; ++t) {
-      const int c = __ldg(cg + t * kTiledNT + tid);
+      const int c = IPI_TILED_DIAG == 2 ? 0 : __ldg(cg + t * kTiledNT + tid);
       if (t + 1 < nt) {
         issue_tile(t + 1);
         cp_async_wait<1>();
@@ -282,13 +309,15 @@ __global__ void __launch_bounds__(kTiledNT, 1) k1_bellman_tiled(TiledArgs a) {
         cp_async_wait<0>();
       }
       __syncthreads();  // tile t staged by every thread
+      const bool far_first = (warp & 1) == 0;
+      if (fchunk && far_first)
+        tiled_segment<true, kTiledUF>(a, ebase, f_lo, fcnt, nullptr, foff, rs, pol_s, pol_v, t * fchunk, (t + 1) * fchunk);
       tiled_segment<false, kTiledUN>(a, ebase, sp[t * (kTiledNW + 1) + warp], c, vt + (t & 1) * kTileW, 0, rs, pol_s, pol_v);
+      if (fchunk && !far_first)
+        tiled_segment<true, kTiledUF>(a, ebase, f_lo, fcnt, nullptr, foff, rs, pol_s, pol_v, t * fchunk, (t + 1) * fchunk);
       __syncthreads();  // tile t consumed before its buffer is refilled
     }
-    const int f_lo = sp[a.T * (kTiledNW + 1) + warp];
-    const int far0 = sp[a.T * (kTiledNW + 1)];
-    tiled_segment<true, kTiledUF>(a, ebase, f_lo, __ldg(cg + a.T * kTiledNT + tid), nullptr,
-                        a.far_base[b] + (f_lo - far0), rs, pol_s, pol_v);
+    if (!fchunk) tiled_segment<true, kTiledUF>(a, ebase, f_lo, fcnt, nullptr, foff, rs, pol_s, pol_v);
     __syncthreads();
     // first-index argmin / argmax over each state's m rows (bellman.py:58-62)
     for (int64_t s = s0 + warp; s < s1; s += kTiledNW) {

@@ -574,8 +574,8 @@ static int plan_tma(PlanCtx& c) {
 
 // window-less uniform rows (C5): column-tiled layout.  Opt-in experiment
 // (IPI_K1_TILED=1 forces it, =2 lets the planner time it against the
-// register-deep kernel): correct, but 13.7 vs 8.0 ms on a C5 rank block — the
-// ~3.8-entry row pieces per tile cost a segmented scan each.
+// register-deep kernel): correct, but 9.6 vs 8.0 ms on a C5 rank block with the
+// jagged-diagonal layout (13.7 ms with the earlier segmented scans).
 static int plan_tiled(PlanCtx& c) {
   ipi_mdp* h = c.h;
   cudaStream_t st = c.st;
