@@ -29,7 +29,15 @@
 namespace ipi {
 
 constexpr int kTileW = 8192;   // columns per V tile (64 KB)
-constexpr int kTiledNW = 32;   // warps per CTA (transform and backup)
+#ifndef IPI_TILED_NW
+#define IPI_TILED_NW 32
+#endif
+#ifndef IPI_TILED_NBUF
+#define IPI_TILED_NBUF 2
+#endif
+constexpr int kTiledNW = IPI_TILED_NW;      // warps per CTA (transform and backup)
+constexpr int kTiledNBuf = IPI_TILED_NBUF;  // V tile buffers (1: two CTAs per SM overlap instead)
+constexpr int kTiledCTAs = 1024 / (kTiledNW * 32);  // resident CTAs per SM the kernel is built for
 constexpr int kTiledNT = kTiledNW * 32;
 #ifndef IPI_TILED_UN
 #define IPI_TILED_UN 8
@@ -260,11 +268,11 @@ __device__ __forceinline__ void tiled_segment(const TiledArgs& a, int64_t ebase,
   if (cur >= 0) rst[cur * kTiledNT] = add_rn(rst[cur * kTiledNT], acc);
 }
 
-__global__ void __launch_bounds__(kTiledNT, 1) k1_bellman_tiled(TiledArgs a) {
+__global__ void __launch_bounds__(kTiledNT, kTiledCTAs) k1_bellman_tiled(TiledArgs a) {
   extern __shared__ __align__(16) double tsm[];
   __shared__ double red[32];
   double* vt = tsm;                        // 2 x kTileW
-  double* rs = tsm + 2 * kTileW;           // [rpl][NT] row sums (row q = tid * rpl + r)
+  double* rs = tsm + kTiledNBuf * kTileW;  // [rpl][NT] row sums (row q = tid * rpl + r)
   int32_t* sp = reinterpret_cast<int32_t*>(rs + (int64_t)a.rpl * kTiledNT);  // splits of the block
   const int T1 = a.T + 1;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -285,7 +293,7 @@ __global__ void __launch_bounds__(kTiledNT, 1) k1_bellman_tiled(TiledArgs a) {
     auto issue_tile = [&](int t) {
       const int64_t c0 = cs + (int64_t)t * kTileW;
       const int64_t len = ce - c0 < kTileW ? ce - c0 : kTileW;
-      const uint32_t dst = vt_s + (uint32_t)((t & 1) * kTileW * 8);
+      const uint32_t dst = vt_s + (uint32_t)((t % kTiledNBuf) * kTileW * 8);
       for (int64_t i = tid; i < len; i += blockDim.x) cp_async8(dst + (uint32_t)(8 * i), a.v + c0 + i);
       cp_async_commit();
     };
@@ -302,7 +310,7 @@ __global__ void __launch_bounds__(kTiledNT, 1) k1_bellman_tiled(TiledArgs a) {
     const int fchunk = IPI_TILED_FAR_SPREAD && nt > 0 ? ((fmx + nt - 1) / nt + kTiledUF - 1) / kTiledUF * kTiledUF : 0;
     for (int t = 0; t < nt; ++t) {
       const int c = IPI_TILED_DIAG == 2 ? 0 : __ldg(cg + t * kTiledNT + tid);
-      if (t + 1 < nt) {
+      if (kTiledNBuf == 2 && t + 1 < nt) {
         issue_tile(t + 1);
         cp_async_wait<1>();
       } else {
@@ -312,10 +320,11 @@ __global__ void __launch_bounds__(kTiledNT, 1) k1_bellman_tiled(TiledArgs a) {
       const bool far_first = (warp & 1) == 0;
       if (fchunk && far_first)
         tiled_segment<true, kTiledUF>(a, ebase, f_lo, fcnt, nullptr, foff, rs, pol_s, pol_v, t * fchunk, (t + 1) * fchunk);
-      tiled_segment<false, kTiledUN>(a, ebase, sp[t * (kTiledNW + 1) + warp], c, vt + (t & 1) * kTileW, 0, rs, pol_s, pol_v);
+      tiled_segment<false, kTiledUN>(a, ebase, sp[t * (kTiledNW + 1) + warp], c, vt + (t % kTiledNBuf) * kTileW, 0, rs, pol_s, pol_v);
       if (fchunk && !far_first)
         tiled_segment<true, kTiledUF>(a, ebase, f_lo, fcnt, nullptr, foff, rs, pol_s, pol_v, t * fchunk, (t + 1) * fchunk);
       __syncthreads();  // tile t consumed before its buffer is refilled
+      if (kTiledNBuf == 1 && t + 1 < nt) issue_tile(t + 1);
     }
     if (!fchunk) tiled_segment<true, kTiledUF>(a, ebase, f_lo, fcnt, nullptr, foff, rs, pol_s, pol_v);
     __syncthreads();
@@ -387,15 +396,15 @@ static TiledArgs tiled_args(const ipi_mdp* h) {
 
 int k1_tiled_smem(const ipi_mdp* h) {
   const int rpl = (h->tl_bs * h->m + kTiledNT - 1) / kTiledNT;
-  return (2 * kTileW + rpl * kTiledNT) * 8 + (h->tl_T + 1) * (kTiledNW + 1) * 4;
+  return (kTiledNBuf * kTileW + rpl * kTiledNT) * 8 + (h->tl_T + 1) * (kTiledNW + 1) * 4;
 }
 
 // Build the tiled layout for h (uniform rows, m * bs <= 8192).  Returns IPI_OK
 // with h->tl_nblocks == 0 when it does not apply or memory is short.
 int k1_tiled_build(ipi_mdp* h, int64_t wt, cudaStream_t st) {
   const int K = h->plan.row_len_max, m = h->m;
-  if (!h->plan.uniform_rows || K <= 0 || m > 8192 || h->n_local <= 0) return IPI_OK;
-  int bs = 8192 / m;
+  if (!h->plan.uniform_rows || K <= 0 || m > 8 * kTiledNT || h->n_local <= 0) return IPI_OK;
+  int bs = 8 * kTiledNT / m;  // rpl <= 8
   bs = bs > 512 ? 512 : bs;
   const int rpl = (bs * m + kTiledNT - 1) / kTiledNT;  // <= 8: a 3-bit row tag
   if (rpl * K >= 65536) return IPI_OK;                  // uint16 per-(tile, thread) counts
@@ -472,7 +481,7 @@ int launch_bellman_tiled(ipi_mdp* h, const double* v_full, int32_t mode, int32_t
   a.gpi = g_pi;
   a.lenpi = len_pi;
   a.res_bits = res_bits;
-  const int grid = (int)std::min<int64_t>(h->tl_nblocks, (int64_t)h->num_sms);
+  const int grid = (int)std::min<int64_t>(h->tl_nblocks, (int64_t)h->num_sms * kTiledCTAs);
   k1_bellman_tiled<<<grid, kTiledNT, k1_tiled_smem(h), st>>>(a);
   IPI_LAUNCH_CHECK();
   return IPI_OK;
