@@ -50,6 +50,18 @@ extern "C" {
 #define IPI_PC_NONE 0
 #define IPI_PC_JACOBI 1
 
+/* GMRES Arnoldi orthogonalisation.  The reference uses modified Gram-Schmidt
+ * (inner.py:251-253): j+2 dependent reductions per step, one pass over the
+ * basis.  CGS2 is classical Gram-Schmidt with one re-orthogonalisation when
+ * the DGKS test asks for it (PETSc's KSPGMRESClassicalGramSchmidtOrthogonalization
+ * with refine_ifneeded, the library madupite runs on): 2 reductions per step
+ * but 2-4 passes over the basis.  AUTO picks MGS where a pass over the basis
+ * costs more than a grid reduction (large systems) and CGS2 where the
+ * reductions dominate (small systems). */
+#define IPI_ORTHO_AUTO 0 /* default */
+#define IPI_ORTHO_MGS 1
+#define IPI_ORTHO_CGS2 2
+
 /* outer status (driver.py:41-44) */
 #define IPI_CONVERGED 0
 #define IPI_OUTER_CAP 1
@@ -84,6 +96,8 @@ typedef struct {
   double richardson_scale; /* -ksp_richardson_scale */
   int32_t mode;            /* IPI_MODE_* */
   int32_t pc_type;         /* -pc_type: IPI_PC_NONE or IPI_PC_JACOBI */
+  int32_t gmres_ortho;     /* IPI_ORTHO_* (-ksp_gmres_modifiedgramschmidt / _classicalgramschmidt) */
+  int32_t reserved;
 } ipi_opts;
 
 /* Solve statistics (driver.py:93-106 SolveResult minus the arrays). */
@@ -264,13 +278,24 @@ int ipi_col_range(const int32_t* col, int64_t nnz, int64_t* cmin, int64_t* cmax,
  * (build_preconditioner JACOBI, inner.py:115-118). */
 int ipi_jacobi_inv_diag(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi,
                         int64_t n, double gamma, double* inv_diag, void* stream);
+/* Diagnostics: enable = 1 makes later persistent inner solves record CTA 0's
+ * %globaltimer at phase boundaries (out[0] = count, out[1..] = ns); enable = 0
+ * copies up to cap entries into out (host) and stops recording. */
+int ipi_k4_trace(int32_t enable, uint64_t* out, int32_t cap);
+/* Diagnostics: the uniform ring SpMV of the persistent kernel as a plain
+ * kernel, y = x - gamma P x (K = 64 rows), timed over reps launches. */
+int ipi_k4_ring_apply_test(const int32_t* col, const double* val, int64_t n, double gamma,
+                           const double* x, double* y, int32_t reps, float* ms, void* stream);
 /* Solve (I - gamma P_pi) x = b from x (in/out) to the floored 2-norm target
  * or max_it iterations, one persistent cooperative kernel per call.
- * inv_diag == NULL: pc = identity; else left Jacobi preconditioning. */
+ * inv_diag == NULL: pc = identity; else left Jacobi preconditioning.
+ * ortho: IPI_ORTHO_* (GMRES only).  The Krylov workspace is one arena per
+ * (device, stream): concurrent calls must use different streams. */
 int ipi_inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi, int64_t n,
                     double gamma, const double* b, double* x, double target_2norm,
                     int32_t max_it, int32_t kind, double richardson_scale,
-                    const double* inv_diag, ipi_inner_report* report, void* stream);
+                    const double* inv_diag, int32_t ortho, ipi_inner_report* report,
+                    void* stream);
 
 /* ---- outer iPI loop (driver.py:109-209) ------------------------------- */
 /* v (device, n) holds V0 on entry and the final V on exit; policy (device,

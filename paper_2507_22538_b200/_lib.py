@@ -8,6 +8,7 @@ loaded, and every compute entry point goes through it.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
@@ -21,6 +22,7 @@ IPI_OK, IPI_EVALIDATION, IPI_EDIMENSION, IPI_ECUDA, IPI_ERESOURCE = 0, 1, 2, 3, 
 MODE_MIN, MODE_MAX = 0, 1
 KSP = {"richardson": 0, "gmres": 1, "bicgstab": 2, "tfqmr": 3}
 PC = {"none": 0, "jacobi": 1}
+ORTHO = {"auto": 0, "mgs": 1, "cgs2": 2}
 STATUS = {0: "converged", 1: "outer_cap", 2: "stalled"}
 
 _p = C.c_void_p
@@ -37,7 +39,7 @@ class InnerReport(C.Structure):
 class Opts(C.Structure):
     _fields_ = [("tol", _f64), ("alpha", _f64), ("max_outer", _i32), ("max_inner", _i32),
                 ("ksp_type", _i32), ("ksp_max_it", _i32), ("richardson_scale", _f64),
-                ("mode", _i32), ("pc_type", _i32)]
+                ("mode", _i32), ("pc_type", _i32), ("gmres_ortho", _i32), ("reserved", _i32)]
 
 
 class Stats(C.Structure):
@@ -110,7 +112,9 @@ _SIGS = {
     "ipi_mgs_pass": (C.c_int, [_p, _i32, _p, _p, _p, _p, _i64, _p, _p]),
     "ipi_jacobi_inv_diag": (C.c_int, [_p, _p, _p, _i64, _f64, _p, _p]),
     "ipi_inner_solve": (C.c_int, [_p, _p, _p, _i64, _f64, _p, _p, _f64, _i32, _i32, _f64, _p,
-                                  C.POINTER(InnerReport), _p]),
+                                  _i32, C.POINTER(InnerReport), _p]),
+    "ipi_k4_trace": (C.c_int, [_i32, _p, _i32]),
+    "ipi_k4_ring_apply_test": (C.c_int, [_p, _p, _i64, _f64, _p, _p, _i32, C.POINTER(C.c_float), _p]),
     "ipi_solve": (C.c_int, [_p, C.POINTER(Opts), _p, _p, _p, _i32, C.POINTER(Stats), _p]),
     "ipi_gen_locality": (C.c_int, [_i64, _i32, _i32, _i64, C.c_uint64, _i64, _i64, _p, _p, _p,
                                    _p, _p]),
@@ -128,7 +132,8 @@ def load(path: Path | str | None = None) -> C.CDLL:
     with _lock:
         if _lib is not None:
             return _lib
-        p = Path(path) if path else LIB_PATH
+        # IPI_LIB: an alternative build of the same ABI (A/B experiments only)
+        p = Path(path) if path else Path(os.environ.get("IPI_LIB", LIB_PATH))
         if not p.exists():
             raise RuntimeError(
                 f"{p.name} is not built ({p}); run `python -m paper_2507_22538_b200._build` "

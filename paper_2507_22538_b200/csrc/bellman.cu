@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_bellman(K1Args a) {
       if (a.gpi) a.gpi[s] = __ldg(a.cost + row0 + ba);
       if (a.lenpi) a.lenpi[s] = (int32_t)(__ldg(a.rp + row0 + ba + 1) - __ldg(a.rp + row0 + ba));
       const double vs = WIN ? gather((int)(a.state0 + s)) : __ldg(a.v + a.state0 + s);
-      res = fmax(res, fabs(sub_rn(vs, bq)));
+      res = res_max(res, fabs(sub_rn(vs, bq)));
     }
   }
   if (a.res_bits) {
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_bellman(K1Args a) {
     __syncthreads();
     if (threadIdx.x == 0) {
       double t = 0.0;
-      for (int w = 0; w < nwarps; ++w) t = fmax(t, red[w]);
+      for (int w = 0; w < nwarps; ++w) t = res_max(t, red[w]);
       // |v - Tv| >= 0: IEEE bit patterns of non-negative doubles are ordered,
       // so an integer max is an exact, order-independent max.
       atomicMax(a.res_bits, (unsigned long long)__double_as_longlong(t));
@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_bellman_uniform(K1Args a, int K
           if (a.gpi) a.gpi[s] = __ldg(a.cost + row0 + ba);
           if (a.lenpi) a.lenpi[s] = K;
           const double vs = WIN ? gather((int)(a.state0 + s)) : __ldg(a.v + a.state0 + s);
-          res = fmax(res, fabs(sub_rn(vs, bq)));
+          res = res_max(res, fabs(sub_rn(vs, bq)));
         }
         bq = mx ? -INFINITY : INFINITY;
         ba = INT_MAX;
@@ -294,7 +294,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_bellman_uniform(K1Args a, int K
     __syncthreads();
     if (threadIdx.x == 0) {
       double t = 0.0;
-      for (int w = 0; w < nwarps; ++w) t = fmax(t, red[w]);
+      for (int w = 0; w < nwarps; ++w) t = res_max(t, red[w]);
       atomicMax(a.res_bits, (unsigned long long)__double_as_longlong(t));
     }
   }
@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(kK1Threads, 2) k1_bellman_flat(K1Args a, int K
         a.applied[s] = q;
         if (a.gpi) a.gpi[s] = __ldg(a.cost + s * m + ba);
         if (a.lenpi) a.lenpi[s] = K;
-        res = fmax(res, fabs(sub_rn(gather((int)(a.state0 + s)), q)));
+        res = res_max(res, fabs(sub_rn(gather((int)(a.state0 + s)), q)));
       }
       carry_q = __shfl_sync(kFull, q, 31);
       carry_a = __shfl_sync(kFull, aa, 31);
@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(kK1Threads, 2) k1_bellman_flat(K1Args a, int K
     __syncthreads();
     if (threadIdx.x == 0) {
       double t = 0.0;
-      for (int w = 0; w < nwarps; ++w) t = fmax(t, red[w]);
+      for (int w = 0; w < nwarps; ++w) t = res_max(t, red[w]);
       atomicMax(a.res_bits, (unsigned long long)__double_as_longlong(t));
     }
   }
@@ -595,7 +595,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_bellman_ring(K1Args a, int win_
         a.applied[s] = bq;
         if (a.gpi) a.gpi[s] = __ldg(a.cost + s * m + ba);
         if (a.lenpi) a.lenpi[s] = K;
-        res = fmax(res, fabs(sub_rn(gather((int)(a.state0 + s)), bq)));
+        res = res_max(res, fabs(sub_rn(gather((int)(a.state0 + s)), bq)));
       }
       __syncwarp();
       bi = 0;
@@ -640,7 +640,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_bellman_ring(K1Args a, int win_
     __syncthreads();
     if (threadIdx.x == 0) {
       double t = 0.0;
-      for (int w = 0; w < NW; ++w) t = fmax(t, red[w]);
+      for (int w = 0; w < NW; ++w) t = res_max(t, red[w]);
       atomicMax(a.res_bits, (unsigned long long)__double_as_longlong(t));
     }
   }
@@ -892,7 +892,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_bellman_uring(K1Args a, int win
         a.applied[s] = ap;
         if (a.gpi) a.gpi[s] = __ldg(a.cost + s * m + pa);
         if (a.lenpi) a.lenpi[s] = K;
-        res = fmax(res, fabs(sub_rn(gather((int)(a.state0 + s)), ap)));
+        res = res_max(res, fabs(sub_rn(gather((int)(a.state0 + s)), ap)));
       }
       t_in_state = 0;
       s_cur = state_of(++kc);
@@ -951,7 +951,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_bellman_uring(K1Args a, int win
     __syncthreads();
     if (threadIdx.x == 0) {
       double t = 0.0;
-      for (int w = 0; w < NW; ++w) t = fmax(t, red[w]);
+      for (int w = 0; w < NW; ++w) t = res_max(t, red[w]);
       atomicMax(a.res_bits, (unsigned long long)__double_as_longlong(t));
     }
   }
@@ -1143,7 +1143,7 @@ __global__ void __launch_bounds__(kK1Threads, 1) k1_bellman_deep(K1Args a, int K
               a.applied[sC] = bq;
               if (a.gpi) a.gpi[sC] = __ldg(a.cost + row0 + ba);
               if (a.lenpi) a.lenpi[sC] = K;
-              res = fmax(res, fabs(sub_rn(gather((int)(a.state0 + sC)), bq)));
+              res = res_max(res, fabs(sub_rn(gather((int)(a.state0 + sC)), bq)));
             }
             bq = mx ? -INFINITY : INFINITY;
             ba = INT_MAX;
@@ -1163,7 +1163,7 @@ __global__ void __launch_bounds__(kK1Threads, 1) k1_bellman_deep(K1Args a, int K
     __syncthreads();
     if (threadIdx.x == 0) {
       double t = 0.0;
-      for (int w = 0; w < nwarps; ++w) t = fmax(t, red[w]);
+      for (int w = 0; w < nwarps; ++w) t = res_max(t, red[w]);
       atomicMax(a.res_bits, (unsigned long long)__double_as_longlong(t));
     }
   }
@@ -1287,8 +1287,6 @@ int launch_bellman(ipi_mdp* h, const double* v_full, int32_t mode, int32_t* poli
                    double* applied, double* g_pi, int32_t* len_pi,
                    unsigned long long* res_bits, cudaStream_t st) {
   if (h->n_local == 0) return IPI_OK;
-  if (h->use_tma)
-    return launch_bellman_tma(h, v_full, mode, policy, applied, g_pi, len_pi, res_bits, st);
   K1Args a;
   a.rp = h->rp;
   a.col = h->col;
@@ -1311,7 +1309,7 @@ int launch_bellman(ipi_mdp* h, const double* v_full, int32_t mode, int32_t* poli
   a.interleave = h->k1_interleave;
   a.rotate = h->k1_rotate;
   a.trace = h->k1_trace;
-  a.gen_u = getenv("IPI_K1_GEN_U") ? atoi(getenv("IPI_K1_GEN_U")) : 8;
+  a.gen_u = h->k1_gen_u;
   const bool win = h->plan.halo >= 0;
   const int blocks = h->plan.k1_blocks, smem = h->plan.k1_smem_bytes;
   int G = 0, P = 0;
@@ -1325,8 +1323,6 @@ int launch_bellman(ipi_mdp* h, const double* v_full, int32_t mode, int32_t* poli
     IPI_LAUNCH_CHECK();
     return IPI_OK;
   }
-  if (h->plan.k1_variant == 9)
-    return launch_bellman_tiled(h, v_full, mode, policy, applied, g_pi, len_pi, res_bits, st);
   if (h->plan.k1_variant == 6) {
     if (a.win_async && h->ring_win_bytes > 0 && (uintptr_t)v_full % 16 != 0) {
       // the window is staged in 16-byte cp.async chunks: realign V once

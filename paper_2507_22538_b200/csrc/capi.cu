@@ -290,6 +290,7 @@ int ipi_mdp_create(const int64_t* row_ptr, const int32_t* col, const double* val
   if (getenv("IPI_K1_WIN_ASYNC")) h->k1_win_async = atoi(getenv("IPI_K1_WIN_ASYNC")) != 0;
   if (getenv("IPI_K1_INTERLEAVE")) h->k1_interleave = atoi(getenv("IPI_K1_INTERLEAVE")) != 0;
   if (getenv("IPI_K1_ROTATE")) h->k1_rotate = atoi(getenv("IPI_K1_ROTATE")) != 0;
+  if (getenv("IPI_K1_GEN_U")) h->k1_gen_u = atoi(getenv("IPI_K1_GEN_U"));
   if (cudaMallocHost(&h->host_pinned, 4096) != cudaSuccess)
     return bail(fail(IPI_ECUDA, "cudaMallocHost failed"));
   const int rc = plan_instance(h, st);
@@ -301,7 +302,6 @@ int ipi_mdp_create(const int64_t* row_ptr, const int32_t* col, const double* val
 void ipi_mdp_destroy(ipi_mdp* h) {
   if (!h) return;
   cudaFree(h->k1_bounds);
-  cudaFree(h->tma_bounds);
   cudaFree(h->pi);
   cudaFree(h->applied);
   cudaFree(h->gpi);
@@ -317,7 +317,7 @@ void ipi_mdp_destroy(ipi_mdp* h) {
   cudaFree(h->invd);
   cudaFree(h->vbuf);
   cudaFree(h->k1_trace);
-  k1_tiled_free(h);
+  ipi_op_destroy(h->op_pi);
   if (h->host_pinned) cudaFreeHost(h->host_pinned);
   delete h;
 }
@@ -798,7 +798,8 @@ int ipi_jacobi_inv_diag(const int64_t* rp_pi, const int32_t* col_pi, const doubl
 int ipi_inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi, int64_t n,
                     double gamma, const double* b, double* x, double target_2norm,
                     int32_t max_it, int32_t kind, double richardson_scale,
-                    const double* inv_diag, ipi_inner_report* report, void* stream) {
+                    const double* inv_diag, int32_t ortho, ipi_inner_report* report,
+                    void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (n <= 0) return fail(IPI_EDIMENSION, "empty system");
   int64_t nnz = 0;
@@ -811,12 +812,22 @@ int ipi_inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* v
   if (rc) return rc;
   const ipi_plan pl = view->plan;
   ipi_mdp_destroy(view);
+  // the planned K3 operator carries the stepped GMRES's SpMV (uniform rows)
+  ipi_op* op = nullptr;
+  if (pl.uniform_rows && kind == IPI_KSP_GMRES) {
+    rc = ipi_op_create(rp_pi, col_pi, val_pi, n, n, 0, gamma, stream, &op);
+    if (rc) return rc;
+  }
   ipi_inner_report* d_rep = nullptr;
-  IPI_CUDA_TRY(cudaMalloc(&d_rep, sizeof(ipi_inner_report)));
+  if (cudaMalloc(&d_rep, sizeof(ipi_inner_report)) != cudaSuccess) {
+    ipi_op_destroy(op);
+    return fail(IPI_ECUDA, "cudaMalloc of the inner report failed");
+  }
   rc = inner_solve(rp_pi, col_pi, val_pi, n, gamma, b, x, target_2norm, max_it, kind,
                    richardson_scale, pl.lanes_per_row, pl.halo,
                    pl.uniform_rows ? pl.row_len_max : 0, d_rep, st, nullptr, 0, inv_diag,
-                   12.0 * (double)nnz + 8.0 * (double)(n + 1));
+                   12.0 * (double)nnz + 8.0 * (double)(n + 1), ortho, op);
+  ipi_op_destroy(op);
   if (rc == IPI_OK && report) {
     cudaError_t e = cudaMemcpyAsync(report, d_rep, sizeof(*report), cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
@@ -824,6 +835,15 @@ int ipi_inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* v
   }
   cudaFree(d_rep);
   return rc;
+}
+
+int ipi_k4_ring_apply_test(const int32_t* col, const double* val, int64_t n, double gamma,
+                           const double* x, double* y, int32_t reps, float* ms, void* stream) {
+  return ring_apply_test(col, val, n, gamma, x, y, reps, ms, (cudaStream_t)stream);
+}
+
+int ipi_k4_trace(int32_t enable, uint64_t* out, int32_t cap) {
+  return k4_trace(enable, reinterpret_cast<unsigned long long*>(out), cap);
 }
 
 // driver.py:109-209 — the outer loop, natively.  One host sync per outer
@@ -844,18 +864,28 @@ int ipi_solve(ipi_mdp* h, const ipi_opts* o, double* v, int32_t* policy, double*
   if (rc) return rc;
   const int64_t n = h->n_local;
   const auto t_start = std::chrono::steady_clock::now();
-  std::vector<cudaEvent_t> ev;
-  auto new_event = [&]() {
-    cudaEvent_t e;
-    cudaEventCreate(&e);
-    ev.push_back(e);
-    return e;
+  // Phase timing with six reused events (greedy, assembly, inner).  The
+  // residual read after every K1 synchronises the stream, so at that point
+  // this iteration's greedy phase and the previous iteration's assembly and
+  // inner phases are complete and can be accumulated; the events are then
+  // recorded again.  The guard destroys them on every exit path.
+  struct Events {
+    cudaEvent_t e[6] = {};
+    Events() {
+      for (auto& x : e) cudaEventCreate(&x);
+    }
+    ~Events() {
+      for (auto x : e) if (x) cudaEventDestroy(x);
+    }
+  } ev;
+  cudaEvent_t g0 = ev.e[0], g1 = ev.e[1], a0 = ev.e[2], a1 = ev.e[3], i0 = ev.e[4], i1 = ev.e[5];
+  double tg = 0, ta = 0, ti = 0;
+  bool pending_phases = false;
+  auto elapsed = [](cudaEvent_t x, cudaEvent_t y) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, x, y);
+    return ms * 1e-3;
   };
-  struct Phase {
-    cudaEvent_t a, b;
-    int kind;  // 0 greedy, 1 assembly, 2 inner
-  };
-  std::vector<Phase> phases;
   double* host = reinterpret_cast<double*>(h->host_pinned);
   ipi_inner_report* hrep = reinterpret_cast<ipi_inner_report*>(host + 8);
   std::vector<double> hist;
@@ -867,17 +897,21 @@ int ipi_solve(ipi_mdp* h, const ipi_opts* o, double* v, int32_t* policy, double*
   double* vnext = h->xbuf;
   bool pending_report = false;
   while (true) {
-    Phase pg{new_event(), new_event(), 0};
-    cudaEventRecord(pg.a, st);
+    cudaEventRecord(g0, st);
     IPI_CUDA_TRY(cudaMemsetAsync(h->res_bits, 0, sizeof(unsigned long long), st));
     rc = launch_bellman(h, vcur, o->mode, h->pi, h->applied, h->gpi, nullptr, h->res_bits, st);
     if (rc) return rc;
-    cudaEventRecord(pg.b, st);
-    phases.push_back(pg);
+    cudaEventRecord(g1, st);
     IPI_CUDA_TRY(cudaMemcpyAsync(host, h->res_bits, sizeof(double), cudaMemcpyDeviceToHost, st));
     if (pending_report)
       IPI_CUDA_TRY(cudaMemcpyAsync(hrep, h->d_report, sizeof(ipi_inner_report), cudaMemcpyDeviceToHost, st));
     IPI_CUDA_TRY(cudaStreamSynchronize(st));
+    tg += elapsed(g0, g1);
+    if (pending_phases) {
+      ta += elapsed(a0, a1);
+      ti += elapsed(i0, i1);
+      pending_phases = false;
+    }
     if (pending_report) {
       inner_total += hrep->iterations;
       pending_report = false;
@@ -900,8 +934,7 @@ int ipi_solve(ipi_mdp* h, const ipi_opts* o, double* v, int32_t* policy, double*
     } else {
       stall = 0;
     }
-    Phase pa{new_event(), new_event(), 1};
-    cudaEventRecord(pa.a, st);
+    cudaEventRecord(a0, st);
     rc = gather_policy(h, h->pi, nullptr, h->rp_pi, h->col_pi, h->val_pi, nullptr, nullptr, st);
     if (rc) return rc;
     if (o->pc_type == IPI_PC_JACOBI) {
@@ -909,8 +942,7 @@ int ipi_solve(ipi_mdp* h, const ipi_opts* o, double* v, int32_t* policy, double*
       rc = jacobi_inv_diag(h->rp_pi, h->col_pi, h->val_pi, n, h->gamma, h->invd, st);
       if (rc) return rc;
     }
-    cudaEventRecord(pa.b, st);
-    phases.push_back(pa);
+    cudaEventRecord(a1, st);
     double target;
     int cap;
     if (o->ksp_max_it > 0) {
@@ -920,14 +952,20 @@ int ipi_solve(ipi_mdp* h, const ipi_opts* o, double* v, int32_t* policy, double*
       target = o->alpha * res;
       cap = o->max_inner;
     }
-    Phase pi_{new_event(), new_event(), 2};
-    cudaEventRecord(pi_.a, st);
+    cudaEventRecord(i0, st);
     IPI_CUDA_TRY(cudaMemcpyAsync(vnext, vcur, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    if (!h->op_pi && h->plan.uniform_rows && o->ksp_type == IPI_KSP_GMRES) {
+      // planned once per handle: P_pi always lives in the same scratch with the
+      // same uniform geometry; only its contents change between iterations
+      rc = ipi_op_create(h->rp_pi, h->col_pi, h->val_pi, n, n, 0, h->gamma, stream, &h->op_pi);
+      if (rc) return rc;
+    }
     rc = inner_solve(h->rp_pi, h->col_pi, h->val_pi, n, h->gamma, h->gpi, vnext, target, cap,
                      o->ksp_type, o->richardson_scale, h->plan.lanes_per_row, h->plan.halo,
                      h->plan.uniform_rows ? h->plan.row_len_max : 0, h->d_report, st, h->kry,
                      h->kry_len, o->pc_type == IPI_PC_JACOBI ? h->invd : nullptr,
-                     (12.0 * h->plan.row_len_mean + 8.0) * (double)n);  // P_pi size estimate
+                     (12.0 * h->plan.row_len_mean + 8.0) * (double)n,  // P_pi size estimate
+                     o->gmres_ortho, h->op_pi);
     if (rc) return rc;
     if (o->ksp_type == IPI_KSP_TFQMR || o->ksp_type == IPI_KSP_BICGSTAB) {
       // these kinds can break down: read the report now (driver.py:189-193)
@@ -944,8 +982,8 @@ int ipi_solve(ipi_mdp* h, const ipi_opts* o, double* v, int32_t* policy, double*
     } else {
       pending_report = true;
     }
-    cudaEventRecord(pi_.b, st);
-    phases.push_back(pi_);
+    cudaEventRecord(i1, st);
+    pending_phases = true;
     std::swap(vcur, vnext);
     ++k;
   }
@@ -953,13 +991,6 @@ int ipi_solve(ipi_mdp* h, const ipi_opts* o, double* v, int32_t* policy, double*
   if (policy) IPI_CUDA_TRY(cudaMemcpyAsync(policy, h->pi, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, st));
   IPI_CUDA_TRY(cudaStreamSynchronize(st));
   const auto t_end = std::chrono::steady_clock::now();
-  double tg = 0, ta = 0, ti = 0;
-  for (auto& ph : phases) {
-    float ms = 0;
-    cudaEventElapsedTime(&ms, ph.a, ph.b);
-    (ph.kind == 0 ? tg : ph.kind == 1 ? ta : ti) += ms * 1e-3;
-  }
-  for (auto e : ev) cudaEventDestroy(e);
   const int nh = std::min<int>((int)hist.size(), hist_cap);
   if (history) std::memcpy(history, hist.data(), sizeof(double) * nh);
   stats->status = status;

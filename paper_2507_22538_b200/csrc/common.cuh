@@ -193,9 +193,18 @@ __device__ __forceinline__ double group_sum(double v) {
 
 __device__ __forceinline__ double warp_sum(double v) { return group_sum<32>(v); }
 
+// NaN-propagating max for the Bellman residual: the reference's
+// np.max(np.abs(v - applied)) (driver.py:136) returns NaN when any entry is
+// NaN, so a diverged iterate can never read as converged.  fmax would drop it.
+// Non-negative doubles and a positive NaN order correctly as unsigned IEEE
+// bits (NaN > +inf), so the integer atomicMax that combines CTAs keeps it.
+__device__ __forceinline__ double res_max(double a, double b) {
+  return a != a ? a : (b != b ? fabs(b) : fmax(a, b));
+}
+
 __device__ __forceinline__ double warp_max(double v) {
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) v = fmax(v, __shfl_xor_sync(kFull, v, off));
+  for (int off = 16; off > 0; off >>= 1) v = res_max(v, __shfl_xor_sync(kFull, v, off));
   return v;
 }
 

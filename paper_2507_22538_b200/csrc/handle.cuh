@@ -32,17 +32,13 @@ struct ipi_mdp {
   double* xbuf = nullptr;
   int64_t* scan_tmp = nullptr;
   double* kry = nullptr;        // per-handle Krylov workspace (ipi_solve)
+  ipi_op* op_pi = nullptr;      // planned K3 operator over the P_pi scratch (stepped GMRES)
   double* invd = nullptr;       // Jacobi inverse diagonal (ipi_solve with pc = jacobi)
   int64_t kry_len = 0;
   int64_t scan_tmp_len = 0;
   ipi_inner_report* d_report = nullptr;
   void* host_pinned = nullptr;  // small pinned staging area
 
-  // K1 TMA pipeline plan (bellman_tma.cu); use_tma = 0 -> register kernels
-  int use_tma = 0;
-  int64_t* tma_bounds = nullptr;
-  int tma_blocks = 0, tma_smem = 0, tma_sc = 0, tma_ns = 0, tma_super = 0, tma_wcap = 0,
-      tma_stage = 0, tma_halo = -1;
   // K1 flat-row cp.async ring (variant 4): window bytes in front of the rings
   int ring_win_bytes = 0;
   int uring_lookahead = 1;  // variant 6: V gathers issued this many steps ahead
@@ -50,15 +46,8 @@ struct ipi_mdp {
   int k1_win_async = 1;     // variant 6: cp.async V window (IPI_K1_WIN_ASYNC=0: scalar loop)
   int k1_interleave = 1;    // variant 6: interleaved state order (IPI_K1_INTERLEAVE=0: contiguous)
   int k1_rotate = 1;        // variant 6: rotated per-CTA start (IPI_K1_ROTATE=0: none)
+  int k1_gen_u = 8;        // variant 0: loads in flight per lane (IPI_K1_GEN_U, read at create)
   unsigned long long* k1_trace = nullptr;  // diagnostics (ipi_mdp_k1_trace)
-  // variant 9: column-tiled layout of the shard (bellman_tiled.cu)
-  double* tl_val = nullptr;
-  uint16_t* tl_key = nullptr;
-  int32_t* tl_farcol = nullptr;
-  int64_t* tl_farbase = nullptr;
-  int32_t* tl_meta = nullptr;
-  int64_t tl_nblocks = 0, tl_wt = 0;
-  int tl_bs = 0, tl_T = 0;
 };
 
 // A planned policy operator (K3): borrowed P_pi rows + the kernel shape.
@@ -124,21 +113,6 @@ bool k1_ring_prepare(int K, int S, int NW, bool win, int smem);
 int uniform_ring_smem(int K, int stages, int warps, int window_bytes);
 bool k1_uring_prepare(int K, int NW, int S, int D, bool win, int smem);
 
-// bellman_tiled.cu: column-tiled K1 for window-less uniform rows (variant 9)
-int k1_tiled_build(ipi_mdp* h, int64_t wt, cudaStream_t st);
-void k1_tiled_free(ipi_mdp* h);
-int k1_tiled_smem(const ipi_mdp* h);
-int launch_bellman_tiled(ipi_mdp* h, const double* v_full, int32_t mode, int32_t* policy,
-                         double* applied, double* g_pi, int32_t* len_pi,
-                         unsigned long long* res_bits, cudaStream_t st);
-
-// bellman_tma.cu
-bool k1_tma_plan(int64_t n_states_max_cta, int m, int K, int halo, int64_t n_global, int* SC,
-                 int* NS, int* super_states, int* win_cap, int* stage_bytes, int* smem_bytes);
-int launch_bellman_tma(ipi_mdp* h, const double* v_full, int32_t mode, int32_t* policy,
-                       double* applied, double* g_pi, int32_t* len_pi,
-                       unsigned long long* res_bits, cudaStream_t st);
-
 // policy.cu
 int gather_policy(ipi_mdp* h, const int32_t* policy, const int32_t* len_pi, int64_t* rp_pi,
                   int32_t* col_pi, double* val_pi, double* g_pi, int64_t* nnz_out,
@@ -159,7 +133,7 @@ int k3_uring_smem(int K, int stages, int warps, int window_bytes);
 int k3_flat_smem(int K, int stages, int warps, int window_bytes);
 bool k3_shape_prepare(int variant, int K, int NW, int S, bool win, int smem);
 int op_launch(const ipi_op* op, const double* x_full, const double* b, int epi, double* y,
-              cudaStream_t st, const double* y_partial = nullptr);
+              cudaStream_t st, const double* y_partial = nullptr, const int* active = nullptr);
 
 // krylov.cu
 int inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi, int64_t n,
@@ -167,16 +141,30 @@ int inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_p
                 int32_t kind, double scale, int lanes, int halo, int uniform_K,
                 ipi_inner_report* d_report, cudaStream_t st, double* workspace = nullptr,
                 int64_t workspace_doubles = 0, const double* inv_diag = nullptr,
-                double pi_bytes = 0.0);  // bytes of P_pi (L2-residency choice; <= 0: read nnz)
+                double pi_bytes = 0.0,   // bytes of P_pi (L2-residency choice; <= 0: read nnz)
+                int ortho = IPI_ORTHO_AUTO,
+                const ipi_op* op = nullptr);  // planned K3 operator of P_pi: stepped GMRES
+// krylov_step.cu
+bool stepped_gmres_fits(int64_t n, int sms);
+int64_t stepped_gmres_workspace(int64_t n, int blocks);
+int stepped_gmres(const ipi_op* op, int64_t n, const double* b, double* x, double target,
+                  int32_t max_it, const double* inv_diag, ipi_inner_report* d_report,
+                  double* ws, int64_t ws_doubles, cudaStream_t st);
 // Jacobi: inv_diag[s] = 1 / (1 - gamma * P_pi[s, s])  (inner.py:115-118)
 int jacobi_inv_diag(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi, int64_t n,
                     double gamma, double* inv_diag, cudaStream_t st);
 // doubles of Krylov workspace inner_solve needs for an n-row system
 inline int64_t krylov_workspace_doubles(int64_t n) {
-  return (int64_t)(kGmresRestart + 1) * n + 2 * n + 4 * 1024;
+  return (int64_t)(kGmresRestart + 1) * n + 2 * n + 2 * 32 * 1024 + 64;
 }
 
-// device scratch arena for the inner solver (per device, grown on demand)
-double* krylov_workspace(int64_t n, int64_t doubles_needed);
+// diagnostics: record K4 phase timestamps (enable = 1) / copy them out and stop (0)
+int k4_trace(int enable, unsigned long long* out, int cap);
+int ring_apply_test(const int32_t* col, const double* val, int64_t n, double gamma, const double* x,
+                    double* y, int reps, float* ms, cudaStream_t st);
+
+// device scratch arena for the standalone inner solver (per device and
+// stream, grown stream-ordered on demand)
+double* krylov_workspace(int64_t doubles_needed, cudaStream_t st);
 
 }  // namespace ipi

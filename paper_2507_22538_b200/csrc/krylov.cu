@@ -19,7 +19,10 @@
 //          true residual per cycle, est_target = |g_j|*(eff/rn)*0.5       :229-283
 //   back substitution with zero-pivot -> 0                                 :286-292
 // Every vector op uses separate mul/add roundings like numpy (no FMA).
+#include <algorithm>
+#include <cstdio>
 #include <cstdlib>
+#include <map>
 #include <mutex>
 
 #include "krylov.cuh"
@@ -29,36 +32,68 @@ namespace ipi {
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
-// one arena per device (the standalone ipi_inner_solve; handles own theirs)
+// One arena per (device, stream) for the standalone ipi_inner_solve (handles
+// own theirs).  Growth frees and allocates stream-ordered, so work already
+// queued on the stream keeps its arena and nothing else is synchronised;
+// solves on different streams never share a basis, partials or barrier.
 static std::mutex g_ws_mu;
-static double* g_ws[64] = {};
-static int64_t g_ws_len[64] = {};
+static std::map<std::pair<int, cudaStream_t>, std::pair<double*, int64_t>> g_ws;
 
-double* krylov_workspace(int64_t /*n*/, int64_t doubles_needed) {
+double* krylov_workspace(int64_t doubles_needed, cudaStream_t st) {
   std::lock_guard<std::mutex> lk(g_ws_mu);
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-  if (g_ws[dev] && g_ws_len[dev] >= doubles_needed) return g_ws[dev];
-  if (g_ws[dev]) {
-    cudaDeviceSynchronize();  // the arena may still be in use by queued solves
-    cudaFree(g_ws[dev]);
-    g_ws[dev] = nullptr;
-    g_ws_len[dev] = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  auto& slot = g_ws[{dev, st}];
+  if (slot.first && slot.second >= doubles_needed) return slot.first;
+  if (slot.first) {
+    cudaFreeAsync(slot.first, st);
+    slot = {nullptr, 0};
   }
-  if (cudaMalloc(&g_ws[dev], sizeof(double) * doubles_needed) != cudaSuccess) {
-    g_ws[dev] = nullptr;
+  double* p = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(double) * doubles_needed, st) != cudaSuccess) {
     cudaGetLastError();
     return nullptr;
   }
-  g_ws_len[dev] = doubles_needed;
-  return g_ws[dev];
+  slot = {p, doubles_needed};
+  return p;
+}
+
+// diagnostics: phase timestamps of the next persistent launches (ipi_k4_trace)
+static unsigned long long* g_k4_trace = nullptr;
+static int g_k4_trace_cap = 0;
+
+int k4_trace(int enable, unsigned long long* out, int cap) {
+  if (enable) {
+    if (!g_k4_trace) {
+      IPI_CUDA_TRY(cudaMalloc(&g_k4_trace, sizeof(unsigned long long) * 8192));
+      IPI_CUDA_TRY(cudaMemset(g_k4_trace, 0, sizeof(unsigned long long)));
+      g_k4_trace_cap = 8192;
+    }
+    return IPI_OK;
+  }
+  if (g_k4_trace && out && cap > 0) {
+    IPI_CUDA_TRY(cudaDeviceSynchronize());
+    IPI_CUDA_TRY(cudaMemcpy(out, g_k4_trace, sizeof(unsigned long long) * std::min(cap, g_k4_trace_cap),
+                            cudaMemcpyDeviceToHost));
+  }
+  cudaFree(g_k4_trace);
+  g_k4_trace = nullptr;
+  g_k4_trace_cap = 0;
+  return IPI_OK;
+}
+
+// environment switches (A/B experiments), read once per process
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
 }
 
 int inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi, int64_t n,
                 double gamma, const double* b, double* x, double target, int32_t max_it,
                 int32_t kind, double scale, int lanes, int halo, int uniform_K,
                 ipi_inner_report* d_report, cudaStream_t st, double* workspace,
-                int64_t workspace_doubles, const double* inv_diag, double pi_bytes) {
+                int64_t workspace_doubles, const double* inv_diag, double pi_bytes, int ortho,
+                const ipi_op* op) {
   if (kind < IPI_KSP_RICHARDSON || kind > IPI_KSP_TFQMR)
     return fail(IPI_EVALIDATION, "unknown inner solver kind " + std::to_string(kind));
   if (max_it < 1) return fail(IPI_EVALIDATION, "iteration cap must be >= 1, got " + std::to_string(max_it));
@@ -70,10 +105,17 @@ int inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_p
   // one 1024-thread CTA per SM (fewer for tiny systems: >= 32 rows per CTA)
   int blocks = sms;
   if ((int64_t)blocks * 32 > n) blocks = (int)std::max<int64_t>(1, n / 32);
-  const int64_t need = (int64_t)(R + 1) * n + 2 * n + 4 * (int64_t)blocks + 8;
+  if (ortho != IPI_ORTHO_AUTO && ortho != IPI_ORTHO_CGS2 && ortho != IPI_ORTHO_MGS)
+    return fail(IPI_EVALIDATION, "unknown GMRES orthogonalisation " + std::to_string(ortho));
+  // AUTO: a grid all-reduce costs ~2-3 us; an MGS pass over a CTA's slice of
+  // one basis vector costs about the same once the slice exceeds a few
+  // thousand rows, below which CGS2's 2 reductions per step beat MGS's j+2
+  // (C4: 0.062 vs 0.089 ms per step; C2: MGS).
+  if (ortho == IPI_ORTHO_AUTO) ortho = n / blocks >= 1024 ? IPI_ORTHO_MGS : IPI_ORTHO_CGS2;
+  const int64_t need = (int64_t)(R + 1) * n + 2 * n + 2 * kPartStride * (int64_t)blocks + 64;
   // caller-owned workspace (per handle, so concurrent handles never share it)
   // or the per-device arena used by the standalone API
-  double* ws = (workspace && workspace_doubles >= need) ? workspace : krylov_workspace(n, need);
+  double* ws = (workspace && workspace_doubles >= need) ? workspace : krylov_workspace(need, st);
   if (!ws) return fail(IPI_ERESOURCE, "cannot allocate Krylov workspace of " + std::to_string(need * 8) + " bytes");
   KArgs a;
   a.rp = rp_pi;
@@ -87,10 +129,17 @@ int inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_p
   a.w = ws + (int64_t)(R + 1) * n;
   a.r = a.w + n;
   a.partials = a.r + n;
-  a.bar = reinterpret_cast<unsigned*>(a.partials + 4 * (int64_t)blocks);
+  a.bar = reinterpret_cast<unsigned*>(a.partials + 2 * kPartStride * (int64_t)blocks);
+  a.ortho = ortho;
+  a.trace = g_k4_trace;
+  a.trace_cap = g_k4_trace_cap;
+  if (a.trace) IPI_CUDA_TRY(cudaMemsetAsync(a.trace, 0, sizeof(unsigned long long), st));
   IPI_CUDA_TRY(cudaMemsetAsync(a.bar, 0, 64, st));
-  a.bar_mode = getenv("IPI_K4_BARRIER") ? atoi(getenv("IPI_K4_BARRIER")) : 0;
-  a.xwin = getenv("IPI_K4_XWIN") ? atoi(getenv("IPI_K4_XWIN")) != 0 : 1;
+  static const int bar_mode = env_int("IPI_K4_BARRIER", 0);
+  static const int xwin = env_int("IPI_K4_XWIN", 1);
+  static const double keep_env = getenv("IPI_K4_KEEP") ? atof(getenv("IPI_K4_KEEP")) : -1.0;
+  a.bar_mode = bar_mode;
+  a.xwin = xwin != 0;
   {  // L2 residency of P_pi across the solve's SpMVs (IPI_K4_KEEP overrides the fraction)
     int l2 = 0;
     cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
@@ -105,7 +154,7 @@ int inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_p
     // whole P_pi when it fits; a fractional hint helped C4's SpMV (-9%) but not its
     // MGS-bound GMRES step and slowed C3's (IPI_K4_KEEP=<fraction> to experiment)
     double f = bytes <= budget ? 1.0 : 0.0;
-    if (getenv("IPI_K4_KEEP")) f = atof(getenv("IPI_K4_KEEP"));
+    if (keep_env >= 0.0) f = keep_env;
     a.keep_frac = (float)std::min(1.0, std::max(0.0, f));
   }
   a.target = target;
@@ -114,6 +163,44 @@ int inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_p
   a.scale = scale;
   a.rep = d_report;
   a.invd = inv_diag;
+  // Large uniform K = 64-class rows with GMRES/MGS: stepped launches (K3 ring
+  // operator + one cooperative MGS/Givens kernel per Arnoldi step,
+  // krylov_step.cu).  IPI_K4_STEPPED=0 keeps the persistent kernels.
+  static const int stepped_env = env_int("IPI_K4_STEPPED", 1);
+  if (stepped_env && op && op->variant == IPI_K3_URING && op->n_local == n && op->state0 == 0 &&
+      kind == IPI_KSP_GMRES && ortho == IPI_ORTHO_MGS && stepped_gmres_fits(n, sms)) {
+    const int64_t sneed = stepped_gmres_workspace(n, sms);
+    double* sws = (workspace && workspace_doubles >= sneed) ? workspace : krylov_workspace(sneed, st);
+    if (!sws) return fail(IPI_ERESOURCE, "cannot allocate the stepped GMRES workspace");
+    return stepped_gmres(op, n, b, x, target, max_it, inv_diag, d_report, sws,
+                         sws == workspace ? workspace_doubles : sneed, st);
+  }
+  // Uniform K = 64-class rows with GMRES/CGS2 or Richardson: the ring kernel
+  // (krylov_ring.cu).  IPI_K4_RING=0 keeps the 1024-thread kernel;
+  // IPI_K4_RING_SHAPE=<warps>x<stages> forces a ring shape.
+  static const int ring_env = env_int("IPI_K4_RING", 1);
+  static const char* shape_env = getenv("IPI_K4_RING_SHAPE");
+  if (ring_env && uniform_K > 0 && (kind == IPI_KSP_RICHARDSON || kind == IPI_KSP_GMRES)) {
+    int NW = 12, S = 3;
+    if (shape_env) sscanf(shape_env, "%dx%d", &NW, &S);
+    if (ring_inner_has(uniform_K, NW, S) && n >= 64 * (int64_t)blocks) {
+      a.K = uniform_K;
+      a.halo = -1;
+      a.win_cap = 0;
+      const int ring = ring_inner_smem(uniform_K, NW, S);
+      const int budget_b = 227 * 1024 - (int)sizeof(KShared) - 1024;
+      const int64_t own_max = (n + blocks - 1) / blocks + 8;
+      // w slice in shared memory only on request: the ring plus a 57 KB slice
+      // leave L1 too small for the gathered x's neighbourhood (IPI_K4_RING_WSMEM=1)
+      static const int wsmem = env_int("IPI_K4_RING_WSMEM", 0);
+      a.own_cap = wsmem && ring + own_max * 8 <= budget_b ? (int)own_max : 0;
+      const int smem = ring + a.own_cap * 8;
+      if (a.ortho == IPI_ORTHO_MGS && (own_max > (int64_t)ring_mgs_elems(NW) * NW * 32 ||
+                                       2 * (own_max + 1) * 8 > ring))
+        a.ortho = IPI_ORTHO_CGS2;  // slices too long for the staged MGS
+      return dispatch_inner_ring(a, uniform_K, NW, S, smem, blocks, st);
+    }
+  }
   int G = lanes, P = 0;
   a.K = 0;
   if (uniform_K > 0 && uniform_shape(uniform_K, &G, &P)) a.K = uniform_K;
@@ -135,7 +222,10 @@ int inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_p
   switch (kind) {
     case IPI_KSP_TFQMR: return dispatch_inner_tfqmr(a, G, P, lanes, win, smem, blocks, st);
     case IPI_KSP_BICGSTAB: return dispatch_inner_bicgstab(a, G, P, lanes, win, smem, blocks, st);
-    default: return dispatch_inner_gmres(a, G, P, lanes, win, smem, blocks, st);
+    default:
+      if (kind == IPI_KSP_GMRES && ortho == IPI_ORTHO_CGS2)
+        return dispatch_inner_gmres_cgs(a, G, P, lanes, win, smem, blocks, st);
+      return dispatch_inner_gmres(a, G, P, lanes, win, smem, blocks, st);
   }
 }
 

@@ -32,6 +32,7 @@ namespace cg = cooperative_groups;
 namespace ipi {
 
 constexpr int R = kGmresRestart;
+constexpr int kKindGmresCgs = 4;  // inner_kernel KIND of GMRES with CGS2 orthogonalisation
 
 struct KArgs {
   const int64_t* rp;
@@ -44,7 +45,8 @@ struct KArgs {
   double* V;         // (R+1) * n Krylov basis
   double* w;         // n
   double* r;         // n
-  double* partials;  // [2 slots][grid][2]
+  double* partials;  // [2 slots][kPartStride values][grid]: value-major, so the CTA
+                     // partials of one value are contiguous for the reducing warp
   double target;
   int max_it;
   int kind;
@@ -59,7 +61,28 @@ struct KArgs {
   int bar_mode;        // GridBarrier::mode (IPI_K4_BARRIER)
   float keep_frac;     // fraction of P_pi accesses marked L2 evict-last (0 = evict-first)
   int xwin;            // stage the SpMV input window (else the window space only holds MGS slices)
+  int ortho;           // GMRES Arnoldi orthogonalisation (resolved): IPI_ORTHO_MGS / IPI_ORTHO_CGS2
+  unsigned long long* trace;  // diagnostics (ipi_k4_trace): phase timestamps or nullptr
+  int trace_cap;
 };
+
+// Diagnostics: CTA 0 records %globaltimer at phase boundaries (trace[1..]);
+// trace[0] counts the records.
+__device__ __forceinline__ void k4_mark(const KArgs& a) {
+  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    const unsigned long long k = a.trace[0];
+    if ((int)k + 1 < a.trace_cap) {
+      a.trace[k + 1] = t;
+      a.trace[0] = k + 1;
+    }
+  }
+}
+
+// doubles per CTA and slot in the all-reduce partials (the CGS dot vector:
+// up to R projections + one norm)
+constexpr int kPartStride = 32;
 
 // Grid barrier for the co-resident (cooperatively launched) CTAs: one release
 // add per CTA on a monotone counter + an acquire spin by the CTA's leader.
@@ -105,6 +128,10 @@ struct GridBarrier {
 struct KShared {
   double red[64];
   double bc[4];
+  double red8[8 * 32];           // block level of an 8-wide chunk (vector all-reduce)
+  double vpart[kPartStride];     // this CTA's partials of a vector all-reduce
+  double cv[kPartStride];        // CGS: first projection  c = V^T w  (+ ||w||^2)
+  double dv[kPartStride];        // CGS: re-orthogonalisation  d = V^T w1
   double H[(R + 1) * R];
   double cs[R], sn[R], g[R + 1], y[R];
   int iflag[4];
@@ -135,7 +162,7 @@ __device__ __forceinline__ void grid_allreduce(double (&v)[NV], const KArgs& a, 
     for (int k = 0; k < NV; ++k) t[k] = warp_sum(lane < nw ? sh.red[k * 32 + lane] : 0.0);
     if (lane == 0) {
 #pragma unroll
-      for (int k = 0; k < NV; ++k) a.partials[((int64_t)slot * nblk + blockIdx.x) * 2 + k] = t[k];
+      for (int k = 0; k < NV; ++k) a.partials[((int64_t)slot * kPartStride + k) * nblk + blockIdx.x] = t[k];
     }
   }
   gb.arrive_and_wait(threadIdx.x == 0);
@@ -145,7 +172,7 @@ __device__ __forceinline__ void grid_allreduce(double (&v)[NV], const KArgs& a, 
     for (int k = 0; k < NV; ++k) {
       double s = 0.0;
       for (int i = lane; i < nblk; i += 32)
-        s = add_rn(s, __ldcg(a.partials + ((int64_t)slot * nblk + i) * 2 + k));
+        s = add_rn(s, __ldcg(a.partials + ((int64_t)slot * kPartStride + k) * nblk + i));
       s = warp_sum(s);
       if (lane == 0) sh.bc[k] = s;
     }
@@ -154,6 +181,101 @@ __device__ __forceinline__ void grid_allreduce(double (&v)[NV], const KArgs& a, 
 #pragma unroll
   for (int k = 0; k < NV; ++k) v[k] = sh.bc[k];
   slot ^= 1;
+}
+
+// Block level of a vector all-reduce: the block sums of acc[0..7] (fixed xor
+// trees: warp, then warp 0..7 over the per-warp values) go to
+// sh.vpart[base + k] for base + k < cnt.
+__device__ __forceinline__ void block_accumulate8(const double (&acc)[8], int base, int cnt,
+                                                  KShared& sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double t[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) t[k] = warp_sum(acc[k]);
+  __syncthreads();  // sh.red8 free (previous chunk's readers done)
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) sh.red8[k * 32 + warp] = t[k];
+  }
+  __syncthreads();
+  if (warp < 8 && base + warp < cnt) {
+    const double v = warp_sum(lane < nw ? sh.red8[warp * 32 + lane] : 0.0);
+    if (lane == 0) sh.vpart[base + warp] = v;
+  }
+}
+
+// Grid level of a vector all-reduce of sh.vpart[0..cnt) (cnt <= kPartStride):
+// per-CTA partials, the grid barrier, then value k is summed over the CTAs in
+// CTA order by warp k % nwarps (fixed order: every CTA gets bit-identical
+// results) into out[k] (shared memory).  Ends with a CTA barrier.
+__device__ __forceinline__ void grid_allreduce_vec(int cnt, double* out, const KArgs& a, int& slot,
+                                                   GridBarrier& gb, KShared& sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int nblk = gridDim.x;
+  __syncthreads();  // sh.vpart complete
+  if ((int)threadIdx.x < cnt)
+    a.partials[((int64_t)slot * kPartStride + threadIdx.x) * nblk + blockIdx.x] = sh.vpart[threadIdx.x];
+  __syncthreads();  // every lane's partial ordered before the leader's release
+  gb.arrive_and_wait(threadIdx.x == 0);
+  __syncthreads();
+  for (int k = warp; k < cnt; k += nw) {
+    double s = 0.0;
+    for (int i = lane; i < nblk; i += 32)
+      s = add_rn(s, __ldcg(a.partials + ((int64_t)slot * kPartStride + k) * nblk + i));
+    s = warp_sum(s);
+    if (lane == 0) out[k] = s;
+  }
+  __syncthreads();
+  slot ^= 1;
+}
+
+// CGS projections of this CTA's slice of w onto the basis: out[l] = <V_l, w>
+// for l < nv and, when with_norm, out[nv] = <w, w>.  One coalesced pass over
+// the nv basis slices (8 in flight per thread), then one vector all-reduce.
+__device__ __forceinline__ void cgs_dots(const KArgs& a, int nv, bool with_norm, const double* wl,
+                                         int64_t s_lo, int64_t s_hi, uint64_t pol, double* out,
+                                         int& slot, GridBarrier& gb, KShared& sh) {
+  const int cnt = nv + (with_norm ? 1 : 0);
+  const int64_t n = a.n;
+  for (int l0 = 0; l0 < cnt; l0 += 8) {
+    double acc[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+#pragma unroll 2
+    for (int64_t i = s_lo + threadIdx.x; i < s_hi; i += blockDim.x) {
+      const double wi = wl[i - s_lo];
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = l0 + u < nv ? ld_hint(a.V + (int64_t)(l0 + u) * n + i, pol) : wi;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (l0 + u < cnt) acc[u] = add_rn(acc[u], mul_rn(v[u], wi));
+    }
+    block_accumulate8(acc, l0, cnt, sh);
+  }
+  grid_allreduce_vec(cnt, out, a, slot, gb, sh);
+}
+
+// w <- w - sum_{l < nv} coef[l] V_l over this CTA's slice (l ascending, separate
+// roundings); returns this thread's share of ||w||^2.
+__device__ __forceinline__ double cgs_update(const KArgs& a, int nv, const double* coef, double* wl,
+                                             int64_t s_lo, int64_t s_hi, uint64_t pol) {
+  const int64_t n = a.n;
+  double q = 0.0;
+  for (int64_t i = s_lo + threadIdx.x; i < s_hi; i += blockDim.x) {
+    double t = wl[i - s_lo];
+    for (int l0 = 0; l0 < nv; l0 += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = l0 + u < nv ? ld_hint(a.V + (int64_t)(l0 + u) * n + i, pol) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (l0 + u < nv) t = sub_rn(t, mul_rn(coef[l0 + u], v[u]));
+    }
+    wl[i - s_lo] = t;
+    q = add_rn(q, mul_rn(t, t));
+  }
+  return q;
 }
 
 // Row sums of P_pi over this CTA's rows with an optional shared-memory window
@@ -266,7 +388,8 @@ __device__ __forceinline__ void spmv_rows(const KArgs& a, const double* xin, int
   }
 }
 
-// KIND: 0 = GMRES + Richardson (runtime a.kind), 2 = BiCGStab, 3 = TFQMR.  Each
+// KIND: 0 = GMRES (MGS) + Richardson (runtime a.kind), 4 = GMRES (CGS2) +
+// Richardson, 2 = BiCGStab, 3 = TFQMR.  Each
 // solver family is its own instantiation (and translation unit) so the hot
 // GMRES kernel does not carry the register pressure of the others.
 template <int G, int P, bool WIN, int KIND>
@@ -587,6 +710,7 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
       const double beta = invd ? sqrt(zz) : rn;
       if (beta == 0.0 || !isfinite(beta)) break;
       for (int64_t i = s_lo + tid; i < s_hi; i += nthr) a.V[i] = a.V[i] / beta;
+      __syncthreads();  // every thread has read the previous cycle's sh.g
       if (tid == 0) {
         for (int k = 0; k < (R + 1) * R; ++k) sh.H[k] = 0.0;
         for (int k = 0; k < R; ++k) sh.cs[k] = sh.sn[k] = 0.0;
@@ -604,7 +728,27 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
         });
         ++it;
         __syncthreads();  // w rows written by group leaders, read per-thread below
-        if (staged) {
+        if constexpr (KIND == kKindGmresCgs) {
+          // Classical Gram-Schmidt with one re-orthogonalisation when needed
+          // (DGKS test, ||w1|| < ||w||/sqrt(2)): 2 all-reduces per step instead of
+          // MGS's j+2 (inner.py:251-253 uses MGS; the projections agree to rounding).
+          cgs_dots(a, j + 1, true, wl, s_lo, s_hi, pol_last, sh.cv, slot, gb, sh);
+          const double nw = sh.cv[j + 1];
+          double q1[1] = {cgs_update(a, j + 1, sh.cv, wl, s_lo, s_hi, pol_last)};
+          grid_allreduce<1>(q1, a, slot, gb, sh);
+          double nw1 = q1[0];
+          const bool reorth = nw1 < 0.5 * nw;  // uniform across the grid
+          if (reorth) {
+            cgs_dots(a, j + 1, false, wl, s_lo, s_hi, pol_last, sh.dv, slot, gb, sh);
+            double q2[1] = {cgs_update(a, j + 1, sh.dv, wl, s_lo, s_hi, pol_first)};
+            grid_allreduce<1>(q2, a, slot, gb, sh);
+            nw1 = q2[0];
+          }
+          if (tid == 0) {
+            for (int l = 0; l <= j; ++l) sh.H[l * R + j] = reorth ? add_rn(sh.cv[l], sh.dv[l]) : sh.cv[l];
+          }
+          p[0] = nw1;
+        } else if (staged) {
           // MGS with the basis slices staged in shared memory (the V window is
           // idle until the next SpMV): V_{l+1} is copied with cp.async before
           // the all-reduce that produces h_l, so each pass costs one barrier
@@ -685,7 +829,7 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
             p[0] = q;
           }
         }
-        grid_allreduce<1>(p, a, slot, gb, sh);
+        if constexpr (KIND != kKindGmresCgs) grid_allreduce<1>(p, a, slot, gb, sh);
         const double hnorm = sqrt(p[0]);
         if (tid == 0) {
           double* H = sh.H;
@@ -802,6 +946,13 @@ static int dispatch_inner(KArgs& a, int G, int P, int lanes, bool win, int smem,
 
 int dispatch_inner_gmres(KArgs& a, int G, int P, int lanes, bool win, int smem, int blocks,
                          cudaStream_t st);
+// krylov_ring.cu: uniform rows (K = 64 class) with the per-warp cp.async ring SpMV
+int ring_inner_smem(int K, int NW, int S);
+int ring_mgs_elems(int NW);  // slice elements per thread the ring kernel's MGS keeps in registers
+bool ring_inner_has(int K, int NW, int S);
+int dispatch_inner_ring(KArgs& a, int K, int NW, int S, int smem, int blocks, cudaStream_t st);
+int dispatch_inner_gmres_cgs(KArgs& a, int G, int P, int lanes, bool win, int smem, int blocks,
+                             cudaStream_t st);
 int dispatch_inner_bicgstab(KArgs& a, int G, int P, int lanes, bool win, int smem, int blocks,
                             cudaStream_t st);
 int dispatch_inner_tfqmr(KArgs& a, int G, int P, int lanes, bool win, int smem, int blocks,

@@ -2,7 +2,7 @@
 //
 // Stages, in order: row statistics + sampled locality histogram, the shared
 // V window and the K1 grid, then the K1 variant (register-deep, uniform ring,
-// generic-rows CTA autotune, flat ring, opt-in TMA ring).  Later stages may
+// generic-rows CTA autotune, flat ring).  Later stages may
 // override earlier choices; each keeps the previous plan when its kernel does
 // not fit.  Environment switches (IPI_K1_*, IPI_URING_*, IPI_RING_*) force
 // shapes for A/B measurements.
@@ -513,121 +513,14 @@ static int plan_flat_ring(PlanCtx& c) {
   return IPI_OK;
 }
 
-// TMA ring for uniform rows (opt-in experiment, IPI_K1_TMA=1)
-static int plan_tma(PlanCtx& c) {
-  ipi_mdp* h = c.h;
-  cudaStream_t st = c.st;
-  ipi_plan& p = h->plan;
-  [[maybe_unused]] const int64_t* row_ptr = h->rp;
-  [[maybe_unused]] const int32_t* col = h->col;
-  [[maybe_unused]] const double* values = h->val;
-  [[maybe_unused]] const double* stage_cost = h->cost;
-  [[maybe_unused]] const int64_t n_local = h->n_local, n_global = h->n_global, state0 = h->state0;
-  [[maybe_unused]] const int32_t m = h->m;
-  [[maybe_unused]] const int64_t rows = c.rows;
-  [[maybe_unused]] const int64_t nnz = p.nnz;
-  // ---- TMA ring plan for uniform rows (one persistent CTA per SM) ------------
-  {
-    // Experimental: off unless IPI_K1_TMA=1.  Measured on C2
-    // it is slower than the register-pipelined kernel (the shared-memory ring
-    // left beside the 72 KB V window holds ~100 KB in flight, the same as the
-    // registers of 32 warps, and the 16-warp ring couples warps through the
-    // producer's empty-barrier waits).
-    const char* env = getenv("IPI_K1_TMA");
-    const bool allow = env && env[0] == '1';
-    if (allow && p.k1_variant == 1 && n_local > 0) {
-      const int blocks = (int)std::min<int64_t>(h->num_sms, std::max<int64_t>(1, n_local / 64));
-      const int64_t per = (n_local + blocks - 1) / blocks;
-      int SC, NS, sup, wcap, stage, smem;
-      if (k1_tma_plan(per + 64, m, p.row_len_max, p.halo, n_global, &SC, &NS, &sup, &wcap, &stage,
-                      &smem)) {
-        std::vector<int64_t> hb(blocks + 1);
-        for (int c = 0; c <= blocks; ++c) {
-          int64_t b = (int64_t)((double)n_local * c / blocks);
-          b = (b / SC) * SC;
-          hb[c] = c == blocks ? n_local : std::min<int64_t>(b, n_local);
-        }
-        if (cudaMalloc(&h->tma_bounds, sizeof(int64_t) * (blocks + 1)) == cudaSuccess &&
-            cudaMemcpy(h->tma_bounds, hb.data(), sizeof(int64_t) * (blocks + 1),
-                       cudaMemcpyHostToDevice) == cudaSuccess) {
-          h->use_tma = 1;
-          h->tma_blocks = blocks;
-          h->tma_smem = smem;
-          h->tma_sc = SC;
-          h->tma_ns = NS;
-          h->tma_super = sup;
-          h->tma_wcap = wcap;
-          h->tma_stage = stage;
-          h->tma_halo = wcap > 0 ? p.halo : -1;
-          p.k1_variant = 2;
-          p.k1_stages = NS;
-          p.k1_tma_chunk_states = SC;
-          p.k1_blocks = blocks;
-          p.k1_threads = (16 + 1) * 32;
-          p.k1_smem_bytes = smem;
-        }
-      }
-    }
-  }
-  return IPI_OK;
-}
-
-// window-less uniform rows (C5): column-tiled layout.  Opt-in experiment
-// (IPI_K1_TILED=1 forces it, =2 lets the planner time it against the
-// register-deep kernel): correct, but 9.6 vs 8.0 ms on a C5 rank block with the
-// jagged-diagonal layout (13.7 ms with the earlier segmented scans).
-static int plan_tiled(PlanCtx& c) {
-  ipi_mdp* h = c.h;
-  cudaStream_t st = c.st;
-  ipi_plan& p = h->plan;
-  const char* env = getenv("IPI_K1_TILED");
-  if (!env || (env[0] != '1' && env[0] != '2')) return IPI_OK;
-  const bool force = env[0] == '1';
-  if (p.k1_variant != 3 || !p.uniform_rows || p.halo >= 0 || (!force && p.nnz < (1ll << 26)))
-    return IPI_OK;
-  // near half-width: the smallest 2^k covering >= 85% of the sampled gathers
-  double cum[41];
-  cum[0] = 0.0;
-  for (int b = 0; b < 40; ++b) cum[b + 1] = cum[b] + (double)c.hst[8 + b];
-  int k = 0;
-  while (k < 30 && cum[40] > 0 && cum[std::min(k, 39) + 1] / cum[40] < 0.85) ++k;
-  const int64_t wt = std::min<int64_t>(1ll << k, h->n_global);
-  int rc = k1_tiled_build(h, wt, st);
-  if (rc) return rc;
-  if (h->tl_nblocks == 0) return IPI_OK;
-  int best = 0;
-  if (!force) {  // time deep (0) vs tiled (1) on the instance
-    K1Scratch tmp(h->n_global, h->n_local, st);
-    const int saved = p.k1_variant;
-    best = !tmp.ok ? -1 : autotune_pick(
-        2, [&](int i) { p.k1_variant = i == 0 ? saved : 9; return true; },
-        [&] { return launch_bellman(h, tmp.v, IPI_MODE_MIN, tmp.policy, tmp.applied, nullptr,
-                                    nullptr, nullptr, st); }, st);
-    p.k1_variant = saved;
-  } else {
-    best = 1;
-  }
-  if (best == 1) {
-    p.k1_variant = 9;
-    p.k1_blocks = (int32_t)std::min<int64_t>(h->tl_nblocks, h->num_sms);
-    p.k1_threads = 1024;
-    p.k1_smem_bytes = k1_tiled_smem(h);
-  } else {
-    k1_tiled_free(h);
-  }
-  return IPI_OK;
-}
-
 int plan_instance(ipi_mdp* h, cudaStream_t st) {
   PlanCtx c{h, st, h->n_local * (int64_t)h->m, {}};
   int rc = plan_row_stats(c);
   if (!rc) rc = plan_window_and_grid(c);
   if (!rc) rc = plan_deep(c);
-  if (!rc) rc = plan_tiled(c);
   if (!rc) rc = plan_uniform_ring(c);
   if (!rc) rc = plan_generic_autotune(c);
   if (!rc) rc = plan_flat_ring(c);
-  if (!rc) rc = plan_tma(c);
   if (rc) return rc;
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(IPI_ECUDA, std::string("planning kernels: ") + cudaGetErrorString(e));

@@ -45,6 +45,7 @@ struct K3Args {
   int pf;  // uniform ring: L2 bulk prefetch distance in steps beyond the ring (0 = off)
   unsigned long long* trace;  // diagnostics: per-CTA (smid, start ns, end ns) or nullptr
   int interleave;  // uniform ring: warp w takes 4-row steps w, w+NW, ... of its CTA (else a contiguous range)
+  const int* active;  // stepped GMRES (krylov_step.cu): skip the launch when *active == 0 (nullable)
 };
 
 __device__ __forceinline__ unsigned long long k3_ns() {
@@ -127,6 +128,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k3_uring(K3Args a, int win_bytes) 
   using L = K3URing<K>;
   constexpr bool NEED_B = EPI >= 2, NEED_XD = EPI == 1 || EPI == 2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  if (a.active && *a.active == 0) return;  // stepped GMRES: the cycle already ended
   k3_trace_begin(a);
   double* win = reinterpret_cast<double*>(smem_raw);
   const int64_t r_lo = k3_split(a.rows, blockIdx.x, gridDim.x, 4);
@@ -298,6 +300,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k3_flat(K3Args a, int win_bytes) {
   using L = K3Flat<K>;
   constexpr bool NEED_B = EPI >= 2, NEED_XD = EPI == 1 || EPI == 2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  if (a.active && *a.active == 0) return;  // stepped GMRES: the cycle already ended
   k3_trace_begin(a);
   double* win = reinterpret_cast<double*>(smem_raw);
   const int64_t r_lo = k3_split(a.rows, blockIdx.x, gridDim.x, 32);
@@ -491,13 +494,13 @@ static bool k3_launch_epi(const ipi_op* op, const K3Args& a, cudaStream_t st) {
 
 // y = epi(P x) over the operator's rows; generic rows use spmv.cu's kernel.
 int op_launch(const ipi_op* op, const double* x_full, const double* b, int epi, double* y,
-              cudaStream_t st, const double* y_partial) {
+              cudaStream_t st, const double* y_partial, const int* active) {
   if (op->n_local <= 0) return IPI_OK;
   if (op->variant == IPI_K3_GENERIC || epi >= 4)  // split halves: generic rows
     return launch_spmv(op->rp, op->col, op->val, op->n_local, x_full, b, op->gamma, epi, y,
                        op->lanes, st, op->state0, y_partial);
   K3Args a{op->col, op->val, op->n_local, op->state0, op->n_global, x_full, b, op->gamma, y, op->halo,
-            op->pf, op->trace, op->interleave};
+            op->pf, op->trace, op->interleave, active};
   bool ok = false;
   switch (epi) {
     case 0: ok = k3_launch_epi<0>(op, a, st); break;

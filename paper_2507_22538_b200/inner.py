@@ -1,7 +1,7 @@
 """Policy-evaluation Krylov solves on the device (mirrors ``mdpsolve.inner``).
 
 ``inner_solve`` (inner.py:163-213) runs the whole solve — Richardson,
-restarted GMRES(30) with MGS/Givens, BiCGStab or TFQMR, each with the
+restarted GMRES(30) with Givens rotations (CGS2 or the reference's MGS), BiCGStab or TFQMR, each with the
 reference's estimate-then-verify stopping and breakdown reporting — as one
 persistent cooperative kernel (krylov*.cu).  Preconditioning: NONE or
 JACOBI on the device path (left preconditioning exactly as the reference
@@ -108,8 +108,11 @@ def build_preconditioner(op, kind: Preconditioner, **_):
 
 def inner_solve(op: PolicyOperator, b, theta0, target_2norm: float, max_it: int,
                 kind: InnerSolver = InnerSolver.GMRES, pc=None, richardson_scale: float = 1.0,
-                workers=None, halo: int = -1):
-    """Approximately solve (I - gamma P) theta = b from theta0 (inner.py:163-213)."""
+                workers=None, halo: int = -1, ortho: str = "auto"):
+    """Approximately solve (I - gamma P) theta = b from theta0 (inner.py:163-213).
+
+    ``ortho`` (extension): GMRES orthogonalisation, "auto" (default), the
+    reference's "mgs", or "cgs2"."""
     was_np = not isinstance(b, torch.Tensor)
     dev = op.p_pi.values.device
     bt = torch.as_tensor(np.asarray(b, dtype=np.float64), device=dev) if was_np else \
@@ -126,6 +129,9 @@ def inner_solve(op: PolicyOperator, b, theta0, target_2norm: float, max_it: int,
         raise NotImplementedError("only the identity and Jacobi preconditioners run on the device")
     if kind not in DEVICE_KINDS:
         raise NotImplementedError(f"inner solver {kind.value!r} is not on the device path yet")
+    if ortho not in _lib.ORTHO:
+        raise ValueError(f"unknown GMRES orthogonalisation {ortho!r}; supported: "
+                         f"{', '.join(_lib.ORTHO)}")
     bt = bt.contiguous()
     x = x.contiguous()
     rep = _lib.InnerReport()
@@ -135,7 +141,8 @@ def inner_solve(op: PolicyOperator, b, theta0, target_2norm: float, max_it: int,
                                           _lib.ptr(x), float(target_2norm), int(max_it),
                                           _lib.KSP[kind.value], float(richardson_scale),
                                           _lib.ptr(pc.inv_diag) if pc is not None else None,
-                                          _lib.C.byref(rep), _lib.stream_ptr()), "ipi_inner_solve")
+                                          _lib.ORTHO[ortho], _lib.C.byref(rep),
+                                          _lib.stream_ptr()), "ipi_inner_solve")
     report = InnerSolveReport(iterations=rep.iterations,
                               final_linear_residual_2norm=rep.final_linear_residual_2norm,
                               converged=bool(rep.converged), breakdown=bool(rep.breakdown),

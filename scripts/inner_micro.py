@@ -32,6 +32,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="1,4,2")
     ap.add_argument("--its", type=int, default=300)
+    ap.add_argument("--ortho", default="cgs2,mgs")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     for cfg in [int(c) for c in a.configs.split(",")]:
@@ -41,7 +42,8 @@ def main():
         p = ipi.gather_policy_matrix(mdp, pi.long())
         b = mdp.stage_cost[torch.arange(mdp.n, device="cuda"), pi.long()].contiguous()
         plan = mdp.plan()
-        for kind in ("gmres", "richardson"):
+        kinds = [("gmres", o) for o in a.ortho.split(",")] + [("richardson", "cgs2")]
+        for kind, ortho in kinds:
             res = {}
             for its in (a.its // 2, a.its):  # slope: excludes planning and launch
                 for _ in range(2):
@@ -52,14 +54,15 @@ def main():
                     rc = _lib.lib().ipi_inner_solve(_lib.ptr(p.row_ptr), _lib.ptr(p.col_idx),
                                                     _lib.ptr(p.values), mdp.n, spec.gamma, _lib.ptr(b),
                                                     _lib.ptr(x), 0.0, its, _lib.KSP[kind], 1.0, None,
-                                                    _lib.C.byref(rep), _lib.stream_ptr())
+                                                    _lib.ORTHO[ortho], _lib.C.byref(rep),
+                                                    _lib.stream_ptr())
                     e1.record()
                     torch.cuda.synchronize()
                     _lib.check(rc)
                 res[its] = (e0.elapsed_time(e1), rep.iterations)
             (t0, i0), (t1, i1) = res[a.its // 2], res[a.its]
             ms = (t1 - t0) / max(i1 - i0, 1)
-            print(f"{spec.name} {kind}: {i1} its, {ms:.4f} ms/it (slope {i0}->{i1}), "
+            print(f"{spec.name} {kind}/{ortho}: {i1} its, {ms:.4f} ms/it (slope {i0}->{i1}), "
                   f"resid {rep.final_linear_residual_2norm:.3e} plan_halo={plan['halo']}", flush=True)
         del p, mdp
         torch.cuda.empty_cache()

@@ -283,38 +283,3 @@ def test_no_window_uniform_rows_pick_deep_kernel():
     rph, colh, valh = (t.cpu().numpy() for t in (rp, col, val))
     pi_ref, ap_ref = orc.greedy(rph, colh, valh, cost.cpu().numpy(), spec.gamma, v.cpu().numpy())
     np.testing.assert_allclose(app.cpu().numpy(), ap_ref, rtol=1e-13, atol=1e-13)
-
-
-@pytest.mark.parametrize("maximize", [False, True])
-@pytest.mark.parametrize("n_states,state0", [(20000, 0), (7777, 123457)])
-def test_tiled_kernel_matches_oracle(monkeypatch, maximize, n_states, state0):
-    """Variant 9 (column-tiled layout for window-less uniform rows, C5's shape)
-    against the oracle and the register-deep kernel on the same shard."""
-    from paper_2507_22538_b200 import devgen
-    from paper_2507_22538_b200.generators import CONFIGS
-    from paper_2507_22538_b200.parallel import MdpShard
-    spec = CONFIGS[5]
-    n, m = 1 << 20, 8
-    rp, col, val, cost = devgen.locality(n, m, spec.K, spec.window, 0, state0, n_states)
-    mode = ipi.Mode.MAX if maximize else ipi.Mode.MIN
-    csr = ipi.CsrMatrix(n_states * m, n, rp, col, val)
-    monkeypatch.setenv("IPI_K1_TILED", "1")
-    sh9 = MdpShard(n, m, spec.gamma, state0, cost, csr, mode=mode)
-    assert sh9.plan()["k1_variant"] == 9, sh9.plan()
-    monkeypatch.setenv("IPI_K1_TILED", "0")
-    sh3 = MdpShard(n, m, spec.gamma, state0, cost, csr, mode=mode)
-    assert sh3.plan()["k1_variant"] == 3, sh3.plan()
-    v = torch.rand(n, dtype=torch.float64, device="cuda") * 10
-    p9, a9, r9 = (t.clone() for t in sh9.bellman(v))
-    p3, a3, r3 = (t.clone() for t in sh3.bellman(v))
-    rph, colh, valh, costh = (t.cpu().numpy() for t in (rp, col, val, cost))
-    pi_ref, ap_ref = orc.greedy(rph, colh, valh, costh, spec.gamma, v.cpu().numpy(), maximize)
-    np.testing.assert_allclose(a9.cpu().numpy(), ap_ref, rtol=1e-13, atol=1e-13)
-    np.testing.assert_allclose(a3.cpu().numpy(), ap_ref, rtol=1e-13, atol=1e-13)
-    gap = orc.q_gap(rph, colh, valh, costh, spec.gamma, v.cpu().numpy(), maximize)
-    bad = np.flatnonzero(p9.cpu().numpy() != pi_ref)
-    assert np.all(gap[bad] < 1e-10)
-    vloc = v[state0:state0 + n_states]
-    assert float(r9.view(torch.float64)[0]) == float((vloc - a9).abs().max())
-    p9b, a9b, _ = sh9.bellman(v)  # deterministic rerun
-    assert torch.equal(p9b, p9) and torch.equal(a9b, a9)
