@@ -455,7 +455,23 @@ def run_ours(args):
             res = ipi.solve(mdp, ipi.SolveOptions(alpha=spec.alpha, tol=spec.atol))
             t_solve = time.perf_counter() - t0
             mdp._handle = None
+            # inner-solve roofline from the solve itself: algorithmic bytes of
+            # every Arnoldi step (K3 on P_pi: 12 nnz_pi + 8n x + 8n w; MGS:
+            # 8n w + 8n V_{j+1} + 8n per basis-vector pass) over time_inner;
+            # the per-cycle residual / x update launches are not counted
+            nnz_pi = n * spec.K
+            inner_bytes = (res.inner_iterations_total * (12 * nnz_pi + 32 * n)
+                           + res.basis_reads_total * 8 * n)
+            inner_ach = inner_bytes / max(res.time_inner, 1e-12) / 1e9
+            roof_solve = {"bound": "hbm", "achieved": inner_ach, "peak": peaks()[0], "unit": "GB/s",
+                          "frac": inner_ach / peaks()[0], "traffic": None,
+                          "kernel": "stepped GMRES (k3_uring + step_ortho)",
+                          "algorithmic_bytes": inner_bytes, "time_inner_s": res.time_inner,
+                          "inner_iterations": res.inner_iterations_total,
+                          "basis_reads": res.basis_reads_total,
+                          "ms_per_inner_iteration": 1e3 * res.time_inner / max(1, res.inner_iterations_total)}
             ipi_rep = {"time_to_tol_s": res.wall_time, "time_incl_validate_s": t_solve,
+                       "roofline_inner_solve": roof_solve,
                        "status": res.status.value, "outer": res.outer_iterations,
                        "inner": res.inner_iterations_total,
                        "final_residual": res.residual_history[-1],

@@ -80,7 +80,8 @@ typedef struct {
   int32_t iterations;
   int32_t converged;
   int32_t breakdown;
-  int32_t pad;
+  int32_t basis_reads; /* GMRES: basis-vector passes of the orthogonalisation (sum of j+1 over
+                          steps, MGS), for the roofline byte count; 0 where not counted */
   double final_linear_residual_2norm;
   double target_2norm; /* effective target after the floor (inner.py:189) */
 } ipi_inner_report;
@@ -109,6 +110,7 @@ typedef struct {
   double time_greedy;
   double time_assembly;
   double time_inner;
+  int64_t basis_reads_total; /* sum of the inner reports' basis_reads */
 } ipi_stats;
 
 /* Kernel plan chosen at ipi_mdp_create: exposed for reports/tests. */

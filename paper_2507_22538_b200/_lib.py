@@ -32,7 +32,7 @@ _f64 = C.c_double
 
 
 class InnerReport(C.Structure):
-    _fields_ = [("iterations", _i32), ("converged", _i32), ("breakdown", _i32), ("pad", _i32),
+    _fields_ = [("iterations", _i32), ("converged", _i32), ("breakdown", _i32), ("basis_reads", _i32),
                 ("final_linear_residual_2norm", _f64), ("target_2norm", _f64)]
 
 
@@ -45,7 +45,7 @@ class Opts(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("status", _i32), ("outer_iterations", _i32), ("inner_iterations_total", _i64),
                 ("wall_time", _f64), ("time_greedy", _f64), ("time_assembly", _f64),
-                ("time_inner", _f64)]
+                ("time_inner", _f64), ("basis_reads_total", _i64)]
 
 
 class Plan(C.Structure):

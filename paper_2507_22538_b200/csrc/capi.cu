@@ -889,7 +889,7 @@ int ipi_solve(ipi_mdp* h, const ipi_opts* o, double* v, int32_t* policy, double*
   double* host = reinterpret_cast<double*>(h->host_pinned);
   ipi_inner_report* hrep = reinterpret_cast<ipi_inner_report*>(host + 8);
   std::vector<double> hist;
-  int64_t inner_total = 0;
+  int64_t inner_total = 0, basis_total = 0;
   int stall = 0;
   int k = 0;
   int status = IPI_CONVERGED;
@@ -914,6 +914,7 @@ int ipi_solve(ipi_mdp* h, const ipi_opts* o, double* v, int32_t* policy, double*
     }
     if (pending_report) {
       inner_total += hrep->iterations;
+      basis_total += hrep->basis_reads;
       pending_report = false;
     }
     const double res = host[0];
@@ -972,6 +973,7 @@ int ipi_solve(ipi_mdp* h, const ipi_opts* o, double* v, int32_t* policy, double*
       IPI_CUDA_TRY(cudaMemcpyAsync(hrep, h->d_report, sizeof(ipi_inner_report), cudaMemcpyDeviceToHost, st));
       IPI_CUDA_TRY(cudaStreamSynchronize(st));
       inner_total += hrep->iterations;
+      basis_total += hrep->basis_reads;
       if (hrep->breakdown) {
         // one plain evaluation sweep from the pre-solve V: theta = g_pi + gamma * P_pi v
         rc = launch_spmv(h->rp_pi, h->col_pi, h->val_pi, n, vcur, h->gpi, h->gamma, 3, vnext,
@@ -1000,6 +1002,7 @@ int ipi_solve(ipi_mdp* h, const ipi_opts* o, double* v, int32_t* policy, double*
   stats->time_greedy = tg;
   stats->time_assembly = ta;
   stats->time_inner = ti;
+  stats->basis_reads_total = basis_total;
   return IPI_OK;
 }
 

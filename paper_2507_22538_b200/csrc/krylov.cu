@@ -62,6 +62,11 @@ double* krylov_workspace(int64_t doubles_needed, cudaStream_t st) {
 static unsigned long long* g_k4_trace = nullptr;
 static int g_k4_trace_cap = 0;
 
+unsigned long long* k4_trace_buffer(int* cap) {
+  *cap = g_k4_trace_cap;
+  return g_k4_trace;
+}
+
 int k4_trace(int enable, unsigned long long* out, int cap) {
   if (enable) {
     if (!g_k4_trace) {

@@ -68,17 +68,20 @@ struct KArgs {
 
 // Diagnostics: CTA 0 records %globaltimer at phase boundaries (trace[1..]);
 // trace[0] counts the records.
-__device__ __forceinline__ void k4_mark(const KArgs& a) {
-  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+__device__ __forceinline__ void k4_mark_raw(unsigned long long* trace, int cap) {
+  if (trace && blockIdx.x == 0 && threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    const unsigned long long k = a.trace[0];
-    if ((int)k + 1 < a.trace_cap) {
-      a.trace[k + 1] = t;
-      a.trace[0] = k + 1;
+    const unsigned long long k = trace[0];
+    if ((int)k + 1 < cap) {
+      trace[k + 1] = t;
+      trace[0] = k + 1;
     }
   }
 }
+__device__ __forceinline__ void k4_mark(const KArgs& a) { k4_mark_raw(a.trace, a.trace_cap); }
+// the buffer ipi_k4_trace enabled (nullptr when off)
+unsigned long long* k4_trace_buffer(int* cap);
 
 // doubles per CTA and slot in the all-reduce partials (the CGS dot vector:
 // up to R projections + one norm)
@@ -899,6 +902,7 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
   }
   if (blockIdx.x == 0 && tid == 0) {
     a.rep->iterations = it;
+    a.rep->basis_reads = 0;  // not counted by the persistent kernels
     a.rep->final_linear_residual_2norm = rn;
     a.rep->converged = (rn <= eff && !brk) ? 1 : 0;
     a.rep->breakdown = brk;

@@ -466,6 +466,7 @@ __global__ void IPI_K4_REGS(NW) inner_ring_kernel(KArgs a) {
   }
   if (blockIdx.x == 0 && tid == 0) {
     a.rep->iterations = it;
+    a.rep->basis_reads = 0;  // not counted by the persistent kernels
     a.rep->final_linear_residual_2norm = rn;
     a.rep->converged = rn <= eff ? 1 : 0;
     a.rep->breakdown = 0;

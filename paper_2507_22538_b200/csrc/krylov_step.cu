@@ -37,7 +37,7 @@ struct StepState {
   double H[(R + 1) * R];
   double cs[R], sn[R], g[R + 1];
   double eff, est_target, rn, target;
-  int j, it, active, done;
+  int j, it, active, done, basis_reads;
 };
 
 // Host-mapped mirror of the flags the host loop reads (written by CTA 0).
@@ -50,7 +50,8 @@ struct StepArgs {
   int64_t n;
   const double* b;
   double* x;
-  double* V;  // (R+1) * n basis
+  double* V;  // (R+1) x ldv basis (ldv even: every slice start 16-byte aligned)
+  int64_t ldv;
   double* w;
   double* r;
   double* partials;
@@ -61,15 +62,23 @@ struct StepArgs {
   StepFlags* hf;  // host-mapped (device pointer)
   int max_it;
   int first;  // step_cycle_start: first call of the solve
+  unsigned long long* trace;  // diagnostics (ipi_k4_trace): step_ortho start / MGS done / end
+  int trace_cap;
 };
 
 constexpr int kStepThreads = 512;
-constexpr int kStepE = 16;  // slice elements per thread: n <= 148 * 512 * 16 = 1.21M
+constexpr int kStepE = 16;  // slice elements per worker thread: n <= 148 * 480 * 16 = 1.14M
+// Warp 0 owns no slice elements: thread 0 leads the grid barriers, and a
+// release (red.release.gpu) waits for the leader's own outstanding loads, so
+// a leader holding V_{l+1} prefetches would serialise them into every
+// all-reduce (3.9 vs ~2.5 us per MGS pass on C2).
+constexpr int kStepWorkers = kStepThreads - 32;
 
+// CTA c's slice of the vectors, boundaries even (16-byte aligned bulk copies)
 __device__ __forceinline__ void step_slice(int64_t n, int64_t& lo, int64_t& hi) {
   const int64_t c = blockIdx.x, nb = gridDim.x;
-  lo = n * c / nb;
-  hi = n * (c + 1) / nb;
+  lo = c == 0 ? 0 : ((n * c / nb) & ~(int64_t)1);
+  hi = c + 1 == nb ? n : ((n * (c + 1) / nb) & ~(int64_t)1);
 }
 
 // grid_allreduce (krylov.cuh) reads only KArgs::partials; wrap ours.
@@ -89,21 +98,32 @@ __device__ __forceinline__ void publish_flags(const StepArgs& a, const StepState
   __threadfence_system();
 }
 
-// One Arnoldi step after the K3 launch wrote w = V_j - gamma P V_j.
+// One Arnoldi step after the K3 launch wrote w = V_j - gamma P V_j: MGS with
+// this CTA's slice of w in registers and V_{l+1}'s slice loaded into
+// registers while the all-reduce producing h_l is in flight, so a pass costs
+// one grid all-reduce plus register arithmetic (C2: ~3.5 us per pass).
+// (Streaming the slices through shared memory with 1-D bulk copies two
+// passes ahead measured slower: 4.5 us per pass.)
 __global__ void __launch_bounds__(kStepThreads, 1) step_ortho(StepArgs a) {
   __shared__ KShared sh;
   __shared__ double hcol[R + 1], cs_s[R], sn_s[R], gj_s, est_s;
   __shared__ int brk_s;
   StepState* st = a.s;
-  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int tid = threadIdx.x;
   // the next cooperative launch's barrier counter (its previous user, two
   // launches back, has retired); reset even when this launch is a no-op
   if (blockIdx.x == 0 && tid == 0) a.bar[a.parity ^ 1] = 0u;
   if (!st->active) return;  // uniform: the previous launch ended the cycle
+  k4_mark_raw(a.trace, a.trace_cap);
   GridBarrier gb{a.bar + a.parity, 0u, 0};
   const KArgs ka = step_kargs(a);
   int slot = 0;
   const int j = st->j;
+  const int64_t n = a.n, ldv = a.ldv;
+  int64_t s_lo, s_hi;
+  step_slice(n, s_lo, s_hi);
+  const int64_t own = s_hi - s_lo;
+  const uint64_t pol_keep = policy_evict_last(), pol_first = policy_evict_first();
   if (tid == 0) {  // snapshot the rotation state before the first grid barrier:
     for (int l = 0; l < j; ++l) {  // CTA 0 updates g[j] after the last one
       cs_s[l] = st->cs[l];
@@ -112,20 +132,17 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_ortho(StepArgs a) {
     gj_s = st->g[j];
     est_s = st->est_target;
   }
-  const int64_t n = a.n;
-  int64_t s_lo, s_hi;
-  step_slice(n, s_lo, s_hi);
-  const int64_t own = s_hi - s_lo;
-  const uint64_t pol_last = policy_evict_last(), pol_first = policy_evict_first();
   double wv[kStepE], vc[kStepE];
+  const int64_t wt = tid - 32;  // worker index (< 0: the control warp)
+  auto elem = [&](int k) -> int64_t { return wt < 0 ? own : wt + (int64_t)k * kStepWorkers; };
 #pragma unroll
   for (int k = 0; k < kStepE; ++k) {
-    const int64_t e = tid + (int64_t)k * nthr;
+    const int64_t e = elem(k);
     double wi = 0.0, v0 = 0.0;
     if (e < own) {
       wi = a.w[s_lo + e];
       if (a.invd) wi = mul_rn(wi, a.invd[s_lo + e]);  // w = pc(A v_j)  (inner.py:249)
-      v0 = ld_hint(a.V + s_lo + e, j > 0 ? pol_last : pol_first);
+      v0 = ld_hint(a.V + s_lo + e, j > 0 ? pol_keep : pol_first);
     }
     wv[k] = wi;
     vc[k] = v0;
@@ -136,11 +153,11 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_ortho(StepArgs a) {
   for (int l = 0; l <= j; ++l) {
     double vn[kStepE];
     if (l < j) {  // V_{l+1} in flight while h_l is reduced
-      const double* Vn = a.V + (int64_t)(l + 1) * n + s_lo;
-      const uint64_t pol = l + 1 < j ? pol_last : pol_first;
+      const double* Vn = a.V + (int64_t)(l + 1) * ldv + s_lo;
+      const uint64_t pol = l + 1 < j ? pol_keep : pol_first;
 #pragma unroll
       for (int k = 0; k < kStepE; ++k) {
-        const int64_t e = tid + (int64_t)k * nthr;
+        const int64_t e = elem(k);
         vn[k] = e < own ? ld_hint(Vn + e, pol) : 0.0;
       }
     }
@@ -164,6 +181,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_ortho(StepArgs a) {
   }
   grid_allreduce<1>(p, ka, slot, gb, sh);
   const double hnorm = sqrt(p[0]);
+  k4_mark_raw(a.trace, a.trace_cap);
   // Givens update (inner.py:256-270), redundantly in every CTA; CTA 0 stores.
   if (tid == 0) {
     hcol[j + 1] = hnorm;
@@ -202,21 +220,21 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_ortho(StepArgs a) {
       const int itn = st->it + 1;
       st->j = jn;
       st->it = itn;
+      st->basis_reads += j + 1;
       st->active = (brk == 0 && jn < R && itn < a.max_it) ? 1 : 0;
       publish_flags(a, *st);
     }
   }
   __syncthreads();
-  if (brk_s == 0 || brk_s == 2) {
-    if (brk_s == 0) {  // V_{j+1} = w / hnorm: the next K3 launch's input, keep it in L2
-      double* Vnew = a.V + (int64_t)(j + 1) * n + s_lo;
+  if (brk_s == 0) {  // V_{j+1} = w / hnorm: the next K3 launch's input, keep it in L2
+    double* Vnew = a.V + (int64_t)(j + 1) * ldv + s_lo;
 #pragma unroll
-      for (int k = 0; k < kStepE; ++k) {
-        const int64_t e = tid + (int64_t)k * nthr;
-        if (e < own) st_hint(Vnew + e, wv[k] / hnorm, pol_last);
-      }
+    for (int k = 0; k < kStepE; ++k) {
+      const int64_t e = elem(k);
+      if (e < own) st_hint(Vnew + e, wv[k] / hnorm, pol_keep);
     }
   }
+  k4_mark_raw(a.trace, a.trace_cap);
 }
 
 // Cycle end (inner.py:272-276): y = H^-1 g by back substitution (:286-292,
@@ -240,7 +258,7 @@ __global__ void __launch_bounds__(kStepThreads) step_cycle_end(StepArgs a) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     double t = 0.0;
-    for (int l = 0; l < j; ++l) t = add_rn(t, mul_rn(a.V[(int64_t)l * n + i], y[l]));
+    for (int l = 0; l < j; ++l) t = add_rn(t, mul_rn(a.V[(int64_t)l * a.ldv + i], y[l]));
     a.x[i] = add_rn(a.x[i], t);
   }
 }
@@ -318,11 +336,12 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_cycle_start(StepArgs a) 
 }
 
 bool stepped_gmres_fits(int64_t n, int sms) {
-  return n <= (int64_t)sms * kStepThreads * kStepE;
+  return (n + sms - 1) / sms + 2 <= (int64_t)kStepWorkers * kStepE;
 }
 
 int64_t stepped_gmres_workspace(int64_t n, int blocks) {
-  return (int64_t)(R + 1) * n + 2 * n + 2 * kPartStride * (int64_t)blocks + 64 +
+  const int64_t ldv = (n + 1) & ~(int64_t)1;
+  return (int64_t)(R + 1) * ldv + 2 * n + 2 + 2 * kPartStride * (int64_t)blocks + 64 +
          (int64_t)(sizeof(StepState) + 7) / 8;
 }
 
@@ -347,15 +366,18 @@ int stepped_gmres(const ipi_op* op, int64_t n, const double* b, double* x, doubl
   a.n = n;
   a.b = b;
   a.x = x;
+  a.ldv = (n + 1) & ~(int64_t)1;
   a.V = ws;
-  a.w = ws + (int64_t)(R + 1) * n;
-  a.r = a.w + n;
+  a.w = ws + (int64_t)(R + 1) * a.ldv;
+  a.r = a.w + n + 2;
   a.partials = a.r + n;
   a.bar = reinterpret_cast<unsigned*>(a.partials + 2 * kPartStride * (int64_t)blocks);
   a.s = reinterpret_cast<StepState*>(a.partials + 2 * kPartStride * (int64_t)blocks + 64);
   a.invd = inv_diag;
   a.hf = hf_dev;
   a.max_it = max_it;
+  a.trace = k4_trace_buffer(&a.trace_cap);
+  if (a.trace) IPI_CUDA_TRY(cudaMemsetAsync(a.trace, 0, sizeof(unsigned long long), st));
   IPI_CUDA_TRY(cudaMemsetAsync(a.bar, 0, 2 * sizeof(unsigned), st));
   {
     StepState init{};
@@ -363,16 +385,14 @@ int stepped_gmres(const ipi_op* op, int64_t n, const double* b, double* x, doubl
     IPI_CUDA_TRY(cudaMemcpyAsync(a.s, &init, sizeof(init), cudaMemcpyHostToDevice, st));
   }
   const int* active = &a.s->active;
-  static bool attr_done[64] = {};
-  if (!attr_done[dev]) {
+  {
     int per_sm = 0;
     IPI_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_ortho, kStepThreads, 0));
     if (per_sm < 1) return fail(IPI_ECUDA, "step_ortho cannot be resident");
-    attr_done[dev] = true;
   }
-  auto coop = [&](const void* fn) -> int {
+  auto coop = [&](const void* fn, int smem = 0) -> int {
     void* args[] = {(void*)&a};
-    IPI_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(kStepThreads), args, 0, st));
+    IPI_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(kStepThreads), args, (size_t)smem, st));
     a.parity ^= 1;
     return IPI_OK;
   };
@@ -410,7 +430,7 @@ int stepped_gmres(const ipi_op* op, int64_t n, const double* b, double* x, doubl
     int issued = 0, waited = 0;
     auto issue = [&]() -> int {
       int e;
-      if ((e = op_launch(op, a.V + (int64_t)issued * n, nullptr, 1, a.w, st, nullptr, active))) return e;
+      if ((e = op_launch(op, a.V + (int64_t)issued * a.ldv, nullptr, 1, a.w, st, nullptr, active))) return e;
       if ((e = coop((const void*)step_ortho))) return e;
       IPI_CUDA_TRY(cudaEventRecord(ev[issued & 1], st));
       ++issued;
@@ -448,6 +468,7 @@ int stepped_gmres(const ipi_op* op, int64_t n, const double* b, double* x, doubl
   rep.final_linear_residual_2norm = fin.rn;
   rep.converged = fin.rn <= fin.eff ? 1 : 0;
   rep.breakdown = 0;
+  rep.basis_reads = fin.basis_reads;
   rep.target_2norm = fin.eff;
   IPI_CUDA_TRY(cudaMemcpyAsync(d_report, &rep, sizeof(rep), cudaMemcpyHostToDevice, st));
   IPI_CUDA_TRY(cudaStreamSynchronize(st));

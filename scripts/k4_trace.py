@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--its", type=int, default=60)
     ap.add_argument("--kind", default="gmres")
+    ap.add_argument("--stepped", action="store_true")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     mdp, spec = devgen.build_instance(a.config)
@@ -72,6 +73,20 @@ def main():
     _lib.check(L.ipi_k4_trace(0, buf.ctypes.data, 8192))
     k = int(buf[0])
     t0 = buf[1:k + 1].astype(np.int64)
+    if a.stepped:
+        # step_ortho marks: start, MGS done, end (3 per step); gaps = K3 + launches
+        t3 = t0[: (len(t0) // 3) * 3].reshape(-1, 3)
+        mgs = (t3[:, 1] - t3[:, 0]) / 1e3
+        giv = (t3[:, 2] - t3[:, 1]) / 1e3
+        gap = (t3[1:, 0] - t3[:-1, 2]) / 1e3
+        print(f"stepped: {len(t3)} steps; MGS median {np.median(mgs):.1f} us (p10 {np.percentile(mgs, 10):.1f}"
+              f" p90 {np.percentile(mgs, 90):.1f}); Givens+write {np.median(giv):.1f} us; "
+              f"ortho end -> next ortho start (K3 + launch gaps) median {np.median(gap):.1f} us")
+        per_j = {}
+        for i, v in enumerate(mgs):
+            per_j.setdefault(i % 30, []).append(v)
+        print("  MGS us by j:", {j: round(float(np.median(v)), 1) for j, v in sorted(per_j.items())})
+        return
     print(f"  initial residual pass (first SpMV of the launch): {(t0[1] - t0[0]) / 1e3:.1f} us, "
           f"its all-reduce {(t0[2] - t0[1]) / 1e3:.1f} us")
     t = t0[3:]

@@ -42,7 +42,7 @@ __device__ __forceinline__ unsigned atom_add_acqrel(unsigned* p, unsigned v) {
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(1024, 1) k(double* partials, unsigned* ctr, double* pub, int iters, double* out) {
+__global__ void __launch_bounds__(1024) k(double* partials, unsigned* ctr, double* pub, int iters, double* out) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double red[32];
   __shared__ double bc;
@@ -97,6 +97,30 @@ __global__ void __launch_bounds__(1024, 1) k(double* partials, unsigned* ctr, do
         s = warp_sum(s);
         if (threadIdx.x == 0) bc = s;
       }
+    } else if (MODE == 4) {
+      // arrivals spread over 8 counters (one 128-byte line each) so the 148
+      // release adds do not serialise on one L2 address; the leader polls all
+      // 8 with relaxed loads (one round trip per poll) and then fences.
+      ++epoch;
+      if (threadIdx.x == 0) {
+        partials[(it & 1) * nb + blockIdx.x] = t;
+        red_release(ctr + 64 + (blockIdx.x & 7) * 32, 1u);
+      }
+      if (threadIdx.x < 8) {
+        const unsigned per = (unsigned)((nb - threadIdx.x + 7) / 8);
+        unsigned v;
+        do {
+          asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr + 64 + threadIdx.x * 32) : "memory");
+        } while (v < epoch * per);
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      }
+      __syncwarp();
+      if (threadIdx.x < 32) {
+        double s = 0;
+        for (int i = threadIdx.x; i < nb; i += 32) s = __dadd_rn(s, __ldcg(partials + (it & 1) * nb + i));
+        s = warp_sum(s);
+        if (threadIdx.x == 0) bc = s;
+      }
     } else {
       ++epoch;
       if (threadIdx.x < 32) {
@@ -135,24 +159,25 @@ int main() {
   cudaMalloc(&partials, 16 * sms * sizeof(double));
   cudaMalloc(&pub, 64);
   cudaMalloc(&out, 64);
-  cudaMalloc(&ctr, 256);
+  cudaMalloc(&ctr, 4096);
   const int iters = 2000;
-  for (int mode = 0; mode < 4; ++mode) {
+  for (int mode = 0; mode < 5; ++mode)
+  for (int threads = 1024; threads >= 128; threads /= 2) {
     for (int rep = 0; rep < 2; ++rep) {
-      cudaMemset(ctr, 0, 256);
+      cudaMemset(ctr, 0, 4096);
       cudaMemset(partials, 0, 16 * sms * sizeof(double));
       void* args[] = {&partials, &ctr, &pub, (void*)&iters, &out};
       cudaEvent_t a, b;
       cudaEventCreate(&a);
       cudaEventCreate(&b);
       cudaEventRecord(a);
-      const void* fn = mode == 0 ? (const void*)k<0> : mode == 1 ? (const void*)k<1> : mode == 2 ? (const void*)k<2> : (const void*)k<3>;
-      cudaError_t e = cudaLaunchCooperativeKernel(fn, sms, 1024, args, 0, 0);
+      const void* fn = mode == 0 ? (const void*)k<0> : mode == 1 ? (const void*)k<1> : mode == 2 ? (const void*)k<2> : mode == 3 ? (const void*)k<3> : (const void*)k<4>;
+      cudaError_t e = cudaLaunchCooperativeKernel(fn, sms, threads, args, 0, 0);
       cudaEventRecord(b);
       cudaEventSynchronize(b);
       float ms;
       cudaEventElapsedTime(&ms, a, b);
-      if (rep) printf("mode %d: %.3f us per all-reduce (%s)\n", mode, ms * 1e3 / iters, cudaGetErrorString(e));
+      if (rep) printf("mode %d threads %4d: %.3f us per all-reduce (%s)\n", mode, threads, ms * 1e3 / iters, cudaGetErrorString(e));
     }
   }
   return 0;
