@@ -188,49 +188,69 @@ def build_shard(ctx, args, torch):
     return spec, n, shard
 
 
-def cpu_baseline_sample(shard, spec, n, torch, target_s=10.0):
-    """CPU oracle greedy on a prefix of the same instance (rank 0, N = 1).
+def bench_config(spec, n, world, nnz):
+    """The workload description both arms print (identical keys and values)."""
+    return {"workload": spec.name, "n_states": n, "n_actions": spec.m, "nnz_per_row": spec.K,
+            "nnz": int(nnz), "gamma": spec.gamma, "window": spec.window,
+            "parallelism": f"rowblock{world}",
+            "l2": "inputs 25.8 GB >> 126 MB L2: no flush needed",
+            "step": "V all-gather (N>1) + fused Bellman backup over all rows"}
 
-    Primary: the C/OpenMP restatement (oracle/mdp_oracle.c, bitwise equal to
-    the reference's greedy_policy on every golden fixture) with all host
-    threads on the first n/4 states.  Secondary: the numpy restatement (the
-    reference's own arithmetic, single thread) on the first n/64 states."""
+
+def cpu_reference_leg(rp, col, val, cost, spec, n, target_s=10.0, v_gpu=None):
+    """The CPU oracle on the FULL C2 instance (the same arrays the GPU holds):
+    greedy_policy throughput (C/OpenMP restatement, bitwise equal to the
+    reference's greedy_policy on every golden fixture; all host threads, best
+    of the reps that fit in ~target_s) and iPI time-to-tolerance of the same
+    instance from V0 = 0 (driver.py:109-209 restated, GMRES, alpha 1e-4, atol
+    1e-8).  When the GPU's solution is given, its distance to the CPU one is
+    reported beside it."""
     import os
     from oracle import c_oracle as co
-    from oracle import mdp_oracle as orc
-    t = shard.transitions
-    S = min(shard.n_local, max(1024, shard.n_local // 4))
-    rows = S * spec.m
-    nnz = int(t.row_ptr[rows])
-    rp = t.row_ptr[: rows + 1].cpu().numpy()
-    col = t.col_idx[:nnz].cpu().numpy()
-    val = t.values[:nnz].cpu().numpy()
-    cost = shard.stage_cost[:S].cpu().numpy()
-    v = np.random.default_rng(1).random(n)
     nt = os.cpu_count() or 1
+    rows = n * spec.m
+    nnz = int(rp[-1])
+    v = np.random.default_rng(1).random(n)
     co.greedy(rp, col, val, cost, spec.gamma, v, nthreads=nt)  # warm-up (page-in)
     times = []
     t_start = time.perf_counter()
-    while time.perf_counter() - t_start < target_s and len(times) < 50:
+    while time.perf_counter() - t_start < target_s and len(times) < 20:
         t0 = time.perf_counter()
         co.greedy(rp, col, val, cost, spec.gamma, v, nthreads=nt)
         times.append(time.perf_counter() - t0)
     best = min(times)
+    t0 = time.perf_counter()
+    sol = co.solve(rp, col, val, cost, spec.gamma, tol=spec.atol, alpha=spec.alpha, nthreads=nt)
+    t_solve = time.perf_counter() - t0
     out = {"value": rows / best, "unit": "(s,a)-backups/s", "cores": nt, "kind": "port",
-           "sample": f"first {S} of {n} states ({rows} rows, {nnz} nnz) of the same C2 instance; "
-                     f"C/OpenMP oracle greedy (oracle/mdp_oracle.c, bitwise equal to the "
-                     f"reference's greedy_policy on the golden fixtures), {nt} threads, best of "
-                     f"{len(times)} reps",
-           "nnz_per_s": nnz / best, "seconds": best}
-    S2 = max(256, S // 16)
+           "sample": f"the full instance: {n} states ({rows} rows, {nnz} nnz), the same arrays as "
+                     f"the GPU run; C/OpenMP oracle greedy (oracle/mdp_oracle.c, bitwise equal to "
+                     f"the reference's greedy_policy on the golden fixtures), {nt} threads, best "
+                     f"of {len(times)} reps",
+           "nnz_per_s": nnz / best, "seconds": best,
+           "ipi_time_to_tol_s": t_solve, "ipi_status": sol.status, "ipi_outer": sol.outer_iterations,
+           "ipi_inner": sol.inner_iterations_total,
+           "ipi_final_residual": sol.residual_history[-1],
+           "ipi_what": "oracle/c_oracle.solve (driver.py:109-209 restated, GMRES(30) MGS, "
+                       f"alpha {spec.alpha}, atol {spec.atol}), {nt} threads"}
+    if v_gpu is not None:
+        out["ipi_gpu_vs_cpu_max_rel_diff"] = float(
+            np.max(np.abs(np.asarray(v_gpu) - sol.values)) / max(1.0, np.max(np.abs(sol.values))))
+    return out
+
+
+def cpu_numpy_sample(rp, col, val, cost, spec, v):
+    """The numpy oracle (the reference's own arithmetic, single thread) on the
+    first n/64 states: the per-core rate of the reference as written."""
+    from oracle import mdp_oracle as orc
+    S2 = max(256, cost.shape[0] // 64)
     r2 = S2 * spec.m
     z2 = int(rp[r2])
     t0 = time.perf_counter()
     orc.greedy(rp[: r2 + 1], col[:z2], val[:z2], cost[:S2], spec.gamma, v)
     dt = time.perf_counter() - t0
-    out["numpy_single_thread"] = {"value": r2 / dt, "unit": "(s,a)-backups/s", "cores": 1,
-                                  "sample": f"first {S2} states, numpy oracle (reference arithmetic)"}
-    return out
+    return {"value": r2 / dt, "unit": "(s,a)-backups/s", "cores": 1,
+            "sample": f"first {S2} states, numpy oracle (reference arithmetic)"}
 
 
 def run_reference(args):
@@ -239,8 +259,9 @@ def run_reference(args):
     The reference is Python/numpy and is not present on the GPU box; its
     algorithm runs as the C/OpenMP restatement (bitwise equal to the
     reference's greedy_policy on every golden fixture), with all host threads,
-    on a bounded sample of the same C2 instance (the first n/8 states, built
-    by the same Philox recipe on the host)."""
+    on the FULL C2 instance (built by the same Philox recipe on the host: the
+    same arrays the GPU arm generates on the device).  A step is one greedy
+    pass over all rows, like the GPU arm's."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -248,11 +269,11 @@ def run_reference(args):
     from paper_2507_22538_b200.generators import CONFIGS
     spec = CONFIGS[WORKLOAD]
     n = spec.n // args.scale
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     nt = os.cpu_count() or 1
-    S = max(1024, n // 8)
-    rp, col, val, cost = co.gen_locality(n, spec.m, spec.K, spec.window, args.seed, 0, S,
+    rp, col, val, cost = co.gen_locality(n, spec.m, spec.K, spec.window, args.seed, 0, n,
                                          nthreads=nt)
-    rows = S * spec.m
+    rows = n * spec.m
     v = np.random.default_rng(1).random(n)
     for _ in range(max(args.warmup, 1)):
         co.greedy(rp, col, val, cost, spec.gamma, v, nthreads=nt)
@@ -261,7 +282,7 @@ def run_reference(args):
         co.greedy(rp, col, val, cost, spec.gamma, v, nthreads=nt)
     dt = (time.perf_counter() - t0) / args.steps
     value = rows / dt
-    sample = (f"first {S} of {n} states ({rows} rows, {rows * spec.K} nnz) of C2 per step; "
+    sample = (f"the full instance per step: {n} states ({rows} rows, {int(rp[-1])} nnz) of C2; "
               f"C/OpenMP oracle greedy (restates bellman.py:44-68, bitwise equal to the "
               f"reference on the golden fixtures), {nt} threads")
     line = {
@@ -269,9 +290,7 @@ def run_reference(args):
         "unit": "(s,a)-backups/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": spec.name, "n_states": n, "n_actions": spec.m,
-                   "nnz_per_row": spec.K, "gamma": spec.gamma, "sample_states": S,
-                   "sample_rows": rows},
+        "config": bench_config(spec, n, world, int(rp[-1])),
         "cpu_baseline": {"value": value, "unit": "(s,a)-backups/s", "cores": nt, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": "(s,a)-backups/s", "h2d_bytes_per_step": 0,
@@ -442,9 +461,8 @@ def run_ours(args):
     out = None
     if rank == 0:
         cpu = None
-        if world == 1 and not args.no_cpu:
-            cpu = cpu_baseline_sample(shard, spec, n, torch)
         ipi_rep = None
+        v_gpu = None
         if world == 1 and not args.no_ipi:
             mdp = ipi.MdpInstance(n=n, m=spec.m, gamma=spec.gamma, stage_cost=shard.stage_cost,
                                   transitions=shard.transitions)
@@ -478,17 +496,22 @@ def run_ours(args):
                        "time_greedy_s": res.time_greedy, "time_assembly_s": res.time_assembly,
                        "time_inner_s": res.time_inner,
                        "residual_history": res.residual_history}
+            v_gpu = res.values
+        if world == 1 and not args.no_cpu:
+            # the same arrays the GPU holds, copied to the host (25.8 GB)
+            t = shard.transitions
+            rp_h, col_h, val_h = (x.cpu().numpy() for x in (t.row_ptr, t.col_idx, t.values))
+            cost_h = shard.stage_cost.cpu().numpy()
+            cpu = cpu_reference_leg(rp_h, col_h, val_h, cost_h, spec, n, v_gpu=v_gpu)
+            cpu["numpy_single_thread"] = cpu_numpy_sample(rp_h, col_h, val_h, cost_h, spec,
+                                                          np.random.default_rng(1).random(n))
+            del rp_h, col_h, val_h, cost_h
         out = {
             "metric": "bellman_backups_per_s", "value": value, "unit": "(s,a)-backups/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (device Philox generator, seed %d)" % args.seed,
-            "config": {"workload": spec.name, "n_states": n, "n_actions": spec.m,
-                       "nnz_per_row": spec.K, "nnz": int(nnz) * (world if world > 1 else 1),
-                       "gamma": spec.gamma, "window": spec.window,
-                       "parallelism": f"rowblock{world}",
-                       "l2": "inputs 25.8 GB >> 126 MB L2: no flush needed",
-                       "step": "V all-gather (N>1) + fused Bellman backup over all rows"},
+            "config": bench_config(spec, n, world, int(nnz) * (world if world > 1 else 1)),
             "nnz_per_s": nnz * world / (ms_step * 1e-3),
             "state_backups_per_s": n / (ms_step * 1e-3),
             "e2e": {"value": e2e_value, "unit": "(s,a)-backups/s", "h2d_bytes_per_step": h2d * world,

@@ -288,6 +288,38 @@ int ipi_k4_trace(int32_t enable, uint64_t* out, int32_t cap);
  * kernel, y = x - gamma P x (K = 64 rows), timed over reps launches. */
 int ipi_k4_ring_apply_test(const int32_t* col, const double* val, int64_t n, double gamma,
                            const double* x, double* y, int32_t reps, float* ms, void* stream);
+/* ---- row-sharded iPI (one process per GPU) ------------ */
+/* The two exchanges of the sharded path, supplied by the caller: NCCL over
+ * NVLink (ipi_comm_nccl) in production, host-staged gloo callbacks in the CPU
+ * tests.  Both are stream-ordered on `stream` and return IPI_OK or an error. */
+typedef struct {
+  void* ctx;
+  int32_t rank, world;
+  /* every rank's block of the state vector (rank r: block_start[r] ..
+   * block_start[r+1], make_partition, model.py:95-109) into `full` */
+  int (*allgather_blocks)(void* ctx, const double* local, double* full, void* stream);
+  /* each rank's `count` doubles -> out (world x count, rank-major) */
+  int (*allgather)(void* ctx, const double* send, double* out, int64_t count, void* stream);
+} ipi_comm;
+/* An ipi_comm over an existing NCCL communicator (ncclComm_t, e.g. torch's
+ * ProcessGroupNCCL._comm_ptr()); block_start (world+1 entries) is copied.
+ * libnccl.so.2 is resolved at run time (the one the process already loaded). */
+int ipi_comm_nccl(void* nccl_comm, int32_t rank, int32_t world, const int64_t* block_start,
+                  ipi_comm* out);
+void ipi_comm_nccl_destroy(ipi_comm* c);
+/* Synchronous copy between any two (UVA) pointers on `stream`: the staging of
+ * host-side collectives (gloo test callbacks). */
+int ipi_memcpy_sync(void* dst, const void* src, int64_t bytes, void* stream);
+/* driver.py:109-209 across ranks: `h` is this rank's shard (ipi_mdp_create with
+ * state0 / n_global), v_local its block of V0 (in) and of the final V (out),
+ * policy its block of the final greedy policy.  Inner solves: GMRES(30) with
+ * CGS2 orthogonalisation (3 all-gathers of partial dots per Arnoldi step) or
+ * Richardson; preconditioner none or jacobi; opts->mode overrides the
+ * shard's.  Every rank returns the same history, counts and status. */
+int ipi_solve_sharded(ipi_mdp* h, const ipi_comm* comm, const ipi_opts* opts, double* v_local,
+                      int32_t* policy, double* history, int32_t hist_cap, ipi_stats* stats,
+                      void* stream);
+
 /* Solve (I - gamma P_pi) x = b from x (in/out) to the floored 2-norm target
  * or max_it iterations, one persistent cooperative kernel per call.
  * inv_diag == NULL: pc = identity; else left Jacobi preconditioning.

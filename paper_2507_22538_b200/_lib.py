@@ -81,6 +81,16 @@ class CsrReport(C.Structure):
                 ("bad_col_range", _i64), ("bad_col_order", _i64), ("nonfinite_values", _i64)]
 
 
+ALLGATHER_BLOCKS_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
+
+
+class Comm(C.Structure):
+    """ipi_comm (include/ipi_b200.h)."""
+    _fields_ = [("ctx", _p), ("rank", _i32), ("world", _i32),
+                ("allgather_blocks", ALLGATHER_BLOCKS_FN), ("allgather", ALLGATHER_FN)]
+
+
 # name -> (restype, argtypes)
 _SIGS = {
     "ipi_last_error": (C.c_char_p, []),
@@ -114,6 +124,11 @@ _SIGS = {
     "ipi_inner_solve": (C.c_int, [_p, _p, _p, _i64, _f64, _p, _p, _f64, _i32, _i32, _f64, _p,
                                   _i32, C.POINTER(InnerReport), _p]),
     "ipi_k4_trace": (C.c_int, [_i32, _p, _i32]),
+    "ipi_memcpy_sync": (C.c_int, [_p, _p, _i64, _p]),
+    "ipi_comm_nccl": (C.c_int, [_p, _i32, _i32, _p, C.POINTER(Comm)]),
+    "ipi_comm_nccl_destroy": (None, [C.POINTER(Comm)]),
+    "ipi_solve_sharded": (C.c_int, [_p, C.POINTER(Comm), C.POINTER(Opts), _p, _p, _p, _i32,
+                                    C.POINTER(Stats), _p]),
     "ipi_k4_ring_apply_test": (C.c_int, [_p, _p, _i64, _f64, _p, _p, _i32, C.POINTER(C.c_float), _p]),
     "ipi_solve": (C.c_int, [_p, C.POINTER(Opts), _p, _p, _p, _i32, C.POINTER(Stats), _p]),
     "ipi_gen_locality": (C.c_int, [_i64, _i32, _i32, _i64, C.c_uint64, _i64, _i64, _p, _p, _p,

@@ -224,7 +224,7 @@ __global__ void cost_finite_kernel(const double* cost, int64_t len, VAcc* acc) {
 }
 
 
-static int ensure_scratch(ipi_mdp* h) {
+int ensure_scratch(ipi_mdp* h) {
   if (h->pi) return IPI_OK;
   const int64_t n = std::max<int64_t>(h->n_local, 1);
   IPI_CUDA_TRY(cudaMalloc(&h->pi, sizeof(int32_t) * n));
@@ -840,6 +840,15 @@ int ipi_inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* v
 int ipi_k4_ring_apply_test(const int32_t* col, const double* val, int64_t n, double gamma,
                            const double* x, double* y, int32_t reps, float* ms, void* stream) {
   return ring_apply_test(col, val, n, gamma, x, y, reps, ms, (cudaStream_t)stream);
+}
+
+int ipi_memcpy_sync(void* dst, const void* src, int64_t bytes, void* stream) {
+  if (bytes <= 0) return IPI_OK;
+  if (!dst || !src) return fail(IPI_EVALIDATION, "null pointer");
+  cudaStream_t st = (cudaStream_t)stream;
+  IPI_CUDA_TRY(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDefault, st));
+  IPI_CUDA_TRY(cudaStreamSynchronize(st));
+  return IPI_OK;
 }
 
 int ipi_k4_trace(int32_t enable, uint64_t* out, int32_t cap) {

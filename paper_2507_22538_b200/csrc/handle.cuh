@@ -152,7 +152,9 @@ int stepped_gmres(const ipi_op* op, int64_t n, const double* b, double* x, doubl
                   double* ws, int64_t ws_doubles, cudaStream_t st);
 // Jacobi: inv_diag[s] = 1 / (1 - gamma * P_pi[s, s])  (inner.py:115-118)
 int jacobi_inv_diag(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi, int64_t n,
-                    double gamma, double* inv_diag, cudaStream_t st);
+                    double gamma, double* inv_diag, cudaStream_t st, int64_t state0 = 0);
+// capi.cu: the handle's per-solve scratch (policy, P_pi, Krylov arena), allocated once
+int ensure_scratch(ipi_mdp* h);
 // doubles of Krylov workspace inner_solve needs for an n-row system
 inline int64_t krylov_workspace_doubles(int64_t n) {
   return (int64_t)(kGmresRestart + 1) * n + 2 * n + 2 * 32 * 1024 + 64;

@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(256) copy_rows_uniform(const int32_t* __restri
 // absent diagonal -> 0 -> inv_diag = 1 (CsrMatrix.diagonal, sparse.py:102-109)
 __global__ void jacobi_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
                               const double* __restrict__ val, int64_t n, double gamma,
-                              double* __restrict__ invd) {
+                              double* __restrict__ invd, int64_t state0) {
   const int lane = threadIdx.x & 31;
   const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -178,7 +178,7 @@ __global__ void jacobi_kernel(const int64_t* __restrict__ rp, const int32_t* __r
     double d = 0.0;
     int found = 0;
     for (int64_t p = rp[s] + lane; p < rp[s + 1]; p += 32)
-      if (col[p] == (int)s) {
+      if (col[p] == (int)(s + state0)) {  // row s of a row block is state state0 + s
         d = val[p];
         found = 1;
       }
@@ -189,11 +189,11 @@ __global__ void jacobi_kernel(const int64_t* __restrict__ rp, const int32_t* __r
 }
 
 int jacobi_inv_diag(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi, int64_t n,
-                    double gamma, double* inv_diag, cudaStream_t st) {
+                    double gamma, double* inv_diag, cudaStream_t st, int64_t state0) {
   if (n <= 0) return IPI_OK;
   int64_t blocks = (n + 7) / 8;
   if (blocks > 148 * 32) blocks = 148 * 32;
-  jacobi_kernel<<<(int)blocks, 256, 0, st>>>(rp_pi, col_pi, val_pi, n, gamma, inv_diag);
+  jacobi_kernel<<<(int)blocks, 256, 0, st>>>(rp_pi, col_pi, val_pi, n, gamma, inv_diag, state0);
   IPI_LAUNCH_CHECK();
   return IPI_OK;
 }

@@ -13,6 +13,7 @@
 // Reductions are deterministic: fixed grid, per-thread grid-stride sums,
 // fixed block trees, and the last block to finish (ticket) adds the block
 // partials in block order.  Same separate mul/add roundings as numpy.
+#include <map>
 #include <mutex>
 
 #include "handle.cuh"
@@ -27,15 +28,17 @@ struct ShardScratch {
   int blocks = 0;
 };
 
+// One scratch (block partials + last-block ticket) per (device, stream): the
+// ticket protocol is only safe for launches that run one after another, which
+// stream order guarantees; two streams get two scratches.
 static std::mutex g_shard_mu;
-static ShardScratch g_shard[64];
+static std::map<std::pair<int, cudaStream_t>, ShardScratch> g_shard;
 
-static int shard_scratch(ShardScratch** out) {
+static int shard_scratch(cudaStream_t st, ShardScratch** out) {
   int dev = 0;
   IPI_CUDA_TRY(cudaGetDevice(&dev));
-  if (dev < 0 || dev >= 64) return fail(IPI_ECUDA, "device index out of range");
   std::lock_guard<std::mutex> lk(g_shard_mu);
-  ShardScratch& s = g_shard[dev];
+  ShardScratch& s = g_shard[{dev, st}];
   if (!s.blk) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -113,7 +116,7 @@ int ipi_dot_partial(const double* a, const double* b, int64_t n, double* out, vo
   if (!out || (n > 0 && (!a || !b))) return fail(IPI_EVALIDATION, "null argument");
   if (n < 0) return fail(IPI_EDIMENSION, "negative length");
   ShardScratch* s = nullptr;
-  int rc = shard_scratch(&s);
+  int rc = shard_scratch((cudaStream_t)stream, &s);
   if (rc) return rc;
   dot_partial_kernel<<<s->blocks, kShardThreads, 0, (cudaStream_t)stream>>>(a, b, n, s->blk,
                                                                             s->ticket, out);
@@ -128,7 +131,7 @@ int ipi_mgs_pass(const double* partials, int32_t R, double* h_out, double* w, co
   if (R < 1) return fail(IPI_EVALIDATION, "rank count must be >= 1");
   if (n < 0) return fail(IPI_EDIMENSION, "negative length");
   ShardScratch* s = nullptr;
-  int rc = shard_scratch(&s);
+  int rc = shard_scratch((cudaStream_t)stream, &s);
   if (rc) return rc;
   mgs_pass_kernel<<<s->blocks, kShardThreads, 0, (cudaStream_t)stream>>>(
       partials, R, h_out, w, v, v_next, n, s->blk, s->ticket, out_partial);

@@ -24,8 +24,9 @@ from . import _lib
 from .model import Mode, Partition, make_partition
 from .sparse import CsrMatrix, DeviceOperator
 
-__all__ = ["MdpShard", "RankContext", "ShardOps", "allgather_blocks", "host_gmres",
-           "host_richardson", "rank_max", "rank_ordered_sum", "solve_sharded"]
+__all__ = ["MdpShard", "NativeComm", "RankContext", "ShardOps", "allgather_blocks", "host_gmres",
+           "host_richardson", "rank_max", "rank_ordered_sum", "solve_sharded",
+           "solve_sharded_native"]
 
 
 @dataclass
@@ -617,8 +618,19 @@ def solve_sharded(ops, opts, n_global: int, v0_local=None, ortho: str | None = N
     import time
     from .driver import STALL_WINDOW, SolveResult, SolveStatus
     from .inner import InnerSolver
+    from .inner import Preconditioner
     if opts.inner not in (InnerSolver.GMRES, InnerSolver.RICHARDSON):
         raise NotImplementedError("the sharded path runs GMRES and Richardson inner solves")
+    if opts.pc is not Preconditioner.NONE:
+        raise NotImplementedError("the host-driven sharded driver has no preconditioner; "
+                                  "use solve_sharded_native (jacobi)")
+    shard = getattr(ops, "shard", None)
+    if opts.mode is not None and shard is not None and opts.mode is not shard.mode:
+        raise NotImplementedError("the host-driven sharded driver runs the shard's own mode; "
+                                  "use solve_sharded_native for a mode override")
+    if v0_local is None and opts.v0 is not None:
+        lo, hi = ops.ctx.block
+        v0_local = torch.as_tensor(opts.v0, dtype=torch.float64)[lo:hi].to(ops.full.device)
     if ortho is None:
         ortho = os.environ.get("IPI_SHARD_ORTHO", "cgs2" if ops.ctx.world > 1 else "mgs")
     if ortho not in ("mgs", "cgs2"):
@@ -670,3 +682,155 @@ def solve_sharded(ops, opts, n_global: int, v0_local=None, ortho: str | None = N
                        outer_iterations=k, inner_iterations_total=inner_total,
                        residual_history=history, status=status,
                        wall_time=time.perf_counter() - t0)
+
+
+# ----------------------------------------------------------------------------
+# Native sharded iPI (ipi_solve_sharded): the production N > 1 path
+# ----------------------------------------------------------------------------
+
+class NativeComm:
+    """The ``ipi_comm`` this rank hands to ``ipi_solve_sharded``.
+
+    With NCCL (one process per GPU, NVLink / NVSwitch) it wraps torch's own
+    communicator (``ProcessGroupNCCL._comm_ptr``): the collectives run as NCCL
+    kernels on the solver's stream, nothing is staged through the host.  With
+    gloo (CPU-side tests, several ranks sharing one GPU) the two callbacks copy
+    the device buffers to the host, run the gloo collective and copy back — a
+    functional stand-in, not a measurement.  World 1 needs no collectives."""
+
+    def __init__(self, ctx: RankContext):
+        import numpy as np
+        import torch.distributed as dist
+        self.ctx = ctx
+        self.c = _lib.Comm()
+        R = ctx.world
+        starts = np.asarray(list(ctx.partition.block_starts), dtype=np.int64)
+        self._starts = starts
+        L = _lib.lib()
+        self.kind = "local"
+        if R > 1 and dist.get_backend() == "nccl":
+            # the communicator exists once a collective ran (eager init otherwise)
+            dist.barrier()
+            pg = dist.distributed_c10d._get_default_group()
+            comm_ptr = pg._get_backend(torch.device("cuda"))._comm_ptr()
+            _lib.check(L.ipi_comm_nccl(comm_ptr, ctx.rank, R, starts.ctypes.data,
+                                       _lib.C.byref(self.c)), "ipi_comm_nccl")
+            self.kind = "nccl"
+        elif R > 1:
+            self._cb_blocks = _lib.ALLGATHER_BLOCKS_FN(self._gloo_blocks)
+            self._cb_gather = _lib.ALLGATHER_FN(self._gloo_gather)
+            self.c.ctx = None
+            self.c.rank, self.c.world = ctx.rank, R
+            self.c.allgather_blocks = self._cb_blocks
+            self.c.allgather = self._cb_gather
+            self.kind = "gloo"
+        else:
+            _lib.check(L.ipi_comm_nccl(None, 0, 1, starts.ctypes.data, _lib.C.byref(self.c)),
+                       "ipi_comm_nccl")
+
+    # host-staged gloo collectives (callbacks from the native driver)
+    def _gloo_blocks(self, _ctx, local_p, full_p, stream):
+        import numpy as np
+        import torch.distributed as dist
+        try:
+            L = _lib.lib()
+            starts = self._starts
+            lo, hi = int(starts[self.ctx.rank]), int(starts[self.ctx.rank + 1])
+            loc = np.empty(hi - lo, dtype=np.float64)
+            if hi > lo:
+                _lib.check(L.ipi_memcpy_sync(loc.ctypes.data, local_p, 8 * (hi - lo), stream))
+            sizes = [int(starts[q + 1] - starts[q]) for q in range(self.ctx.world)]
+            mx = max(sizes)
+            pad = torch.zeros(mx, dtype=torch.float64)
+            pad[: hi - lo] = torch.from_numpy(loc)
+            bufs = [torch.empty(mx, dtype=torch.float64) for _ in sizes]
+            dist.all_gather(bufs, pad)
+            full = np.concatenate([bufs[q][: sizes[q]].numpy() for q in range(len(sizes))])
+            _lib.check(L.ipi_memcpy_sync(full_p, full.ctypes.data, 8 * full.size, stream))
+            return 0
+        except Exception:  # pragma: no cover - surfaced as the driver's error code
+            import traceback
+            traceback.print_exc()
+            return 3
+
+    def _gloo_gather(self, _ctx, send_p, out_p, count, stream):
+        import numpy as np
+        import torch.distributed as dist
+        try:
+            L = _lib.lib()
+            snd = np.empty(count, dtype=np.float64)
+            _lib.check(L.ipi_memcpy_sync(snd.ctypes.data, send_p, 8 * count, stream))
+            bufs = [torch.empty(count, dtype=torch.float64) for _ in range(self.ctx.world)]
+            dist.all_gather(bufs, torch.from_numpy(snd))
+            out = torch.cat(bufs).numpy()
+            _lib.check(L.ipi_memcpy_sync(out_p, out.ctypes.data, 8 * out.size, stream))
+            return 0
+        except Exception:  # pragma: no cover
+            import traceback
+            traceback.print_exc()
+            return 3
+
+    def __del__(self):
+        if getattr(self, "kind", None) in ("nccl", "local"):
+            try:
+                _lib.lib().ipi_comm_nccl_destroy(_lib.C.byref(self.c))
+            except Exception:
+                pass
+
+
+def solve_sharded_native(shard: "MdpShard", ctx: RankContext, opts, v0_local=None,
+                         comm: NativeComm | None = None):
+    """driver.py:109-209 across ranks through ``ipi_solve_sharded``: K1 on the
+    shard with the all-gathered V, K2 on the local rows, the sharded GMRES
+    (CGS2, 3 all-gathers of partial dots per Arnoldi step) or Richardson with
+    every scalar on the device, one host sync per Arnoldi step and per outer
+    iteration.  Honours ``opts.mode`` (overrides the shard's), ``opts.pc``
+    (none / jacobi), ``opts.v0`` / ``v0_local`` (this rank's block).
+    BiCGStab / TFQMR and the SOR / EXACT preconditioners raise
+    NotImplementedError.  Returns a SolveResult whose values / policy are the
+    gathered full vectors (identical on every rank)."""
+    import numpy as np
+    from .driver import SolveResult, SolveStatus
+    from .inner import InnerSolver, Preconditioner
+    opts.check()
+    if opts.inner not in (InnerSolver.GMRES, InnerSolver.RICHARDSON):
+        raise NotImplementedError(f"inner solver {opts.inner.value!r} runs on one GPU only; the "
+                                  "sharded driver runs GMRES and Richardson")
+    if opts.pc not in (Preconditioner.NONE, Preconditioner.JACOBI):
+        raise NotImplementedError(f"preconditioner {opts.pc.value!r} is not on the device path")
+    dev = shard.stage_cost.device
+    lo, hi = ctx.block
+    if v0_local is None and opts.v0 is not None:
+        v0 = opts.v0
+        v0_full = v0 if isinstance(v0, torch.Tensor) else torch.as_tensor(np.asarray(v0, np.float64))
+        if tuple(v0_full.shape) != (shard.n_global,):
+            from .model import ValidationError
+            raise ValidationError(f"v0 length {tuple(v0_full.shape)} does not match n = {shard.n_global}")
+        v0_local = v0_full[lo:hi]
+    v = (torch.zeros(hi - lo, dtype=torch.float64, device=dev) if v0_local is None
+         else v0_local.detach().to(dev, torch.float64).clone().contiguous())
+    pol = torch.empty(hi - lo, dtype=torch.int32, device=dev)
+    mode = opts.mode or shard.mode
+    o = _lib.Opts(tol=opts.tol, alpha=opts.alpha, max_outer=opts.max_outer,
+                  max_inner=opts.max_inner, ksp_type=_lib.KSP[opts.inner.value],
+                  ksp_max_it=opts.ksp_max_it or 0, richardson_scale=opts.richardson_scale,
+                  mode=_lib.MODE_MAX if mode is Mode.MAX else _lib.MODE_MIN,
+                  pc_type=_lib.PC[opts.pc.value], gmres_ortho=_lib.ORTHO["cgs2"])
+    comm = comm or NativeComm(ctx)
+    hist = np.zeros(opts.max_outer + 2, dtype=np.float64)
+    st = _lib.Stats()
+    _lib.check(_lib.lib().ipi_solve_sharded(shard.handle(), _lib.C.byref(comm.c), _lib.C.byref(o),
+                                            _lib.ptr(v), _lib.ptr(pol), hist.ctypes.data,
+                                            hist.shape[0], _lib.C.byref(st), _lib.stream_ptr()),
+               "ipi_solve_sharded")
+    full = torch.empty(shard.n_global, dtype=torch.float64, device=dev)
+    values = allgather_blocks(v, full, ctx.partition).clone()
+    pol_full = allgather_blocks(pol.to(torch.float64), torch.empty_like(full), ctx.partition)
+    nh = st.outer_iterations + 1
+    return SolveResult(values=values.cpu().numpy(), policy=pol_full.cpu().numpy().astype(np.int64),
+                       outer_iterations=st.outer_iterations,
+                       inner_iterations_total=int(st.inner_iterations_total),
+                       residual_history=[float(x) for x in hist[:nh]],
+                       status=SolveStatus(_lib.STATUS[st.status]), wall_time=st.wall_time,
+                       time_greedy=st.time_greedy, time_assembly=st.time_assembly,
+                       time_inner=st.time_inner, values_device=values)
