@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--scale", type=int, default=1, help="divide n by this (debug only)")
     ap.add_argument("--no-ipi", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5 block at N >= 2")
     return ap.parse_args()
 
 
@@ -299,6 +300,92 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def sharded_ipi(solve_fn, shard, ctx, opts, dev, dist):
+    """Time-to-tolerance of the native sharded driver, max over ranks."""
+    import torch
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    res = solve_fn(shard, ctx, opts)
+    torch.cuda.synchronize()
+    tt = torch.tensor([time.perf_counter() - t0, res.wall_time, res.time_greedy,
+                       res.time_assembly, res.time_inner], device=dev, dtype=torch.float64)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    return {"time_to_tol_s": float(tt[1]), "time_incl_gather_s": float(tt[0]),
+            "time_greedy_s": float(tt[2]), "time_assembly_s": float(tt[3]),
+            "time_inner_s": float(tt[4]), "status": res.status.value,
+            "outer": res.outer_iterations, "inner": res.inner_iterations_total,
+            "final_residual": res.residual_history[-1], "residual_history": res.residual_history,
+            "driver": "ipi_solve_sharded (native; CGS2 GMRES, %s collectives)" % dist.get_backend()}
+
+
+def run_c5(args, ipi, dev, dist, world, local):
+    """BASELINE configs[4] (C5, the sharded-only config: n = 2^24, 16 actions,
+    64 nnz per row, +-65536 window, 206 GB) at N >= 2: one step = the V
+    all-gather + K1 over this rank's rows, timed like the headline (events,
+    max over ranks), and the sharded solve's time-to-tolerance.  Reported as
+    extra keys; the headline line stays C2 (the metric's config)."""
+    import statistics as stats_
+    import torch
+    from paper_2507_22538_b200 import devgen
+    from paper_2507_22538_b200.generators import CONFIGS
+    from paper_2507_22538_b200.parallel import (MdpShard, RankContext, allgather_blocks,
+                                                solve_sharded_native)
+    spec = CONFIGS[5]
+    n = spec.n // args.scale
+    ctx = RankContext.from_env(n)
+    lo, hi = ctx.block
+    t_gen = time.perf_counter()
+    rp, col, val, cost = devgen.locality(n, spec.m, spec.K, spec.window, args.seed, lo, hi - lo)
+    shard = MdpShard(n, spec.m, spec.gamma, lo, cost,
+                     ipi.CsrMatrix((hi - lo) * spec.m, n, rp, col, val))
+    torch.cuda.synchronize()
+    t_gen = time.perf_counter() - t_gen
+    plan = shard.plan()
+    rng = torch.Generator(device="cpu").manual_seed(1)
+    v_full = torch.rand(n, generator=rng, dtype=torch.float64).to(dev)
+    v_local = v_full[lo:hi].clone()
+    st = torch.cuda.current_stream()
+    for _ in range(max(args.warmup, 3)):
+        allgather_blocks(v_local, v_full, ctx.partition)
+        shard.bellman(v_full)
+    torch.cuda.synchronize()
+    dist.barrier()
+    steps = max(3, min(args.steps, 10))
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(steps)]
+    t_begin, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_begin.record(st)
+    for i in range(steps):
+        allgather_blocks(v_local, v_full, ctx.partition)
+        ev[i][0].record(st)
+        shard.bellman(v_full)
+        ev[i][1].record(st)
+    t_end.record(st)
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms = torch.tensor([t_begin.elapsed_time(t_end) / steps,
+                       stats_.mean(a.elapsed_time(b) for a, b in ev)], device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms_step, ms_k1 = float(ms[0]), float(ms[1])
+    alg = k1_bytes(hi - lo, spec.m, plan["nnz"], bool(plan["uniform_rows"]), n_v=n)
+    peak, _ = peaks()
+    out = {"workload": spec.name, "n_states": n, "n_actions": spec.m, "nnz_per_row": spec.K,
+           "window": spec.window, "nnz": n * spec.m * spec.K, "scale": args.scale,
+           "value": n * spec.m / (ms_step * 1e-3), "unit": "(s,a)-backups/s",
+           "ms_per_step": ms_step, "steps": steps,
+           "per_gpu_value": n * spec.m / world / (ms_step * 1e-3),
+           "roofline_k1_rank": {"bound": "hbm", "k1_ms": ms_k1, "algorithmic_bytes_per_launch": alg,
+                                "achieved": alg / (ms_k1 * 1e-3) / 1e9, "peak": peak,
+                                "frac": alg / (ms_k1 * 1e-3) / 1e9 / peak, "unit": "GB/s"},
+           "plan": plan, "gen_seconds": t_gen,
+           "step": "V all-gather + fused Bellman backup over this rank's rows (max over ranks)"}
+    if not args.no_ipi:
+        opts = ipi.SolveOptions(alpha=spec.alpha, tol=spec.atol)
+        out["ipi"] = sharded_ipi(solve_sharded_native, shard, ctx, opts, dev, dist)
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -444,20 +531,14 @@ def run_ours(args):
 
     ipi_sharded = None
     if world > 1 and not args.no_ipi:
-        from paper_2507_22538_b200.parallel import ShardOps, solve_sharded
-        ops = ShardOps(shard, ctx)
+        from paper_2507_22538_b200.parallel import solve_sharded_native
         opts = ipi.SolveOptions(alpha=spec.alpha, tol=spec.atol)
-        torch.cuda.synchronize()
-        dist.barrier()
-        t0 = time.perf_counter()
-        res_sh = solve_sharded(ops, opts, n)
-        torch.cuda.synchronize()
-        tt = torch.tensor([time.perf_counter() - t0], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ipi_sharded = {"time_to_tol_s": float(tt[0]), "status": res_sh.status.value,
-                       "outer": res_sh.outer_iterations, "inner": res_sh.inner_iterations_total,
-                       "final_residual": res_sh.residual_history[-1],
-                       "driver": "parallel.solve_sharded (host-driven phases, %s)" % dist.get_backend()}
+        ipi_sharded = sharded_ipi(solve_sharded_native, shard, ctx, opts, dev, dist)
+    c5 = None
+    if world > 1 and not args.no_c5:
+        del shard
+        torch.cuda.empty_cache()
+        c5 = run_c5(args, ipi, dev, dist, world, local)
     out = None
     if rank == 0:
         cpu = None
@@ -526,6 +607,8 @@ def run_ours(args):
             "ipi": ipi_rep if ipi_rep is not None else ipi_sharded,
             "gen_seconds": t_gen,
         }
+        if c5 is not None:
+            out["c5"] = c5
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
