@@ -178,3 +178,60 @@ def test_unsupported_kinds_raise():
             solve_sharded_native(shard, ctx, ipi.SolveOptions(inner=ipi.InnerSolver.from_name(kind)))
     with pytest.raises(NotImplementedError):
         solve_sharded_native(shard, ctx, ipi.SolveOptions(pc=ipi.Preconditioner.SOR_FORWARD))
+
+
+def _cb_trans(s, a):
+    rng = np.random.default_rng(1000 * s + a)
+    k = 1 + (s * 7 + a) % 9
+    cols = rng.choice(300, size=k, replace=False)
+    p = rng.random(k) + 0.1
+    return cols.tolist(), (p / p.sum()).tolist()
+
+
+def _cb_cost(s, a):
+    return ((s * 13 + a * 7) % 17) / 17.0
+
+
+def _callback_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2507_22538_b200.frontend import build_shard_from_callbacks
+        from paper_2507_22538_b200.parallel import RankContext, solve_sharded_native
+        ctx = RankContext.from_env(300)
+        shard = build_shard_from_callbacks(300, 3, 0.95, _cb_cost, _cb_trans, ctx)
+        res = solve_sharded_native(shard, ctx, ipi.SolveOptions(max_outer=300))
+        q.put((rank, res.status.value, res.outer_iterations, res.values.tolist(),
+               res.policy.tolist(), res.residual_history, res.inner_iterations_total))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_per_rank_callback_construction_solves_like_one_process():
+    """build_shard_from_callbacks at world 2 (each rank evaluates only its
+    block, problems.py:419-488) -> the native sharded solve reproduces the
+    one-process solve of createTransitionProbabilityTensor's instance."""
+    import paper_2507_22538_b200.frontend as mf
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_callback_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted((q.get(timeout=600) for _ in procs), key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert out[0][1:] == out[1][1:]
+    P = mf.createTransitionProbabilityTensor(300, 3, _cb_trans)
+    cost = mf.createStageCostMatrix(300, 3, _cb_cost)
+    mdp = ipi.MdpInstance(n=300, m=3, gamma=0.95, stage_cost=cost.data, transitions=P.data)
+    ref = ipi.solve(mdp, ipi.SolveOptions(max_outer=300))
+    _, status, outer, values, policy, _, _ = out[0]
+    assert status == ref.status.value and outer == ref.outer_iterations
+    np.testing.assert_allclose(values, ref.values, rtol=1e-8, atol=1e-8)
+    np.testing.assert_array_equal(policy, ref.policy)

@@ -489,3 +489,77 @@ def test_halo_exchange_gloo_world3():
     assert all(enabled and ok for _, enabled, ok, _ in out), out
     # the middle rank receives both halos (7 + 11 entries), the outer ranks one each
     assert [b // 8 for *_, b in out] == [11, 18, 7]
+
+
+# ----------------------------------------------------------------------------
+# per-rank callback construction (problems.py:419-488 with workers = ranks):
+# each rank evaluates only its partition block; the blocks concatenate to the
+# one-process build bit for bit
+# ----------------------------------------------------------------------------
+
+def _cb_trans(s, a):
+    rng = np.random.default_rng(1000 * s + a)
+    k = 1 + (s * 7 + a) % 9                       # ragged rows, 1..9 successors
+    cols = rng.choice(53, size=k, replace=False)
+    p = rng.random(k) + 0.1
+    return cols.tolist(), (p / p.sum()).tolist()
+
+
+def _cb_cost(s, a):
+    return 0.5 * s - 0.25 * a
+
+
+def _callback_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2507_22538_b200.frontend import callback_block
+        from paper_2507_22538_b200.parallel import RankContext
+        ctx = RankContext.from_env(53)
+        lo, hi = ctx.block
+        rp, cols, vals, cost = callback_block(53, 3, lo, hi, _cb_trans, _cb_cost)
+        got = [None] * world
+        dist.all_gather_object(got, (rank, lo, hi, rp.tolist(), cols.tolist(), vals.tolist(),
+                                     cost.tolist()))
+        q.put(got)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_callback_construction_per_rank_gloo_world2():
+    import torch.multiprocessing as mp
+    from paper_2507_22538_b200.frontend import callback_block
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_callback_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    rp, cols, vals, cost = callback_block(53, 3, 0, 53, _cb_trans, _cb_cost)
+    blocks = sorted(outs[0])
+    assert blocks == sorted(outs[1])  # every rank saw the same gathered blocks
+    # concatenating the ranks' blocks reproduces the sequential build exactly
+    assert [b[1] for b in blocks] == [0, 27] and blocks[-1][2] == 53
+    off = 0
+    rp_cat = [0]
+    for _, lo, hi, brp, bcols, bvals, bcost in blocks:
+        rp_cat += [off + x for x in brp[1:]]
+        off += brp[-1]
+    np.testing.assert_array_equal(rp_cat, rp)
+    np.testing.assert_array_equal(np.concatenate([b[4] for b in blocks]), cols)
+    assert np.concatenate([b[5] for b in blocks]).tobytes() == vals.tobytes()
+    assert np.concatenate([b[6] for b in blocks]).tobytes() == cost.tobytes()
+
+
+def test_callback_block_errors_name_the_pair():
+    from paper_2507_22538_b200.frontend import callback_block
+    with pytest.raises(ipi.ValidationError, match=r"trans_fn\(s=4, a=1\).*pre-allocation"):
+        callback_block(10, 2, 3, 6, lambda s, a: (([0, 1, 2], [0.2, 0.3, 0.5]) if (s, a) == (4, 1)
+                                                  else ([0], [1.0])), prealloc=2)
+    with pytest.raises(ipi.ValidationError, match="sum to"):
+        callback_block(10, 2, 0, 1, lambda s, a: ([0, 1], [0.2, 0.3]))
