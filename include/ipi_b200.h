@@ -133,6 +133,8 @@ typedef struct {
                               5 flat rows (registers), 6 uniform rows (cp.async ring) */
   int32_t k1_stages;       /* shared-memory ring stages (variants 2, 4, 6) */
   int32_t k1_tma_chunk_states; /* states per TMA stage (variant 2) */
+  int32_t contiguous_rows; /* every row's columns are consecutive (banded rows, C4): the
+                              generic kernels read one column per row */
 } ipi_plan;
 
 /* Plan of a policy operator (ipi_op_create): exposed for reports/tests. */

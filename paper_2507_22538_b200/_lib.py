@@ -54,7 +54,7 @@ class Plan(C.Structure):
                 ("k1_blocks", _i32), ("k1_threads", _i32), ("k1_smem_bytes", _i32),
                 ("inner_blocks", _i32), ("inner_threads", _i32), ("inner_smem_bytes", _i32),
                 ("uniform_rows", _i32), ("k1_variant", _i32), ("k1_stages", _i32),
-                ("k1_tma_chunk_states", _i32)]
+                ("k1_tma_chunk_states", _i32), ("contiguous_rows", _i32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "pad"}
@@ -148,7 +148,7 @@ def load(path: Path | str | None = None) -> C.CDLL:
         if _lib is not None:
             return _lib
         # IPI_LIB: an alternative build of the same ABI (A/B experiments only)
-        p = Path(path) if path else Path(os.environ.get("IPI_LIB", LIB_PATH))
+        p = Path(path) if path else Path(os.environ.get("IPI_LIB") or LIB_PATH)
         if not p.exists():
             raise RuntimeError(
                 f"{p.name} is not built ({p}); run `python -m paper_2507_22538_b200._build` "

@@ -47,7 +47,7 @@ struct K1Args {
   int32_t interleave;  // uniform ring: warps take interleaved states
   int32_t rotate;      // uniform ring: per-CTA rotated start in the warp's state sequence
   unsigned long long* trace;  // diagnostics: per-CTA (smid, t_start, t_end) or nullptr
-  int32_t gen_u;              // generic rows, G = 32: loads in flight per lane (4, 8, 16)
+  int32_t contig;             // generic rows: columns consecutive within each row (plan)
 };
 
 __device__ __forceinline__ unsigned long long global_ns() {
@@ -61,7 +61,10 @@ __device__ __forceinline__ unsigned sm_id() {
   return r;
 }
 
-template <int G, bool WIN, int UL = (G == 32 ? 8 : 4)>
+// CONTIG: every row's columns are consecutive (plan.contiguous_rows, C4's
+// banded rows): entry q's column is c0 + (q - p0), so the column stream is not
+// read (8 instead of 12 bytes per entry).
+template <int G, bool WIN, bool CONTIG = false, int UL = (G == 32 ? 8 : 4)>
 __global__ void __launch_bounds__(kK1Threads) k1_bellman(K1Args a) {
   extern __shared__ double win[];
   __shared__ double red[32];
@@ -101,6 +104,8 @@ __global__ void __launch_bounds__(kK1Threads) k1_bellman(K1Args a) {
       double acc = 0.0;
       if (act < m) {
         const int64_t p0 = __ldg(a.rp + row0 + act), p1 = __ldg(a.rp + row0 + act + 1);
+        int c0 = 0;
+        if constexpr (CONTIG) c0 = p1 > p0 ? __ldg(a.col + p0) : 0;
         // long rows (G = 32, e.g. C4's ~570-entry rows): 8 loads in flight per lane
         constexpr int U = UL;
         for (int64_t p = p0 + gl; p < p1; p += U * G) {
@@ -111,7 +116,8 @@ __global__ void __launch_bounds__(kK1Threads) k1_bellman(K1Args a) {
             const int64_t q = p + (int64_t)u * G;
             if (q < p1) {
               vv[u] = ld_stream(a.val + q, pol);
-              cc[u] = ld_stream(a.col + q, pol);
+              if constexpr (CONTIG) cc[u] = c0 + (int)(q - p0);
+              else cc[u] = ld_stream(a.col + q, pol);
             } else {
               vv[u] = 0.0;
               cc[u] = -1;
@@ -1208,14 +1214,9 @@ static cudaError_t uniform_smem(int G, int P, int smem) {
 
 template <int G>
 static void launch_g(const K1Args& a, bool win, int blocks, int smem, cudaStream_t st) {
-  if (G == 32 && a.gen_u == 4) {  // long rows, 4 loads per lane (A/B: IPI_K1_GEN_U)
-    if (win) k1_bellman<G, true, 4><<<blocks, kK1Threads, smem, st>>>(a);
-    else k1_bellman<G, false, 4><<<blocks, kK1Threads, 0, st>>>(a);
-    return;
-  }
-  if (G == 32 && a.gen_u == 16) {
-    if (win) k1_bellman<G, true, 16><<<blocks, kK1Threads, smem, st>>>(a);
-    else k1_bellman<G, false, 16><<<blocks, kK1Threads, 0, st>>>(a);
+  if (G == 32 && a.contig) {  // banded rows (C4)
+    if (win) k1_bellman<G, true, true><<<blocks, kK1Threads, smem, st>>>(a);
+    else k1_bellman<G, false, true><<<blocks, kK1Threads, 0, st>>>(a);
     return;
   }
   if (win)
@@ -1227,8 +1228,7 @@ static void launch_g(const K1Args& a, bool win, int blocks, int smem, cudaStream
 template <int G>
 static cudaError_t set_smem_attr(int smem) {
   cudaError_t e = raise_smem_limit(k1_bellman<G, true>, smem);
-  if (G == 32 && e == cudaSuccess) e = raise_smem_limit(k1_bellman<G, true, 4>, smem);
-  if (G == 32 && e == cudaSuccess) e = raise_smem_limit(k1_bellman<G, true, 16>, smem);
+  if (G == 32 && e == cudaSuccess) e = raise_smem_limit(k1_bellman<G, true, true>, smem);
   return e;
 }
 
@@ -1309,7 +1309,7 @@ int launch_bellman(ipi_mdp* h, const double* v_full, int32_t mode, int32_t* poli
   a.interleave = h->k1_interleave;
   a.rotate = h->k1_rotate;
   a.trace = h->k1_trace;
-  a.gen_u = h->k1_gen_u;
+  a.contig = h->plan.contiguous_rows;
   const bool win = h->plan.halo >= 0;
   const int blocks = h->plan.k1_blocks, smem = h->plan.k1_smem_bytes;
   int G = 0, P = 0;

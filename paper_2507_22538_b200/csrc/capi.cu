@@ -290,7 +290,6 @@ int ipi_mdp_create(const int64_t* row_ptr, const int32_t* col, const double* val
   if (getenv("IPI_K1_WIN_ASYNC")) h->k1_win_async = atoi(getenv("IPI_K1_WIN_ASYNC")) != 0;
   if (getenv("IPI_K1_INTERLEAVE")) h->k1_interleave = atoi(getenv("IPI_K1_INTERLEAVE")) != 0;
   if (getenv("IPI_K1_ROTATE")) h->k1_rotate = atoi(getenv("IPI_K1_ROTATE")) != 0;
-  if (getenv("IPI_K1_GEN_U")) h->k1_gen_u = atoi(getenv("IPI_K1_GEN_U"));
   if (cudaMallocHost(&h->host_pinned, 4096) != cudaSuccess)
     return bail(fail(IPI_ECUDA, "cudaMallocHost failed"));
   const int rc = plan_instance(h, st);
@@ -826,7 +825,7 @@ int ipi_inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* v
   rc = inner_solve(rp_pi, col_pi, val_pi, n, gamma, b, x, target_2norm, max_it, kind,
                    richardson_scale, pl.lanes_per_row, pl.halo,
                    pl.uniform_rows ? pl.row_len_max : 0, d_rep, st, nullptr, 0, inv_diag,
-                   12.0 * (double)nnz + 8.0 * (double)(n + 1), ortho, op);
+                   12.0 * (double)nnz + 8.0 * (double)(n + 1), ortho, op, pl.contiguous_rows);
   ipi_op_destroy(op);
   if (rc == IPI_OK && report) {
     cudaError_t e = cudaMemcpyAsync(report, d_rep, sizeof(*report), cudaMemcpyDeviceToHost, st);
@@ -975,7 +974,7 @@ int ipi_solve(ipi_mdp* h, const ipi_opts* o, double* v, int32_t* policy, double*
                      h->plan.uniform_rows ? h->plan.row_len_max : 0, h->d_report, st, h->kry,
                      h->kry_len, o->pc_type == IPI_PC_JACOBI ? h->invd : nullptr,
                      (12.0 * h->plan.row_len_mean + 8.0) * (double)n,  // P_pi size estimate
-                     o->gmres_ortho, h->op_pi);
+                     o->gmres_ortho, h->op_pi, h->plan.contiguous_rows);
     if (rc) return rc;
     if (o->ksp_type == IPI_KSP_TFQMR || o->ksp_type == IPI_KSP_BICGSTAB) {
       // these kinds can break down: read the report now (driver.py:189-193)

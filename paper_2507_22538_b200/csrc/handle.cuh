@@ -46,7 +46,6 @@ struct ipi_mdp {
   int k1_win_async = 1;     // variant 6: cp.async V window (IPI_K1_WIN_ASYNC=0: scalar loop)
   int k1_interleave = 1;    // variant 6: interleaved state order (IPI_K1_INTERLEAVE=0: contiguous)
   int k1_rotate = 1;        // variant 6: rotated per-CTA start (IPI_K1_ROTATE=0: none)
-  int k1_gen_u = 8;        // variant 0: loads in flight per lane (IPI_K1_GEN_U, read at create)
   unsigned long long* k1_trace = nullptr;  // diagnostics (ipi_mdp_k1_trace)
 };
 
@@ -143,7 +142,8 @@ int inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_p
                 int64_t workspace_doubles = 0, const double* inv_diag = nullptr,
                 double pi_bytes = 0.0,   // bytes of P_pi (L2-residency choice; <= 0: read nnz)
                 int ortho = IPI_ORTHO_AUTO,
-                const ipi_op* op = nullptr);  // planned K3 operator of P_pi: stepped GMRES
+                const ipi_op* op = nullptr,   // planned K3 operator of P_pi: stepped GMRES
+                int contig = 0);              // P_pi rows have consecutive columns
 // krylov_step.cu
 bool stepped_gmres_fits(int64_t n, int sms);
 int64_t stepped_gmres_workspace(int64_t n, int blocks);

@@ -98,7 +98,7 @@ int inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_p
                 int32_t kind, double scale, int lanes, int halo, int uniform_K,
                 ipi_inner_report* d_report, cudaStream_t st, double* workspace,
                 int64_t workspace_doubles, const double* inv_diag, double pi_bytes, int ortho,
-                const ipi_op* op) {
+                const ipi_op* op, int contig) {
   if (kind < IPI_KSP_RICHARDSON || kind > IPI_KSP_TFQMR)
     return fail(IPI_EVALIDATION, "unknown inner solver kind " + std::to_string(kind));
   if (max_it < 1) return fail(IPI_EVALIDATION, "iteration cap must be >= 1, got " + std::to_string(max_it));
@@ -136,6 +136,7 @@ int inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_p
   a.partials = a.r + n;
   a.bar = reinterpret_cast<unsigned*>(a.partials + 2 * kPartStride * (int64_t)blocks);
   a.ortho = ortho;
+  a.contig = contig;
   a.trace = g_k4_trace;
   a.trace_cap = g_k4_trace_cap;
   if (a.trace) IPI_CUDA_TRY(cudaMemsetAsync(a.trace, 0, sizeof(unsigned long long), st));
@@ -155,10 +156,13 @@ int inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_p
       cudaStreamSynchronize(st);
       bytes = 12.0 * (double)nnz_h + 8.0 * (double)(n + 1);
     }
+    // contiguous rows stream 8 B per entry (values) instead of 12: C4's 137 MB
+    // P_pi becomes ~92 MB, of which half marked evict-last measured best
+    // (C4 iPI 53.0 ms at 0.5 vs 57.0 at 0 and 58.0 at 1: all of it evicts the
+    // basis and K1's working set); a larger P_pi streams evict-first
+    if (contig) bytes *= 8.0 / 12.0;
     const double budget = 0.6 * (double)l2;
-    // whole P_pi when it fits; a fractional hint helped C4's SpMV (-9%) but not its
-    // MGS-bound GMRES step and slowed C3's (IPI_K4_KEEP=<fraction> to experiment)
-    double f = bytes <= budget ? 1.0 : 0.0;
+    double f = bytes <= budget ? 1.0 : (contig && bytes <= (double)l2 ? 0.5 : 0.0);
     if (keep_env >= 0.0) f = keep_env;
     a.keep_frac = (float)std::min(1.0, std::max(0.0, f));
   }

@@ -61,6 +61,7 @@ struct KArgs {
   int bar_mode;        // GridBarrier::mode (IPI_K4_BARRIER)
   float keep_frac;     // fraction of P_pi accesses marked L2 evict-last (0 = evict-first)
   int xwin;            // stage the SpMV input window (else the window space only holds MGS slices)
+  int contig;          // generic rows: columns consecutive within each row (CONTIG instances)
   int ortho;           // GMRES Arnoldi orthogonalisation (resolved): IPI_ORTHO_MGS / IPI_ORTHO_CGS2
   unsigned long long* trace;  // diagnostics (ipi_k4_trace): phase timestamps or nullptr
   int trace_cap;
@@ -287,7 +288,7 @@ __device__ __forceinline__ double cgs_update(const KArgs& a, int nv, const doubl
 // generic rows (G lanes strided over the row, 4 loads in flight); P > 0:
 // uniform even-length rows, P 16-byte value pairs per lane, batches
 // software-pipelined across row groups (same scheme as K1's fast path).
-template <int G, int P, bool WIN, class Epi>
+template <int G, int P, bool WIN, bool CONTIG, class Epi>
 __device__ __forceinline__ void spmv_rows(const KArgs& a, const double* xin, int64_t s_lo,
                                           int64_t s_hi, double* win, uint64_t pol, Epi&& epi) {
   int64_t w_lo = 0, w_len = 0;
@@ -322,6 +323,8 @@ __device__ __forceinline__ void spmv_rows(const KArgs& a, const double* xin, int
       double acc = 0.0;
       if (s < s_hi) {
         const int64_t p0 = __ldg(a.rp + s), p1 = __ldg(a.rp + s + 1);
+        int c0 = 0;  // CONTIG: consecutive columns, entry q's column is c0 + (q - p0)
+        if constexpr (CONTIG) c0 = p1 > p0 ? __ldg(a.col + p0) : 0;
         for (int64_t p = p0 + gl; p < p1; p += 4 * G) {
           double vv[4];
           int cc[4];
@@ -330,7 +333,8 @@ __device__ __forceinline__ void spmv_rows(const KArgs& a, const double* xin, int
             const int64_t q = p + (int64_t)u * G;
             if (q < p1) {
               vv[u] = ld_stream(a.val + q, pol);
-              cc[u] = ld_stream(a.col + q, pol);
+              if constexpr (CONTIG) cc[u] = c0 + (int)(q - p0);
+              else cc[u] = ld_stream(a.col + q, pol);
             } else {
               vv[u] = 0.0;
               cc[u] = -1;
@@ -395,7 +399,7 @@ __device__ __forceinline__ void spmv_rows(const KArgs& a, const double* xin, int
 // Richardson, 2 = BiCGStab, 3 = TFQMR.  Each
 // solver family is its own instantiation (and translation unit) so the hot
 // GMRES kernel does not carry the register pressure of the others.
-template <int G, int P, bool WIN, int KIND>
+template <int G, int P, bool WIN, int KIND, bool CONTIG = false>
 __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
   GridBarrier gb{a.bar, 0u, a.bar_mode};
   extern __shared__ double win[];
@@ -434,7 +438,7 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
   // ---- r = b - (x - gamma P x), ||b||, ||r|| --------------------------------
   double acc2[2] = {0.0, 0.0};
   for (int64_t i = s_lo + tid; i < s_hi; i += nthr) acc2[0] = add_rn(acc2[0], mul_rn(b[i], b[i]));
-  spmv_rows<G, P, WIN>(a, x, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
+  spmv_rows<G, P, WIN, CONTIG>(a, x, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
     const double ri = sub_rn(b[s], sub_rn(xs, mul_rn(gam, px)));
     r[s] = ri;
     acc2[1] = add_rn(acc2[1], mul_rn(ri, ri));
@@ -448,7 +452,7 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
   auto true_residual = [&]() -> double {
     gb.sync();
     double q[1] = {0.0};
-    spmv_rows<G, P, WIN>(a, x, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
+    spmv_rows<G, P, WIN, CONTIG>(a, x, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
       const double ri = sub_rn(b[s], sub_rn(xs, mul_rn(gam, px)));
       r[s] = ri;
       q[0] = add_rn(q[0], mul_rn(ri, ri));
@@ -494,7 +498,7 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
       }
       gb.sync();
       double p2[2] = {0.0, 0.0};
-      spmv_rows<G, P, WIN>(a, yv, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
+      spmv_rows<G, P, WIN, CONTIG>(a, yv, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
         const double u = pcv(s, sub_rn(xs, mul_rn(gam, px)));
         uv[s] = u;
         vv[s] = u;
@@ -525,7 +529,7 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
           } else {
             for (int64_t i = s_lo + tid; i < s_hi; i += nthr) yv[i] = sub_rn(yv[i], mul_rn(alpha, vv[i]));
             gb.sync();
-            spmv_rows<G, P, WIN>(a, yv, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
+            spmv_rows<G, P, WIN, CONTIG>(a, yv, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
               const double u = pcv(s, sub_rn(xs, mul_rn(gam, px)));
               uv[s] = u;
               const double w = sub_rn(wv[s], mul_rn(alpha, u));
@@ -571,7 +575,7 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
         }
         gb.sync();
         p2[0] = p2[1] = 0.0;
-        spmv_rows<G, P, WIN>(a, yv, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
+        spmv_rows<G, P, WIN, CONTIG>(a, yv, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
           const double u = pcv(s, sub_rn(xs, mul_rn(gam, px)));
           uv[s] = u;
           const double v = add_rn(vt[s], u);
@@ -603,7 +607,7 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
         if (fabs(rho) <= mul_rn(mul_rn(1e-14, rtn), est)) { brk = 1; break; }
         gb.sync();
         double p2[2] = {0.0, 0.0};
-        spmv_rows<G, P, WIN>(a, pv, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
+        spmv_rows<G, P, WIN, CONTIG>(a, pv, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
           const double v = pcv(s, sub_rn(xs, mul_rn(gam, px)));
           vv[s] = v;
           p2[0] = add_rn(p2[0], mul_rn(rt[s], v));
@@ -627,7 +631,7 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
           ++it;
           gb.sync();
           double q[1] = {0.0};
-          spmv_rows<G, P, WIN>(a, x, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
+          spmv_rows<G, P, WIN, CONTIG>(a, x, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
             const double ri = sub_rn(b[s], sub_rn(xs, mul_rn(gam, px)));
             r[s] = ri;
             q[0] = add_rn(q[0], mul_rn(ri, ri));
@@ -650,7 +654,7 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
         }
         gb.sync();
         double p3[2] = {0.0, 0.0};
-        spmv_rows<G, P, WIN>(a, sv, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
+        spmv_rows<G, P, WIN, CONTIG>(a, sv, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
           const double t = pcv(s, sub_rn(xs, mul_rn(gam, px)));
           tv[s] = t;
           p3[0] = add_rn(p3[0], mul_rn(t, t));
@@ -697,7 +701,7 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
       ++it;
       gb.sync();
       double acc1[1] = {0.0};
-      spmv_rows<G, P, WIN>(a, x, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
+      spmv_rows<G, P, WIN, CONTIG>(a, x, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
         const double ri = sub_rn(b[s], sub_rn(xs, mul_rn(gam, px)));
         r[s] = ri;
         acc1[0] = add_rn(acc1[0], mul_rn(ri, ri));
@@ -726,19 +730,24 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
         const double* Vj = a.V + (int64_t)j * n;
         const double* V0 = a.V;
         double p[1] = {0.0};
-        spmv_rows<G, P, WIN>(a, Vj, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
+        if constexpr (KIND == kKindGmresCgs) k4_mark(a);
+        spmv_rows<G, P, WIN, CONTIG>(a, Vj, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
           wl[s - s_lo] = pcv(s, sub_rn(xs, mul_rn(gam, px)));
         });
         ++it;
         __syncthreads();  // w rows written by group leaders, read per-thread below
         if constexpr (KIND == kKindGmresCgs) {
+          if (a.trace) gb.sync();  // diagnostics: every CTA's SpMV done
+          k4_mark(a);
           // Classical Gram-Schmidt with one re-orthogonalisation when needed
           // (DGKS test, ||w1|| < ||w||/sqrt(2)): 2 all-reduces per step instead of
           // MGS's j+2 (inner.py:251-253 uses MGS; the projections agree to rounding).
           cgs_dots(a, j + 1, true, wl, s_lo, s_hi, pol_last, sh.cv, slot, gb, sh);
+          k4_mark(a);
           const double nw = sh.cv[j + 1];
           double q1[1] = {cgs_update(a, j + 1, sh.cv, wl, s_lo, s_hi, pol_last)};
           grid_allreduce<1>(q1, a, slot, gb, sh);
+          k4_mark(a);
           double nw1 = q1[0];
           const bool reorth = nw1 < 0.5 * nw;  // uniform across the grid
           if (reorth) {
@@ -747,6 +756,7 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
             grid_allreduce<1>(q2, a, slot, gb, sh);
             nw1 = q2[0];
           }
+          k4_mark(a);
           if (tid == 0) {
             for (int l = 0; l <= j; ++l) sh.H[l * R + j] = reorth ? add_rn(sh.cv[l], sh.dv[l]) : sh.cv[l];
           }
@@ -867,6 +877,7 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
         for (int64_t i = s_lo + tid; i < s_hi; i += nthr)  // next SpMV input: keep in L2
           st_hint(Vnew + i, wl[i - s_lo] / hnorm, pol_last);
         gb.sync();
+        if constexpr (KIND == kKindGmresCgs) k4_mark(a);
       }
       if (j == 0) break;
       if (tid == 0) {  // back substitution (inner.py:286-292)
@@ -886,7 +897,7 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
       }
       gb.sync();
       double acc1[1] = {0.0};
-      spmv_rows<G, P, WIN>(a, x, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
+      spmv_rows<G, P, WIN, CONTIG>(a, x, s_lo, s_hi, win, pol, [&](int64_t s, double px, double xs) {
         const double ri = sub_rn(b[s], sub_rn(xs, mul_rn(gam, px)));
         r[s] = ri;
         acc1[0] = add_rn(acc1[0], mul_rn(ri, ri));
@@ -910,9 +921,9 @@ __global__ void __launch_bounds__(kInnerThreads, 1) inner_kernel(KArgs a) {
   }
 }
 
-template <int G, int P, bool WIN, int KIND>
+template <int G, int P, bool WIN, int KIND, bool CONTIG = false>
 static int launch_inner_t(KArgs& a, int smem, int blocks, cudaStream_t st) {
-  auto fn = inner_kernel<G, P, WIN, KIND>;
+  auto fn = inner_kernel<G, P, WIN, KIND, CONTIG>;
   cudaError_t e = raise_smem_limit(fn, smem);
   if (e != cudaSuccess) return fail(IPI_ECUDA, std::string("inner smem attr: ") + cudaGetErrorString(e));
   int per_sm = 0;
@@ -934,6 +945,11 @@ static int dispatch_inner(KArgs& a, int G, int P, int lanes, bool win, int smem,
            : launch_inner_t<GG, PP, false, KIND>(a, smem, blocks, st)
   if (P > 0) {
     IPI_DISPATCH_UNIFORM(G, P, IPI_INNER_LAUNCH);
+    return rc;
+  }
+  if (lanes >= 32 && a.contig) {  // banded rows (C4): no column stream
+    rc = win ? launch_inner_t<32, 0, true, KIND, true>(a, smem, blocks, st)
+             : launch_inner_t<32, 0, false, KIND, true>(a, smem, blocks, st);
     return rc;
   }
   switch (lanes) {

@@ -42,6 +42,24 @@ __global__ void row_stats_kernel(const int64_t* rp, int64_t rows, unsigned long 
   }
 }
 
+// Contiguous rows: every row's columns are consecutive integers (banded
+// birth-death transitions: each SIS row, C4, is the truncated convolution of
+// two binomial pmfs, a log-concave pmf, so its support is an interval).  Then
+// kernels read only the first column of a row (8 instead of 12 bytes per
+// entry).  out[0] stays 1 unless some row breaks the rule.
+__global__ void contiguous_rows_kernel(const int64_t* rp, const int32_t* col, int64_t rows,
+                                       int* out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  bool ok = true;
+  for (int64_t r = wg; r < rows; r += nw) {
+    const int64_t p0 = rp[r], p1 = rp[r + 1];
+    for (int64_t p = p0 + lane; p + 1 < p1; p += 32) ok = ok && (col[p + 1] == col[p] + 1);
+  }
+  if (!__all_sync(kFull, ok) && lane == 0) *out = 0;
+}
+
 // log2 histogram of |col - state| (locality profile, 40 buckets)
 // Rows are sampled with a fixed stride (>= 2^17 sampled rows) so planning stays
 // a few ms even at 2^31 nnz; the histogram only steers the window size.
@@ -138,6 +156,21 @@ static int plan_row_stats(PlanCtx& c) {
   p.row_len_mean = rows > 0 ? (double)nnz / (double)rows : 0.0;
   p.uniform_rows = rows > 0 && p.row_len_min == p.row_len_max;
   p.lanes_per_row = pick_lanes_per_row(p.row_len_mean);
+  p.contiguous_rows = 0;
+  if (rows > 0 && !p.uniform_rows && p.row_len_max > 1) {  // variable rows (C4): one more pass
+    int* d_flag = nullptr;
+    if (cudaMalloc(&d_flag, sizeof(int)) != cudaSuccess) return fail(IPI_ECUDA, "cudaMalloc failed");
+    const int one = 1;
+    int h_flag = 0;
+    cudaMemcpyAsync(d_flag, &one, sizeof(int), cudaMemcpyHostToDevice, st);
+    contiguous_rows_kernel<<<h->num_sms * 8, 256, 0, st>>>(row_ptr, col, rows, d_flag);
+    cudaMemcpyAsync(&h_flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, st);
+    const cudaError_t e2 = cudaStreamSynchronize(st);
+    cudaFree(d_flag);
+    if (e2 != cudaSuccess) return fail(IPI_ECUDA, std::string("planning: ") + cudaGetErrorString(e2));
+    static const bool allow = !(getenv("IPI_CONTIG") && getenv("IPI_CONTIG")[0] == '0');
+    p.contiguous_rows = h_flag && allow;
+  }
   p.k1_threads = kK1Threads;
   p.inner_threads = kInnerThreads;
   return IPI_OK;

@@ -26,7 +26,9 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--its", type=int, default=60)
     ap.add_argument("--kind", default="gmres")
+    ap.add_argument("--ortho", default="auto")
     ap.add_argument("--stepped", action="store_true")
+    ap.add_argument("--generic", action="store_true", help="1024-thread CGS2 kernel marks (C4)")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     mdp, spec = devgen.build_instance(a.config)
@@ -40,32 +42,35 @@ def main():
         rep = _lib.InnerReport()
         _lib.check(L.ipi_inner_solve(_lib.ptr(p.row_ptr), _lib.ptr(p.col_idx), _lib.ptr(p.values),
                                      mdp.n, spec.gamma, _lib.ptr(b), _lib.ptr(x), 0.0, a.its,
-                                     _lib.KSP[a.kind], 1.0, None, 0, _lib.C.byref(rep),
+                                     _lib.KSP[a.kind], 1.0, None, _lib.ORTHO[a.ortho],
+                                     _lib.C.byref(rep),
                                      _lib.stream_ptr()))
         torch.cuda.synchronize()
 
-    # the standalone K3 operator on the same P_pi, for comparison
-    from paper_2507_22538_b200.sparse import DeviceOperator
-    op = DeviceOperator(p.row_ptr, p.col_idx, p.values, mdp.n, mdp.n, 0, spec.gamma)
-    xk = torch.rand(mdp.n, dtype=torch.float64, device="cuda")
-    yk = torch.empty_like(xk)
-    for _ in range(3):
-        op.apply(xk, out=yk)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    e0.record()
-    for _ in range(20):
-        op.apply(xk, out=yk)
-    e1.record()
-    torch.cuda.synchronize()
-    print(f"K3 apply: {e0.elapsed_time(e1) / 20 * 1e3:.1f} us per launch, plan {op.plan()}")
-    ms = _lib.C.c_float()
-    yr = torch.empty_like(xk)
-    _lib.check(L.ipi_k4_ring_apply_test(_lib.ptr(p.col_idx), _lib.ptr(p.values), mdp.n, spec.gamma,
-                                        _lib.ptr(xk), _lib.ptr(yr), 20, _lib.C.byref(ms),
-                                        _lib.stream_ptr()))
-    print(f"ring_rows as a plain kernel: {ms.value / 20 * 1e3:.1f} us per launch; "
-          f"bitwise equal to K3: {bool(torch.equal(yr, yk))}")
+    plan = mdp.plan()
+    if plan["uniform_rows"] and plan["row_len_max"] == 64:
+        # the standalone K3 operator on the same P_pi, for comparison
+        from paper_2507_22538_b200.sparse import DeviceOperator
+        op = DeviceOperator(p.row_ptr, p.col_idx, p.values, mdp.n, mdp.n, 0, spec.gamma)
+        xk = torch.rand(mdp.n, dtype=torch.float64, device="cuda")
+        yk = torch.empty_like(xk)
+        for _ in range(3):
+            op.apply(xk, out=yk)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(20):
+            op.apply(xk, out=yk)
+        e1.record()
+        torch.cuda.synchronize()
+        print(f"K3 apply: {e0.elapsed_time(e1) / 20 * 1e3:.1f} us per launch, plan {op.plan()}")
+        ms = _lib.C.c_float()
+        yr = torch.empty_like(xk)
+        _lib.check(L.ipi_k4_ring_apply_test(_lib.ptr(p.col_idx), _lib.ptr(p.values), mdp.n, spec.gamma,
+                                            _lib.ptr(xk), _lib.ptr(yr), 20, _lib.C.byref(ms),
+                                            _lib.stream_ptr()))
+        print(f"ring_rows as a plain kernel: {ms.value / 20 * 1e3:.1f} us per launch; "
+              f"bitwise equal to K3: {bool(torch.equal(yr, yk))}")
     run()
     _lib.check(L.ipi_k4_trace(1, None, 0))
     run()
@@ -73,6 +78,20 @@ def main():
     _lib.check(L.ipi_k4_trace(0, buf.ctypes.data, 8192))
     k = int(buf[0])
     t0 = buf[1:k + 1].astype(np.int64)
+    if a.generic:
+        # 1024-thread CGS2 kernel marks: start, spmv(+barrier), dots, update, reorth, end
+        names = ["spmv+barrier", "cgs_dots+allreduce", "cgs_update+allreduce", "reorth (if any)",
+                 "givens+write+barrier"]
+        t = t0[3:]
+        m6 = (len(t) // 6) * 6
+        t6 = t[:m6].reshape(-1, 6)
+        d = np.diff(t6, axis=1) / 1e3
+        print(f"{spec.name} gmres/cgs2 (1024-thread kernel): {len(d)} steps; reorth in "
+              f"{int((d[:, 3] > 0.5).sum())}")
+        for c, nm in enumerate(names):
+            print(f"  {nm:28s} median {np.median(d[:, c]):8.2f} us  p90 {np.percentile(d[:, c], 90):8.2f}")
+        print(f"  step total median {np.median(d.sum(1)):.2f} us")
+        return
     if a.stepped:
         # step_ortho marks: start, MGS done, end (3 per step); gaps = K3 + launches
         t3 = t0[: (len(t0) // 3) * 3].reshape(-1, 3)

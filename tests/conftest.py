@@ -55,3 +55,20 @@ def load_golden(name):
 @pytest.fixture
 def rng():
     return np.random.default_rng(20240817)
+
+
+def assert_outer_count(res, ref, tol, alpha):
+    """Outer counts must be equal, except for the one documented mechanism:
+    the last inner solve only reaches ||r||_2 <= alpha * res_{k-1}, so V_k is
+    pinned to that slack and a summation-order difference can put the two
+    runs' k-th residual on opposite sides of tol (observed once on C4, 34 vs
+    33).  Then the k-th residuals must straddle tol and agree within the
+    inner solve's slack; anything else is a real trajectory divergence."""
+    ko, kr = res.outer_iterations, ref.outer_iterations
+    if ko == kr:
+        return
+    assert abs(ko - kr) == 1, (ko, kr)
+    k = min(ko, kr)
+    h, r = res.residual_history[k], ref.residual_history[k]
+    assert min(h, r) <= tol < max(h, r), (h, r, tol)
+    assert abs(h - r) <= 1e-6 * r + alpha * ref.residual_history[k - 1], (h, r)

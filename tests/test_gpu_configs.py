@@ -17,6 +17,7 @@ if not torch.cuda.is_available():  # pragma: no cover
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
 import paper_2507_22538_b200 as ipi  # noqa: E402
+from conftest import assert_outer_count  # noqa: E402
 from paper_2507_22538_b200 import devgen, generators as gen  # noqa: E402
 from paper_2507_22538_b200.bellman import greedy_device  # noqa: E402
 
@@ -84,11 +85,7 @@ def solve_parity(mdp, spec, arrays, *, tol=None, kind="gmres", max_outer=1000):
     ref = orc.solve(rp, col, val, cost, spec.gamma, tol=tol, alpha=spec.alpha, kind=kind,
                     max_outer=max_outer)
     assert res.status.value == ref.status
-    # The last inner solve only reaches ||r||_2 <= alpha*res; when the oracle's final
-    # outer residual lands within that slack of tol, a rounding-order difference can
-    # cost one extra outer step (observed once on C4: 34 vs 33, final V within 2e-10).
-    assert abs(res.outer_iterations - ref.outer_iterations) <= 1, (res.residual_history,
-                                                                   ref.residual_history)
+    assert_outer_count(res, ref, tol, spec.alpha)
     k = min(len(res.residual_history), len(ref.residual_history)) - 1
     h, hr = np.asarray(res.residual_history[:k]), np.asarray(ref.residual_history[:k])
     slack = np.concatenate(([0.0], spec.alpha * hr[:-1])) if k else hr
@@ -249,7 +246,7 @@ def test_c2_full_size_oracle_parity(c2_full):
     res_gpu = ipi.solve(mdp, ipi.SolveOptions(alpha=spec.alpha, tol=spec.atol))
     ref = co.solve(rp, col, val, cost, spec.gamma, tol=spec.atol, alpha=spec.alpha, nthreads=nt)
     assert res_gpu.status.value == ref.status == "converged"
-    assert abs(res_gpu.outer_iterations - ref.outer_iterations) <= 1
+    assert_outer_count(res_gpu, ref, spec.atol, spec.alpha)
     scale = max(1.0, np.abs(ref.values).max())
     np.testing.assert_allclose(res_gpu.values, ref.values, rtol=1e-8, atol=1e-8 * scale)
     diff = np.flatnonzero(res_gpu.policy != ref.policy)
@@ -277,7 +274,7 @@ def test_sharded_driver_matches_persistent_solver(kind):
     res = solve_sharded(ShardOps(shard, ctx), opts, mdp.n)
     ref = ipi.solve(mdp, opts)
     assert res.status == ref.status
-    assert abs(res.outer_iterations - ref.outer_iterations) <= 1
+    assert_outer_count(res, ref, spec.atol, spec.alpha)
     np.testing.assert_allclose(res.values, ref.values, rtol=1e-8, atol=1e-8)
     np.testing.assert_array_equal(res.policy, ref.policy)
 
@@ -322,7 +319,7 @@ def test_c4_full_size_oracle_parity():
     res_gpu = ipi.solve(mdp, ipi.SolveOptions(alpha=spec.alpha, tol=spec.atol))
     ref = co.solve(rp, col, val, cost, spec.gamma, tol=spec.atol, alpha=spec.alpha, nthreads=nt)
     assert res_gpu.status.value == ref.status == "converged"
-    assert abs(res_gpu.outer_iterations - ref.outer_iterations) <= 1
+    assert_outer_count(res_gpu, ref, spec.atol, spec.alpha)
     scale = max(1.0, np.abs(ref.values).max())
     np.testing.assert_allclose(res_gpu.values, ref.values, rtol=1e-8, atol=1e-8 * scale)
     diff = np.flatnonzero(res_gpu.policy != ref.policy)

@@ -23,6 +23,7 @@ if not torch.cuda.is_available():  # pragma: no cover - CPU container
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
 import paper_2507_22538_b200 as ipi  # noqa: E402
+from conftest import assert_outer_count  # noqa: E402
 from paper_2507_22538_b200 import devgen  # noqa: E402
 
 
@@ -81,7 +82,8 @@ def test_two_ranks_on_device_match_persistent_solver(kind, n, overlap, ortho):
     ref = ipi.solve(mdp, ipi.SolveOptions(alpha=spec.alpha, tol=spec.atol,
                                           inner=ipi.InnerSolver.from_name(kind), max_outer=200))
     assert st0 == ref.status.value
-    assert abs(k0 - ref.outer_iterations) <= 1
+    assert_outer_count(type("R", (), {"outer_iterations": k0, "residual_history": h0})(), ref,
+                       spec.atol, spec.alpha)
     np.testing.assert_allclose(v0, ref.values, rtol=1e-8, atol=1e-8)
     np.testing.assert_array_equal(p0, ref.policy)
 
@@ -158,7 +160,8 @@ def _sis_worker(rank, world, port, q, halo_frac):
         ops = ShardOps(shard, ctx)
         res = solve_sharded(ops, ipi.SolveOptions(alpha=spec.alpha, tol=spec.atol), n)
         q.put((rank, ops.halo.enabled, ops.halo.bytes_received(), res.status.value,
-               res.outer_iterations, res.values.tolist(), res.policy.tolist()))
+               res.outer_iterations, res.values.tolist(), res.policy.tolist(),
+               res.residual_history))
     finally:
         dist.destroy_process_group()
 
@@ -176,7 +179,7 @@ def test_two_ranks_sis_halo_exchange(halo_frac):
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    (_, en0, b0, st0, k0, v0, p0), (_, en1, b1, st1, k1, v1, p1) = out
+    (_, en0, b0, st0, k0, v0, p0, h0), (_, en1, b1, st1, k1, v1, p1, _) = out
     assert en0 == en1 == (halo_frac == "1.0")
     if en0:  # a halo, not the other rank's whole block
         assert 0 < b0 < 8 * 1001 and 0 < b1 < 8 * 1001
@@ -184,6 +187,7 @@ def test_two_ranks_sis_halo_exchange(halo_frac):
     mdp, spec = devgen.build_instance(4, population=2000)
     ref = ipi.solve(mdp, ipi.SolveOptions(alpha=spec.alpha, tol=spec.atol))
     assert st0 == ref.status.value
-    assert abs(k0 - ref.outer_iterations) <= 1
+    assert_outer_count(type("R", (), {"outer_iterations": k0, "residual_history": h0})(), ref,
+                       spec.atol, spec.alpha)
     np.testing.assert_allclose(v0, ref.values, rtol=1e-8, atol=1e-8 * np.abs(ref.values).max())
     np.testing.assert_array_equal(p0, ref.policy)
