@@ -64,6 +64,11 @@ struct StepArgs {
   int first;  // step_cycle_start: first call of the solve
   unsigned long long* trace;  // diagnostics (ipi_k4_trace): step_ortho start / MGS done / end
   int trace_cap;
+  unsigned long long* board;  // LL all-reduce mailboxes + result slots (ll_allreduce)
+  unsigned call_base;         // first LL call number of this launch (unique per launch)
+  int pf;                     // step_ortho: basis vectors prefetched into L2 ahead of the MGS pass
+  long long* prof;            // diagnostics (IPI_STEP_PROF=1): cycle counters of CTA 1, or nullptr
+  int dbg;                    // timing experiments (IPI_STEP_DBG): 1 = skip the basis loads (wrong results)
 };
 
 constexpr int kStepThreads = 512;
@@ -79,6 +84,154 @@ __device__ __forceinline__ void step_slice(int64_t n, int64_t& lo, int64_t& hi) 
   const int64_t c = blockIdx.x, nb = gridDim.x;
   lo = c == 0 ? 0 : ((n * c / nb) & ~(int64_t)1);
   hi = c + 1 == nb ? n : ((n * (c + 1) / nb) & ~(int64_t)1);
+}
+
+// step_ortho: CTA 0 is the all-reduce's reducer and owns no elements; the
+// worker CTAs 1..nb-1 split the vectors.
+__device__ __forceinline__ void ortho_slice(int64_t n, int64_t& lo, int64_t& hi) {
+  const int64_t c = (int64_t)blockIdx.x - 1, nb = (int64_t)gridDim.x - 1;
+  if (c < 0) {
+    lo = hi = 0;
+    return;
+  }
+  lo = c == 0 ? 0 : ((n * c / nb) & ~(int64_t)1);
+  hi = c + 1 == nb ? n : ((n * (c + 1) / nb) & ~(int64_t)1);
+}
+
+// ---------------------------------------------------------------------------
+// LL all-reduce: a deterministic grid all-reduce of NV <= 3 doubles without a
+// counter barrier or fences.  A message is two 8-byte words, each carrying 32
+// data bits and the 32-bit call number, so every word validates itself and no
+// ordering between words is needed (relaxed gpu-scope accesses; the protocol
+// NCCL's LL uses).  Worker CTAs post their block partial to their mailbox;
+// CTA 0 gathers with one polling lane per mailbox (warp 5 v + q takes value v
+// of CTAs 32 q + lane: with a single polling warp the fan-in cost 1.4 us more,
+// scripts/micro/allreduce_ll2.cu), adds them in CTA order (lane-wise over q,
+// then the fixed xor tree) and posts the sums to the result slots every worker
+// polls.  Measured 1.64 us per call on 148 CTAs against 2.3 us for the counter
+// barrier + ordered partial reads of grid_allreduce.  Call numbers never repeat
+// within a solve (the board is zeroed per solve; numbers start at 1), so a
+// stale mailbox can never match.
+// ---------------------------------------------------------------------------
+constexpr int kLLVals = 3;
+constexpr int kLLChunks = 5;  // reducer lanes cover up to 160 CTAs
+
+struct LLShared {
+  double red[kLLVals * 32];
+  double xs[kLLVals][kLLChunks][32];
+  double bc[4];
+};
+
+__device__ __forceinline__ void ll_store(unsigned long long* dst, double v, unsigned call) {
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+  const unsigned long long w0 = (bits & 0xffffffffull) | ((unsigned long long)call << 32);
+  const unsigned long long w1 = (bits >> 32) | ((unsigned long long)call << 32);
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(dst), "l"(w0), "l"(w1) : "memory");
+}
+__device__ __forceinline__ double ll_wait(const unsigned long long* src, unsigned call) {
+  unsigned long long w0, w1;
+  do {
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(src) : "memory");
+  } while ((unsigned)(w0 >> 32) != call || (unsigned)(w1 >> 32) != call);
+  return __longlong_as_double((long long)((w0 & 0xffffffffull) | (w1 << 32)));
+}
+
+int64_t ll_board_words(int blocks) { return 2 * ((int64_t)kLLVals * blocks + kLLVals + 5); }
+
+// Named CTA barriers of the split all-reduce: the worker warps arrive on
+// kBarPosted without waiting (their partials are in shared memory), issue
+// whatever loads they want in flight during the exchange, and wait on
+// kBarResult, which the control warp (warp 0) arrives on once the sums are in
+// sh.bc.  (With the loads issued before a blocking barrier the workers only
+// reached it after the load queue had drained: +0.8 us per MGS pass.)
+constexpr int kBarPosted = 1, kBarResult = 2, kBarGo = 3;
+__device__ __forceinline__ void bar_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// First half, every thread of every CTA: `v` holds the thread's partials
+// (ignored in CTA 0).  Worker threads return at once; warp 0 of a worker CTA
+// returns after posting the block's partial; CTA 0 returns after publishing.
+template <int NV>
+__device__ __forceinline__ void ll_post(const double (&v)[NV], unsigned long long* board, unsigned& call,
+                                        LLShared& sh) {
+  static_assert(NV <= kLLVals, "LL all-reduce carries up to kLLVals values");
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nb = gridDim.x;
+  const int nthr = blockDim.x;
+  unsigned long long* pub = board + 2 * (int64_t)kLLVals * nb;
+  ++call;
+  if (blockIdx.x != 0) {
+    if (warp != 0) {
+      double t[NV];
+#pragma unroll
+      for (int k = 0; k < NV; ++k) t[k] = warp_sum(v[k]);
+      if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) sh.red[k * 32 + warp] = t[k];
+      }
+      bar_arrive(kBarPosted, nthr);
+      // the block's post enters the memory pipeline ahead of the callers' loads:
+      // behind a 57 KB load burst it left the SM ~1500 cycles late
+      bar_sync(kBarGo, nthr);
+    } else {
+      bar_sync(kBarPosted, nthr);
+      const int nw = nthr >> 5;
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {  // warp 0 holds no elements: lanes 1.. carry the workers
+        const double tk = warp_sum(lane >= 1 && lane < nw ? sh.red[k * 32 + lane] : 0.0);
+        if (lane == k) ll_store(board + 2 * ((int64_t)k * nb + blockIdx.x), tk, call);
+      }
+      bar_arrive(kBarGo, nthr);
+    }
+  } else {
+    if (warp < kLLChunks * NV) {
+      const int k = warp / kLLChunks, q = warp % kLLChunks, c = lane + 32 * q;
+      sh.xs[k][q][lane] = c >= 1 && c < nb ? ll_wait(board + 2 * ((int64_t)k * nb + c), call) : 0.0;
+    }
+    __syncthreads();
+    if (warp < NV) {
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < kLLChunks; ++q)
+        if (lane + 32 * q < nb) s = add_rn(s, sh.xs[warp][q][lane]);
+      s = warp_sum(s);
+      if (lane == 0) {
+        ll_store(pub + 2 * warp, s, call);
+        sh.bc[warp] = s;
+      }
+    }
+  }
+}
+
+// Second half: on return every thread of the grid holds the sums in `v`.
+template <int NV>
+__device__ __forceinline__ void ll_wait_result(double (&v)[NV], unsigned long long* board, unsigned call,
+                                               LLShared& sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nb = gridDim.x;
+  const int nthr = blockDim.x;
+  const unsigned long long* pub = board + 2 * (int64_t)kLLVals * nb;
+  if (blockIdx.x != 0) {
+    if (warp == 0) {
+      if (lane < NV) sh.bc[lane] = ll_wait(pub + 2 * lane, call);
+      bar_arrive(kBarResult, nthr);
+    } else {
+      bar_sync(kBarResult, nthr);
+    }
+  } else {
+    __syncthreads();
+  }
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v[k] = sh.bc[k];
+}
+
+template <int NV>
+__device__ __forceinline__ void ll_allreduce(double (&v)[NV], unsigned long long* board, unsigned& call,
+                                             LLShared& sh) {
+  ll_post<NV>(v, board, call, sh);
+  ll_wait_result<NV>(v, board, call, sh);
 }
 
 // grid_allreduce (krylov.cuh) reads only KArgs::partials; wrap ours.
@@ -98,6 +251,54 @@ __device__ __forceinline__ void publish_flags(const StepArgs& a, const StepState
   __threadfence_system();
 }
 
+// Givens update of the new Hessenberg column (inner.py:256-270), run by
+// thread 0 of every CTA on identical inputs; CTA 0 stores the state.  Every
+// CTA took its snapshot of the state before its first all-reduce of the
+// launch, so CTA 0 may update it here.
+__device__ __forceinline__ void step_givens(const StepArgs& a, StepState* st, int j, double hnorm,
+                                            double* hcol, const double* cs_s, const double* sn_s,
+                                            double gj_s, double est_s, int& brk_s) {
+  if (threadIdx.x != 0) return;
+  hcol[j + 1] = hnorm;
+  for (int l = 0; l < j; ++l) {
+    const double hl = hcol[l], hl1 = hcol[l + 1];
+    const double cs = cs_s[l], sn = sn_s[l];
+    hcol[l] = add_rn(mul_rn(cs, hl), mul_rn(sn, hl1));
+    hcol[l + 1] = add_rn(mul_rn(-sn, hl), mul_rn(cs, hl1));
+  }
+  const double denom = hypot(hcol[j], hcol[j + 1]);
+  int brk = 0;
+  double csj = 0.0, snj = 0.0, gj = gj_s, gj1 = 0.0;
+  if (denom == 0.0) {
+    brk = 1;
+  } else {
+    csj = hcol[j] / denom;
+    snj = hcol[j + 1] / denom;
+    hcol[j] = denom;
+    hcol[j + 1] = 0.0;
+    gj1 = mul_rn(-snj, gj);
+    gj = mul_rn(csj, gj);
+    if (fabs(gj1) <= est_s || hnorm == 0.0) brk = 2;
+  }
+  brk_s = brk;
+  if (blockIdx.x == 0) {
+    for (int l = 0; l <= j + 1; ++l) st->H[l * R + j] = hcol[l];
+    if (brk != 1) {
+      st->cs[j] = csj;
+      st->sn[j] = snj;
+      st->g[j] = gj;
+      st->g[j + 1] = gj1;
+    }
+    const int jn = brk == 1 ? j : j + 1;
+    const int itn = st->it + 1;
+    st->j = jn;
+    st->it = itn;
+    st->basis_reads += j + 1;
+    st->active = (brk == 0 && jn < R && itn < a.max_it) ? 1 : 0;
+    publish_flags(a, *st);
+  }
+}
+
 // One Arnoldi step after the K3 launch wrote w = V_j - gamma P V_j: MGS with
 // this CTA's slice of w in registers and V_{l+1}'s slice loaded into
 // registers while the all-reduce producing h_l is in flight, so a pass costs
@@ -105,7 +306,7 @@ __device__ __forceinline__ void publish_flags(const StepArgs& a, const StepState
 // (Streaming the slices through shared memory with 1-D bulk copies two
 // passes ahead measured slower: 4.5 us per pass.)
 __global__ void __launch_bounds__(kStepThreads, 1) step_ortho(StepArgs a) {
-  __shared__ KShared sh;
+  __shared__ LLShared sh;
   __shared__ double hcol[R + 1], cs_s[R], sn_s[R], gj_s, est_s;
   __shared__ int brk_s;
   StepState* st = a.s;
@@ -115,16 +316,14 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_ortho(StepArgs a) {
   if (blockIdx.x == 0 && tid == 0) a.bar[a.parity ^ 1] = 0u;
   if (!st->active) return;  // uniform: the previous launch ended the cycle
   k4_mark_raw(a.trace, a.trace_cap);
-  GridBarrier gb{a.bar + a.parity, 0u, 0};
-  const KArgs ka = step_kargs(a);
-  int slot = 0;
+  unsigned call = a.call_base;
   const int j = st->j;
   const int64_t n = a.n, ldv = a.ldv;
   int64_t s_lo, s_hi;
-  step_slice(n, s_lo, s_hi);
+  ortho_slice(n, s_lo, s_hi);
   const int64_t own = s_hi - s_lo;
   const uint64_t pol_keep = policy_evict_last(), pol_first = policy_evict_first();
-  if (tid == 0) {  // snapshot the rotation state before the first grid barrier:
+  if (tid == 0) {  // snapshot the rotation state before the first all-reduce:
     for (int l = 0; l < j; ++l) {  // CTA 0 updates g[j] after the last one
       cs_s[l] = st->cs[l];
       sn_s[l] = st->sn[l];
@@ -132,6 +331,14 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_ortho(StepArgs a) {
     gj_s = st->g[j];
     est_s = st->est_target;
   }
+  // The basis does not stay in L2 across the K3 launches (P_pi streams 822 MB
+  // per step), and with only V_{l+1} in flight a pass waits one DRAM round
+  // trip (3.3 us per pass on C2).  The control warp therefore pulls this CTA's
+  // slices of the next a.pf vectors into L2 with bulk prefetches; the register
+  // loads below then hit L2.
+  const uint32_t pf_bytes = (uint32_t)((own * 8) & ~(int64_t)15);
+  if (tid < a.pf && tid + 1 <= j && pf_bytes)
+    l2_prefetch(a.V + (int64_t)(tid + 1) * ldv + s_lo, pf_bytes);
   double wv[kStepE], vc[kStepE];
   const int64_t wt = tid - 32;  // worker index (< 0: the control warp)
   auto elem = [&](int k) -> int64_t { return wt < 0 ? own : wt + (int64_t)k * kStepWorkers; };
@@ -151,6 +358,8 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_ortho(StepArgs a) {
 #pragma unroll
   for (int k = 0; k < kStepE; ++k) p[0] = add_rn(p[0], mul_rn(vc[k], wv[k]));
   for (int l = 0; l <= j; ++l) {
+    const long long pc0 = a.prof ? clock64() : 0;
+    ll_post<1>(p, a.board, call, sh);
     double vn[kStepE];
     if (l < j) {  // V_{l+1} in flight while h_l is reduced
       const double* Vn = a.V + (int64_t)(l + 1) * ldv + s_lo;
@@ -158,10 +367,13 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_ortho(StepArgs a) {
 #pragma unroll
       for (int k = 0; k < kStepE; ++k) {
         const int64_t e = elem(k);
-        vn[k] = e < own ? ld_hint(Vn + e, pol) : 0.0;
+        vn[k] = e < own && !(a.dbg & 1) ? ld_hint(Vn + e, pol) : 0.0;
       }
     }
-    grid_allreduce<1>(p, ka, slot, gb, sh);
+    if (tid == 0 && l + 1 + a.pf <= j && pf_bytes)
+      l2_prefetch(a.V + (int64_t)(l + 1 + a.pf) * ldv + s_lo, pf_bytes);
+    ll_wait_result<1>(p, a.board, call, sh);
+    if (a.prof && blockIdx.x == 1 && tid == 32) a.prof[4] += clock64() - pc0;  // a worker's whole call
     const double h = p[0];
     if (tid == 0) hcol[l] = h;
     double q = 0.0;
@@ -178,53 +390,183 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_ortho(StepArgs a) {
       for (int k = 0; k < kStepE; ++k) q = add_rn(q, mul_rn(wv[k], wv[k]));
     }
     p[0] = q;
+    if (a.prof && blockIdx.x == 1 && tid == 32) {
+      a.prof[5] += clock64() - pc0;  // whole pass
+      a.prof[3] += 1;
+    }
   }
-  grid_allreduce<1>(p, ka, slot, gb, sh);
+  ll_allreduce<1>(p, a.board, call, sh);
   const double hnorm = sqrt(p[0]);
   k4_mark_raw(a.trace, a.trace_cap);
-  // Givens update (inner.py:256-270), redundantly in every CTA; CTA 0 stores.
-  if (tid == 0) {
-    hcol[j + 1] = hnorm;
-    for (int l = 0; l < j; ++l) {
-      const double hl = hcol[l], hl1 = hcol[l + 1];
-      const double cs = cs_s[l], sn = sn_s[l];
-      hcol[l] = add_rn(mul_rn(cs, hl), mul_rn(sn, hl1));
-      hcol[l + 1] = add_rn(mul_rn(-sn, hl), mul_rn(cs, hl1));
-    }
-    const double denom = hypot(hcol[j], hcol[j + 1]);
-    int brk = 0;
-    double csj = 0.0, snj = 0.0, gj = gj_s, gj1 = 0.0;
-    if (denom == 0.0) {
-      brk = 1;
-    } else {
-      csj = hcol[j] / denom;
-      snj = hcol[j + 1] / denom;
-      hcol[j] = denom;
-      hcol[j + 1] = 0.0;
-      gj1 = mul_rn(-snj, gj);
-      gj = mul_rn(csj, gj);
-      if (fabs(gj1) <= est_s || hnorm == 0.0) brk = 2;
-    }
-    brk_s = brk;
-    // every CTA took its snapshot of st before its first grid barrier, so
-    // CTA 0 may update the state now
-    if (blockIdx.x == 0) {
-      for (int l = 0; l <= j + 1; ++l) st->H[l * R + j] = hcol[l];
-      if (brk != 1) {
-        st->cs[j] = csj;
-        st->sn[j] = snj;
-        st->g[j] = gj;
-        st->g[j + 1] = gj1;
-      }
-      const int jn = brk == 1 ? j : j + 1;
-      const int itn = st->it + 1;
-      st->j = jn;
-      st->it = itn;
-      st->basis_reads += j + 1;
-      st->active = (brk == 0 && jn < R && itn < a.max_it) ? 1 : 0;
-      publish_flags(a, *st);
+  step_givens(a, st, j, hnorm, hcol, cs_s, sn_s, gj_s, est_s, brk_s);
+  __syncthreads();
+  if (brk_s == 0) {  // V_{j+1} = w / hnorm: the next K3 launch's input, keep it in L2
+    double* Vnew = a.V + (int64_t)(j + 1) * ldv + s_lo;
+#pragma unroll
+    for (int k = 0; k < kStepE; ++k) {
+      const int64_t e = elem(k);
+      if (e < own) st_hint(Vnew + e, wv[k] / hnorm, pol_keep);
     }
   }
+  k4_mark_raw(a.trace, a.trace_cap);
+}
+
+// Pair-blocked MGS: the same Arnoldi step with the basis taken two vectors per
+// all-reduce, so a step makes ceil((j+1)/2) + 1 dependent grid exchanges
+// instead of j + 2.  For the pair (V_l, V_{l+1}) one exchange carries
+//   d0 = <V_l, w_l>,  d1 = <V_{l+1}, w_l>,  G = <V_{l+1}, V_l>
+// and h_l = d0, h_{l+1} = d1 - h_l G, which is MGS's <V_{l+1}, w_l - h_l V_l>
+// expanded by linearity: identical in exact arithmetic, and it keeps MGS's
+// correction for a basis that has lost orthogonality (G is the measured
+// inner product, ~1e-16 here, not assumed zero).  w is then updated as MGS
+// does, (w - h_l V_l) - h_{l+1} V_{l+1}.  h_l is bitwise MGS's; h_{l+1}
+// differs from it by rounding of order eps |w|.
+//
+// Data movement: the pair in use lives in registers (va, vb); the next pair is
+// copied into shared memory with cp.async (16-byte chunks, every thread copies
+// exactly the elements it owns, so it waits only on its own groups) while the
+// exchange of the current pair is in flight.  The dots of the next pair read
+// shared memory directly (the LDS traffic hides under the FP64 pipe); the
+// register copy of that pair happens during its own exchange.
+constexpr int kPairChunks = kStepE / 2;                          // 16-byte chunks per thread and vector
+constexpr int kPairSmem = 2 * kPairChunks * kStepWorkers * 16;   // two vectors staged
+
+__global__ void __launch_bounds__(kStepThreads, 1) step_ortho_pair(StepArgs a) {
+  extern __shared__ __align__(16) unsigned char stage_raw[];
+  __shared__ LLShared sh;
+  __shared__ double hcol[R + 1], cs_s[R], sn_s[R], gj_s, est_s;
+  __shared__ int brk_s;
+  StepState* st = a.s;
+  const int tid = threadIdx.x;
+  if (blockIdx.x == 0 && tid == 0) a.bar[a.parity ^ 1] = 0u;
+  if (!st->active) return;  // uniform: the previous launch ended the cycle
+  k4_mark_raw(a.trace, a.trace_cap);
+  unsigned call = a.call_base;
+  const int j = st->j;
+  const int64_t n = a.n, ldv = a.ldv;
+  int64_t s_lo, s_hi;
+  ortho_slice(n, s_lo, s_hi);
+  const int64_t own = s_hi - s_lo;
+  const uint64_t pol_keep = policy_evict_last(), pol_first = policy_evict_first();
+  if (tid == 0) {
+    for (int l = 0; l < j; ++l) {
+      cs_s[l] = st->cs[l];
+      sn_s[l] = st->sn[l];
+    }
+    gj_s = st->g[j];
+    est_s = st->est_target;
+  }
+  const int64_t wt = tid - 32;  // worker index (< 0: the control warp owns nothing)
+  // element k of this thread: chunk k/2 (16 bytes), half k%2
+  auto elem = [&](int k) -> int64_t {
+    return wt < 0 ? own : 2 * (wt + (int64_t)(k >> 1) * kStepWorkers) + (k & 1);
+  };
+  const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(stage_raw);
+  auto slot = [&](int v, int c) -> uint32_t {  // byte offset of chunk c of staged vector v
+    return (uint32_t)(((v * kPairChunks + c) * kStepWorkers + (int)(wt < 0 ? 0 : wt)) * 16);
+  };
+  // stage vectors l, l+1 (those <= j) of the basis: this thread's chunks only
+  auto stage_pair = [&](int l) {
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      if (l + v <= j) {
+        const double* Vl = a.V + (int64_t)(l + v) * ldv + s_lo;
+        const uint64_t pol = l + v < j ? pol_keep : pol_first;
+#pragma unroll
+        for (int c = 0; c < kPairChunks; ++c) {
+          const int64_t e = elem(2 * c);
+          if (e < own) cp_async16(stage_s + slot(v, c), Vl + e, e + 1 < own ? 16u : 8u, pol);
+        }
+      }
+    }
+    cp_async_commit();
+  };
+  auto staged = [&](int v, int c) -> double2 {
+    return *reinterpret_cast<const double2*>(stage_raw + slot(v, c));
+  };
+  double wv[kStepE], va[kStepE], vb[kStepE];
+#pragma unroll
+  for (int k = 0; k < kStepE; ++k) {
+    const int64_t e = elem(k);
+    double wi = 0.0, v0 = 0.0, v1 = 0.0;
+    if (e < own) {
+      wi = a.w[s_lo + e];
+      if (a.invd) wi = mul_rn(wi, a.invd[s_lo + e]);  // w = pc(A v_j)  (inner.py:249)
+      v0 = ld_hint(a.V + s_lo + e, j > 0 ? pol_keep : pol_first);
+      if (j >= 1) v1 = ld_hint(a.V + ldv + s_lo + e, j > 1 ? pol_keep : pol_first);
+    }
+    wv[k] = wi;
+    va[k] = v0;
+    vb[k] = v1;
+  }
+  if (j >= 2) stage_pair(2);
+  double p[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+  for (int k = 0; k < kStepE; ++k) {
+    p[0] = add_rn(p[0], mul_rn(va[k], wv[k]));
+    p[1] = add_rn(p[1], mul_rn(vb[k], wv[k]));
+    p[2] = add_rn(p[2], mul_rn(vb[k], va[k]));
+  }
+  for (int l = 0; l <= j; l += 2) {
+    const bool two = l + 1 <= j, more = l + 2 <= j;
+    ll_post<3>(p, a.board, call, sh);
+    if (l > 0) {
+      // the pair being exchanged moves from the stage to registers (its dots
+      // were taken from the stage), then the stage takes the next pair
+#pragma unroll
+      for (int c = 0; c < kPairChunks; ++c) {
+        const bool ok = elem(2 * c) < own;  // chunks past the slice were never staged
+        const double2 x = ok ? staged(0, c) : make_double2(0.0, 0.0);
+        const double2 y = ok && two ? staged(1, c) : make_double2(0.0, 0.0);
+        va[2 * c] = x.x;
+        va[2 * c + 1] = x.y;
+        vb[2 * c] = y.x;
+        vb[2 * c + 1] = y.y;
+      }
+      if (more) stage_pair(l + 2);
+    }
+    ll_wait_result<3>(p, a.board, call, sh);
+    const double h0 = p[0];
+    const double h1 = two ? sub_rn(p[1], mul_rn(h0, p[2])) : 0.0;
+    if (tid == 0) {
+      hcol[l] = h0;
+      if (two) hcol[l + 1] = h1;
+    }
+#pragma unroll
+    for (int k = 0; k < kStepE; ++k) {
+      wv[k] = sub_rn(wv[k], mul_rn(h0, va[k]));
+      if (two) wv[k] = sub_rn(wv[k], mul_rn(h1, vb[k]));
+    }
+    double q0 = 0.0, q1 = 0.0, q2 = 0.0;
+    if (more) {
+      const bool two_n = l + 3 <= j;
+      cp_async_wait<0>();  // this thread's chunks of the next pair
+#pragma unroll
+      for (int c = 0; c < kPairChunks; ++c) {
+        const bool ok = elem(2 * c) < own;
+        const double2 x = ok ? staged(0, c) : make_double2(0.0, 0.0);
+        const double2 y = ok && two_n ? staged(1, c) : make_double2(0.0, 0.0);
+        // a chunk's second half is zero-filled past the slice end (8-byte copy)
+        q0 = add_rn(q0, mul_rn(x.x, wv[2 * c]));
+        q0 = add_rn(q0, mul_rn(x.y, wv[2 * c + 1]));
+        q1 = add_rn(q1, mul_rn(y.x, wv[2 * c]));
+        q1 = add_rn(q1, mul_rn(y.y, wv[2 * c + 1]));
+        q2 = add_rn(q2, mul_rn(y.x, x.x));
+        q2 = add_rn(q2, mul_rn(y.y, x.y));
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < kStepE; ++k) q0 = add_rn(q0, mul_rn(wv[k], wv[k]));
+    }
+    p[0] = q0;
+    p[1] = q1;
+    p[2] = q2;
+  }
+  double pn[1] = {p[0]};
+  ll_allreduce<1>(pn, a.board, call, sh);
+  const double hnorm = sqrt(pn[0]);
+  k4_mark_raw(a.trace, a.trace_cap);
+  step_givens(a, st, j, hnorm, hcol, cs_s, sn_s, gj_s, est_s, brk_s);
   __syncthreads();
   if (brk_s == 0) {  // V_{j+1} = w / hnorm: the next K3 launch's input, keep it in L2
     double* Vnew = a.V + (int64_t)(j + 1) * ldv + s_lo;
@@ -336,13 +678,14 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_cycle_start(StepArgs a) 
 }
 
 bool stepped_gmres_fits(int64_t n, int sms) {
-  return (n + sms - 1) / sms + 2 <= (int64_t)kStepWorkers * kStepE;
+  const int64_t workers = sms - 1;  // CTA 0 is the all-reduce's reducer
+  return sms >= 2 && sms <= 32 * kLLChunks && (n + workers - 1) / workers + 2 <= (int64_t)kStepWorkers * kStepE;
 }
 
 int64_t stepped_gmres_workspace(int64_t n, int blocks) {
   const int64_t ldv = (n + 1) & ~(int64_t)1;
   return (int64_t)(R + 1) * ldv + 2 * n + 2 + 2 * kPartStride * (int64_t)blocks + 64 +
-         (int64_t)(sizeof(StepState) + 7) / 8;
+         (((int64_t)(sizeof(StepState) + 7) / 8 + 1) & ~(int64_t)1) + ll_board_words(blocks);
 }
 
 // Host loop (inner.py:229-283).  `op` is the planned K3 operator of P_pi.
@@ -373,18 +716,34 @@ int stepped_gmres(const ipi_op* op, int64_t n, const double* b, double* x, doubl
   a.partials = a.r + n;
   a.bar = reinterpret_cast<unsigned*>(a.partials + 2 * kPartStride * (int64_t)blocks);
   a.s = reinterpret_cast<StepState*>(a.partials + 2 * kPartStride * (int64_t)blocks + 64);
+  a.board = reinterpret_cast<unsigned long long*>(
+      reinterpret_cast<double*>(a.s) + (((int64_t)(sizeof(StepState) + 7) / 8 + 1) & ~(int64_t)1));
+  a.call_base = 0;
+  static const int pf_env = getenv("IPI_STEP_PF") ? atoi(getenv("IPI_STEP_PF")) : 4;
+  a.pf = std::min(std::max(pf_env, 0), 32);
+  static const int dbg_env = getenv("IPI_STEP_DBG") ? atoi(getenv("IPI_STEP_DBG")) : 0;
+  a.dbg = dbg_env;
+  static const int prof_env = getenv("IPI_STEP_PROF") ? atoi(getenv("IPI_STEP_PROF")) : 0;
+  if (prof_env) {
+    IPI_CUDA_TRY(cudaMalloc(&a.prof, 64 * sizeof(long long)));
+    IPI_CUDA_TRY(cudaMemsetAsync(a.prof, 0, 64 * sizeof(long long), st));
+  }
   a.invd = inv_diag;
   a.hf = hf_dev;
   a.max_it = max_it;
   a.trace = k4_trace_buffer(&a.trace_cap);
   if (a.trace) IPI_CUDA_TRY(cudaMemsetAsync(a.trace, 0, sizeof(unsigned long long), st));
   IPI_CUDA_TRY(cudaMemsetAsync(a.bar, 0, 2 * sizeof(unsigned), st));
+  IPI_CUDA_TRY(cudaMemsetAsync(a.board, 0, ll_board_words(blocks) * sizeof(unsigned long long), st));
   {
     StepState init{};
     init.target = target;
     IPI_CUDA_TRY(cudaMemcpyAsync(a.s, &init, sizeof(init), cudaMemcpyHostToDevice, st));
   }
   const int* active = &a.s->active;
+  // IPI_STEP_PAIR=0: one basis vector per grid exchange (bitwise MGS) instead of the pair-blocked kernel
+  static const int pair = getenv("IPI_STEP_PAIR") ? atoi(getenv("IPI_STEP_PAIR")) : 1;
+  if (pair) IPI_CUDA_TRY(raise_smem_limit(step_ortho_pair, kPairSmem));
   {
     int per_sm = 0;
     IPI_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_ortho, kStepThreads, 0));
@@ -431,7 +790,8 @@ int stepped_gmres(const ipi_op* op, int64_t n, const double* b, double* x, doubl
     auto issue = [&]() -> int {
       int e;
       if ((e = op_launch(op, a.V + (int64_t)issued * a.ldv, nullptr, 1, a.w, st, nullptr, active))) return e;
-      if ((e = coop((const void*)step_ortho))) return e;
+      if ((e = pair ? coop((const void*)step_ortho_pair, kPairSmem) : coop((const void*)step_ortho))) return e;
+      a.call_base += R + 2;  // a launch makes at most R + 1 calls
       IPI_CUDA_TRY(cudaEventRecord(ev[issued & 1], st));
       ++issued;
       return IPI_OK;
@@ -469,6 +829,14 @@ int stepped_gmres(const ipi_op* op, int64_t n, const double* b, double* x, doubl
   rep.converged = fin.rn <= fin.eff ? 1 : 0;
   rep.breakdown = 0;
   rep.basis_reads = fin.basis_reads;
+  if (a.prof) {
+    long long h[8] = {};
+    cudaMemcpy(h, a.prof, sizeof(h), cudaMemcpyDeviceToHost);
+    cudaFree(a.prof);
+    const double c = h[3] ? (double)h[3] : 1.0;
+    fprintf(stderr, "[step prof] CTA 1, %lld MGS passes: all-reduce (a worker's view) %.0f, whole pass %.0f cycles\n",
+            h[3], h[4] / c, h[5] / c);
+  }
   rep.target_2norm = fin.eff;
   IPI_CUDA_TRY(cudaMemcpyAsync(d_report, &rep, sizeof(rep), cudaMemcpyHostToDevice, st));
   IPI_CUDA_TRY(cudaStreamSynchronize(st));

@@ -32,19 +32,22 @@ __device__ __forceinline__ bool ll_try(const unsigned long long* src, unsigned c
 
 template <int MODE, int NCOPY>
 __global__ void __launch_bounds__(512, 1) k(double* partials, unsigned* ctr, unsigned long long* mb,
-                                            unsigned long long* pub, int iters, double* out) {
+                                            unsigned long long* pub, int iters, double* out, long long* prof) {
   __shared__ double red[32];
+  long long c_red = 0, c_comm = 0, c_bc = 0;
   __shared__ double bc;
   const int nb = gridDim.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   double acc = threadIdx.x * 1e-3 + blockIdx.x;
   unsigned call = 0;
   for (int it = 0; it < iters; ++it) {
     ++call;
+    const long long t0 = clock64();
     double t = warp_sum(acc);
     if (lane == 0) red[warp] = t;
     __syncthreads();
     if (warp == 0) {
       t = warp_sum(lane < nw ? red[lane] : 0.0);
+      const long long t1 = clock64();
       if (MODE == 0) {
         if (lane == 0) {
           partials[(it & 1) * nb + blockIdx.x] = t;
@@ -99,22 +102,25 @@ __global__ void __launch_bounds__(512, 1) k(double* partials, unsigned* ctr, uns
           if (lane == 0) bc = s;
         }
       }
+      const long long t2 = clock64();
+      c_red += t1 - t0; c_comm += t2 - t1;
     }
     __syncthreads();
     acc = __dadd_rn(acc, bc * 1e-30);
   }
   if (threadIdx.x == 0 && blockIdx.x == 1) out[MODE] = acc;
+  if (threadIdx.x == 0 && blockIdx.x < 2) { prof[blockIdx.x * 2] = c_red; prof[blockIdx.x * 2 + 1] = c_comm; }
 }
 
 template <int MODE, int NCOPY>
 void run(int sms, int threads, double* partials, unsigned* ctr, unsigned long long* mb,
-         unsigned long long* pub, double* out) {
+         unsigned long long* pub, double* out, long long* prof) {
   const int iters = 4000;
   for (int rep = 0; rep < 2; ++rep) {
     cudaMemset(ctr, 0, 4096);
     cudaMemset(mb, 0, 16 * 1024);
     cudaMemset(pub, 0, 16 * 1024);
-    void* args[] = {&partials, &ctr, &mb, &pub, (void*)&iters, &out};
+    void* args[] = {&partials, &ctr, &mb, &pub, (void*)&iters, &out, &prof};
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
@@ -126,6 +132,8 @@ void run(int sms, int threads, double* partials, unsigned* ctr, unsigned long lo
     cudaEventElapsedTime(&ms, a, b);
     double h[4] = {};
     cudaMemcpy(h, out, sizeof(h), cudaMemcpyDeviceToHost);
+    long long hp[4]; cudaMemcpy(hp, prof, sizeof(hp), cudaMemcpyDeviceToHost);
+    if (rep) printf("   cycles/call: cta0 reduce %lld comm %lld | cta1 reduce %lld comm %lld\n", hp[0]/iters, hp[1]/iters, hp[2]/iters, hp[3]/iters);
     if (rep)
       printf("mode %d ncopy %2d threads %4d: %.3f us per all-reduce (%s) check %.17g\n", MODE, NCOPY, threads,
              ms * 1e3 / iters, cudaGetErrorString(e), h[MODE]);
@@ -143,12 +151,12 @@ int main() {
   cudaMalloc(&pub, 16 * 1024);
   cudaMalloc(&out, 64);
   cudaMalloc(&ctr, 4096);
-  for (int threads : {512, 128}) {
-    run<0, 1>(sms, threads, partials, ctr, mb, pub, out);
-    run<1, 1>(sms, threads, partials, ctr, mb, pub, out);
-    run<1, 4>(sms, threads, partials, ctr, mb, pub, out);
-    run<1, 16>(sms, threads, partials, ctr, mb, pub, out);
-    run<1, 32>(sms, threads, partials, ctr, mb, pub, out);
+  long long* prof; cudaMalloc(&prof, 64);
+  for (int nb : {2, 8, 32, 74, 148}) {
+    printf("--- %d CTAs\n", nb);
+    run<0, 1>(nb, 512, partials, ctr, mb, pub, out, prof);
+    run<1, 1>(nb, 512, partials, ctr, mb, pub, out, prof);
+    run<1, 16>(nb, 512, partials, ctr, mb, pub, out, prof);
   }
   return 0;
 }
