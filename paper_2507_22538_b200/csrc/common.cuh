@@ -203,6 +203,17 @@ __device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
+// Programmatic dependent launch (PDL): a kernel launched with the
+// programmatic-stream-serialization attribute may start while its predecessor
+// in the stream is still running; griddep_wait() blocks until the predecessor
+// has completed and its writes are visible (a no-op for a normal launch), and
+// griddep_launch_dependents() lets the successor's CTAs be scheduled as soon
+// as every CTA of this grid has called it (or exited).
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // Register batch of P value pairs + column pairs (uniform-row fast paths).
 template <int P>
 struct Batch {

@@ -132,7 +132,8 @@ int k3_uring_smem(int K, int stages, int warps, int window_bytes);
 int k3_flat_smem(int K, int stages, int warps, int window_bytes);
 bool k3_shape_prepare(int variant, int K, int NW, int S, bool win, int smem);
 int op_launch(const ipi_op* op, const double* x_full, const double* b, int epi, double* y,
-              cudaStream_t st, const double* y_partial = nullptr, const int* active = nullptr);
+              cudaStream_t st, const double* y_partial = nullptr, const int* active = nullptr,
+              int pdl = 0);
 
 // krylov.cu
 int inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi, int64_t n,

@@ -67,8 +67,7 @@ struct StepArgs {
   unsigned long long* board;  // LL all-reduce mailboxes + result slots (ll_allreduce)
   unsigned call_base;         // first LL call number of this launch (unique per launch)
   int pf;                     // step_ortho: basis vectors prefetched into L2 ahead of the MGS pass
-  long long* prof;            // diagnostics (IPI_STEP_PROF=1): cycle counters of CTA 1, or nullptr
-  int dbg;                    // timing experiments (IPI_STEP_DBG): 1 = skip the basis loads (wrong results)
+  int pdl;                    // step_ortho*: launched with programmatic stream serialization
 };
 
 constexpr int kStepThreads = 512;
@@ -311,6 +310,10 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_ortho(StepArgs a) {
   __shared__ int brk_s;
   StepState* st = a.s;
   const int tid = threadIdx.x;
+  if (a.pdl) {
+    griddep_wait();
+    griddep_launch_dependents();
+  }
   // the next cooperative launch's barrier counter (its previous user, two
   // launches back, has retired); reset even when this launch is a no-op
   if (blockIdx.x == 0 && tid == 0) a.bar[a.parity ^ 1] = 0u;
@@ -358,7 +361,6 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_ortho(StepArgs a) {
 #pragma unroll
   for (int k = 0; k < kStepE; ++k) p[0] = add_rn(p[0], mul_rn(vc[k], wv[k]));
   for (int l = 0; l <= j; ++l) {
-    const long long pc0 = a.prof ? clock64() : 0;
     ll_post<1>(p, a.board, call, sh);
     double vn[kStepE];
     if (l < j) {  // V_{l+1} in flight while h_l is reduced
@@ -367,13 +369,12 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_ortho(StepArgs a) {
 #pragma unroll
       for (int k = 0; k < kStepE; ++k) {
         const int64_t e = elem(k);
-        vn[k] = e < own && !(a.dbg & 1) ? ld_hint(Vn + e, pol) : 0.0;
+        vn[k] = e < own ? ld_hint(Vn + e, pol) : 0.0;
       }
     }
     if (tid == 0 && l + 1 + a.pf <= j && pf_bytes)
       l2_prefetch(a.V + (int64_t)(l + 1 + a.pf) * ldv + s_lo, pf_bytes);
     ll_wait_result<1>(p, a.board, call, sh);
-    if (a.prof && blockIdx.x == 1 && tid == 32) a.prof[4] += clock64() - pc0;  // a worker's whole call
     const double h = p[0];
     if (tid == 0) hcol[l] = h;
     double q = 0.0;
@@ -390,10 +391,6 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_ortho(StepArgs a) {
       for (int k = 0; k < kStepE; ++k) q = add_rn(q, mul_rn(wv[k], wv[k]));
     }
     p[0] = q;
-    if (a.prof && blockIdx.x == 1 && tid == 32) {
-      a.prof[5] += clock64() - pc0;  // whole pass
-      a.prof[3] += 1;
-    }
   }
   ll_allreduce<1>(p, a.board, call, sh);
   const double hnorm = sqrt(p[0]);
@@ -420,7 +417,9 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_ortho(StepArgs a) {
 // correction for a basis that has lost orthogonality (G is the measured
 // inner product, ~1e-16 here, not assumed zero).  w is then updated as MGS
 // does, (w - h_l V_l) - h_{l+1} V_{l+1}.  h_l is bitwise MGS's; h_{l+1}
-// differs from it by rounding of order eps |w|.
+// differs from it by rounding of order eps |w|.  The inner products use fused
+// multiply-adds (the reference's are BLAS dots, whose rounding order is not
+// specified either); the w updates keep numpy's separate mul / sub roundings.
 //
 // Data movement: the pair in use lives in registers (va, vb); the next pair is
 // copied into shared memory with cp.async (16-byte chunks, every thread copies
@@ -440,6 +439,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_ortho_pair(StepArgs a) {
   const int tid = threadIdx.x;
   if (blockIdx.x == 0 && tid == 0) a.bar[a.parity ^ 1] = 0u;
   if (!st->active) return;  // uniform: the previous launch ended the cycle
+  if (a.pdl) griddep_launch_dependents();  // the next K3 launch may stage its first P_pi rows
   k4_mark_raw(a.trace, a.trace_cap);
   unsigned call = a.call_base;
   const int j = st->j;
@@ -484,28 +484,39 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_ortho_pair(StepArgs a) {
   auto staged = [&](int v, int c) -> double2 {
     return *reinterpret_cast<const double2*>(stage_raw + slot(v, c));
   };
+  // The basis and the solver state were written by launches that finished
+  // before the K3 launch ahead of this one started: under programmatic
+  // dependent launch they are read while that K3 launch drains; only w waits.
   double wv[kStepE], va[kStepE], vb[kStepE];
 #pragma unroll
   for (int k = 0; k < kStepE; ++k) {
     const int64_t e = elem(k);
-    double wi = 0.0, v0 = 0.0, v1 = 0.0;
+    double v0 = 0.0, v1 = 0.0;
     if (e < own) {
-      wi = a.w[s_lo + e];
-      if (a.invd) wi = mul_rn(wi, a.invd[s_lo + e]);  // w = pc(A v_j)  (inner.py:249)
       v0 = ld_hint(a.V + s_lo + e, j > 0 ? pol_keep : pol_first);
       if (j >= 1) v1 = ld_hint(a.V + ldv + s_lo + e, j > 1 ? pol_keep : pol_first);
     }
-    wv[k] = wi;
     va[k] = v0;
     vb[k] = v1;
   }
   if (j >= 2) stage_pair(2);
+  if (a.pdl) griddep_wait();
+#pragma unroll
+  for (int k = 0; k < kStepE; ++k) {
+    const int64_t e = elem(k);
+    double wi = 0.0;
+    if (e < own) {
+      wi = a.w[s_lo + e];
+      if (a.invd) wi = mul_rn(wi, a.invd[s_lo + e]);  // w = pc(A v_j)  (inner.py:249)
+    }
+    wv[k] = wi;
+  }
   double p[3] = {0.0, 0.0, 0.0};
 #pragma unroll
   for (int k = 0; k < kStepE; ++k) {
-    p[0] = add_rn(p[0], mul_rn(va[k], wv[k]));
-    p[1] = add_rn(p[1], mul_rn(vb[k], wv[k]));
-    p[2] = add_rn(p[2], mul_rn(vb[k], va[k]));
+    p[0] = fma(va[k], wv[k], p[0]);
+    p[1] = fma(vb[k], wv[k], p[1]);
+    p[2] = fma(vb[k], va[k], p[2]);
   }
   for (int l = 0; l <= j; l += 2) {
     const bool two = l + 1 <= j, more = l + 2 <= j;
@@ -547,16 +558,16 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_ortho_pair(StepArgs a) {
         const double2 x = ok ? staged(0, c) : make_double2(0.0, 0.0);
         const double2 y = ok && two_n ? staged(1, c) : make_double2(0.0, 0.0);
         // a chunk's second half is zero-filled past the slice end (8-byte copy)
-        q0 = add_rn(q0, mul_rn(x.x, wv[2 * c]));
-        q0 = add_rn(q0, mul_rn(x.y, wv[2 * c + 1]));
-        q1 = add_rn(q1, mul_rn(y.x, wv[2 * c]));
-        q1 = add_rn(q1, mul_rn(y.y, wv[2 * c + 1]));
-        q2 = add_rn(q2, mul_rn(y.x, x.x));
-        q2 = add_rn(q2, mul_rn(y.y, x.y));
+        q0 = fma(x.x, wv[2 * c], q0);
+        q0 = fma(x.y, wv[2 * c + 1], q0);
+        q1 = fma(y.x, wv[2 * c], q1);
+        q1 = fma(y.y, wv[2 * c + 1], q1);
+        q2 = fma(y.x, x.x, q2);
+        q2 = fma(y.y, x.y, q2);
       }
     } else {
 #pragma unroll
-      for (int k = 0; k < kStepE; ++k) q0 = add_rn(q0, mul_rn(wv[k], wv[k]));
+      for (int k = 0; k < kStepE; ++k) q0 = fma(wv[k], wv[k], q0);
     }
     p[0] = q0;
     p[1] = q1;
@@ -721,13 +732,6 @@ int stepped_gmres(const ipi_op* op, int64_t n, const double* b, double* x, doubl
   a.call_base = 0;
   static const int pf_env = getenv("IPI_STEP_PF") ? atoi(getenv("IPI_STEP_PF")) : 4;
   a.pf = std::min(std::max(pf_env, 0), 32);
-  static const int dbg_env = getenv("IPI_STEP_DBG") ? atoi(getenv("IPI_STEP_DBG")) : 0;
-  a.dbg = dbg_env;
-  static const int prof_env = getenv("IPI_STEP_PROF") ? atoi(getenv("IPI_STEP_PROF")) : 0;
-  if (prof_env) {
-    IPI_CUDA_TRY(cudaMalloc(&a.prof, 64 * sizeof(long long)));
-    IPI_CUDA_TRY(cudaMemsetAsync(a.prof, 0, 64 * sizeof(long long), st));
-  }
   a.invd = inv_diag;
   a.hf = hf_dev;
   a.max_it = max_it;
@@ -749,8 +753,33 @@ int stepped_gmres(const ipi_op* op, int64_t n, const double* b, double* x, doubl
     IPI_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_ortho, kStepThreads, 0));
     if (per_sm < 1) return fail(IPI_ECUDA, "step_ortho cannot be resident");
   }
-  auto coop = [&](const void* fn, int smem = 0) -> int {
+  // IPI_STEP_PDL=0: plain stream order between the K3 and step_ortho launches
+  static int pdl_ok = getenv("IPI_STEP_PDL") ? atoi(getenv("IPI_STEP_PDL")) : 1;
+  auto coop = [&](const void* fn, int smem = 0, bool pdl = false) -> int {
     void* args[] = {(void*)&a};
+    a.pdl = pdl && pdl_ok ? 1 : 0;
+    if (a.pdl) {
+      cudaLaunchAttribute attr[2];
+      attr[0].id = cudaLaunchAttributeCooperative;
+      attr[0].val.cooperative = 1;
+      attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[1].val.programmaticStreamSerializationAllowed = 1;
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(blocks);
+      cfg.blockDim = dim3(kStepThreads);
+      cfg.dynamicSmemBytes = (size_t)smem;
+      cfg.stream = st;
+      cfg.attrs = attr;
+      cfg.numAttrs = 2;
+      const cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
+      if (e == cudaSuccess) {
+        a.parity ^= 1;
+        return IPI_OK;
+      }
+      cudaGetLastError();  // the combination is refused: fall back to stream order for good
+      pdl_ok = 0;
+      a.pdl = 0;
+    }
     IPI_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(kStepThreads), args, (size_t)smem, st));
     a.parity ^= 1;
     return IPI_OK;
@@ -789,8 +818,9 @@ int stepped_gmres(const ipi_op* op, int64_t n, const double* b, double* x, doubl
     int issued = 0, waited = 0;
     auto issue = [&]() -> int {
       int e;
-      if ((e = op_launch(op, a.V + (int64_t)issued * a.ldv, nullptr, 1, a.w, st, nullptr, active))) return e;
-      if ((e = pair ? coop((const void*)step_ortho_pair, kPairSmem) : coop((const void*)step_ortho))) return e;
+      if ((e = op_launch(op, a.V + (int64_t)issued * a.ldv, nullptr, 1, a.w, st, nullptr, active, pdl_ok))) return e;
+      if ((e = pair ? coop((const void*)step_ortho_pair, kPairSmem, true) : coop((const void*)step_ortho, 0, true)))
+        return e;
       a.call_base += R + 2;  // a launch makes at most R + 1 calls
       IPI_CUDA_TRY(cudaEventRecord(ev[issued & 1], st));
       ++issued;
@@ -829,15 +859,6 @@ int stepped_gmres(const ipi_op* op, int64_t n, const double* b, double* x, doubl
   rep.converged = fin.rn <= fin.eff ? 1 : 0;
   rep.breakdown = 0;
   rep.basis_reads = fin.basis_reads;
-  if (a.prof) {
-    long long h[8] = {};
-    cudaMemcpy(h, a.prof, sizeof(h), cudaMemcpyDeviceToHost);
-    cudaFree(a.prof);
-    const double c = h[3] ? (double)h[3] : 1.0;
-    fprintf(stderr, "[step prof] CTA 1, %lld MGS passes: all-reduce (a worker's view) %.0f, whole pass %.0f cycles\n",
-            h[3], h[4] / c, h[5] / c);
-  }
-  rep.target_2norm = fin.eff;
   IPI_CUDA_TRY(cudaMemcpyAsync(d_report, &rep, sizeof(rep), cudaMemcpyHostToDevice, st));
   IPI_CUDA_TRY(cudaStreamSynchronize(st));
   return IPI_OK;

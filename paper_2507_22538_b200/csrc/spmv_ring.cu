@@ -46,6 +46,8 @@ struct K3Args {
   unsigned long long* trace;  // diagnostics: per-CTA (smid, start ns, end ns) or nullptr
   int interleave;  // uniform ring: warp w takes 4-row steps w, w+NW, ... of its CTA (else a contiguous range)
   const int* active;  // stepped GMRES (krylov_step.cu): skip the launch when *active == 0 (nullable)
+  int pdl;  // launched with programmatic stream serialization: x, b and *active are read only
+            // after griddep_wait(); the first ring stages (P_pi, never written here) go out before it
 };
 
 __device__ __forceinline__ unsigned long long k3_ns() {
@@ -128,7 +130,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k3_uring(K3Args a, int win_bytes) 
   using L = K3URing<K>;
   constexpr bool NEED_B = EPI >= 2, NEED_XD = EPI == 1 || EPI == 2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  if (a.active && *a.active == 0) return;  // stepped GMRES: the cycle already ended
+  const bool early = a.pdl && !WIN && !NEED_B;  // prologue before the predecessor has finished
+  if (a.pdl && !early) griddep_wait();
+  if (!early && a.active && *a.active == 0) return;  // stepped GMRES: the cycle already ended
   k3_trace_begin(a);
   double* win = reinterpret_cast<double*>(smem_raw);
   const int64_t r_lo = k3_split(a.rows, blockIdx.x, gridDim.x, 4);
@@ -257,6 +261,14 @@ __global__ void __launch_bounds__(NW * 32, 1) k3_uring(K3Args a, int win_bytes) 
   if (WIN) k3_window_issue(a, smem_raw, r_lo, r_hi, w_lo, w_len);
 #pragma unroll 1
   for (int q = 0; q < S; ++q) issue(q, q);
+  if (early) {  // P_pi's first stages are in flight; x and *active need the predecessor
+    griddep_wait();
+    if (a.active && *a.active == 0) {
+      cp_async_wait<0>();
+      return;
+    }
+  }
+  if (a.pdl) griddep_launch_dependents();
   if (WIN) {
     cp_async_wait<S>();  // the window group landed (this thread's copies)
     __syncthreads();     // ... and every thread's
@@ -298,6 +310,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k3_flat(K3Args a, int win_bytes) {
   static_assert(K == 2 || K == 4, "flat ring handles K = 2 or 4");
   static_assert(S >= 4, "ring needs 4 stages (gathers two batches ahead)");
   using L = K3Flat<K>;
+  if (a.pdl) {
+    griddep_wait();
+    griddep_launch_dependents();
+  }
   constexpr bool NEED_B = EPI >= 2, NEED_XD = EPI == 1 || EPI == 2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   if (a.active && *a.active == 0) return;  // stepped GMRES: the cycle already ended
@@ -468,6 +484,21 @@ bool k3_shape_prepare(int variant, int K, int NW, int S, bool win, int smem) {
   return ok && e == cudaSuccess;
 }
 
+template <class Kern>
+static void k3_go(Kern kern, const ipi_op* op, int threads, const K3Args& a, int wb, cudaStream_t st) {
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(op->blocks);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = (size_t)op->smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = a.pdl ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, a, wb);
+}
+
 template <int EPI>
 static bool k3_launch_epi(const ipi_op* op, const K3Args& a, cudaStream_t st) {
   bool ok = false;
@@ -476,14 +507,14 @@ static bool k3_launch_epi(const ipi_op* op, const K3Args& a, cudaStream_t st) {
 #define IPI_K3U_GO(KK, WW, SS)                                                                   \
   if (!ok && op->variant == IPI_K3_URING && op->K == KK && op->warps == WW && op->stages == SS) { \
     ok = true;                                                                                   \
-    if (win) k3_uring<KK, WW, SS, EPI, true><<<op->blocks, WW * 32, op->smem, st>>>(a, wb);       \
-    else k3_uring<KK, WW, SS, EPI, false><<<op->blocks, WW * 32, op->smem, st>>>(a, 0);           \
+    if (win) k3_go(k3_uring<KK, WW, SS, EPI, true>, op, WW * 32, a, wb, st);                      \
+    else k3_go(k3_uring<KK, WW, SS, EPI, false>, op, WW * 32, a, 0, st);                          \
   }
 #define IPI_K3F_GO(KK, WW, SS)                                                                  \
   if (!ok && op->variant == IPI_K3_FLAT && op->K == KK && op->warps == WW && op->stages == SS) { \
     ok = true;                                                                                  \
-    if (win) k3_flat<KK, WW, SS, EPI, true><<<op->blocks, WW * 32, op->smem, st>>>(a, wb);       \
-    else k3_flat<KK, WW, SS, EPI, false><<<op->blocks, WW * 32, op->smem, st>>>(a, 0);           \
+    if (win) k3_go(k3_flat<KK, WW, SS, EPI, true>, op, WW * 32, a, wb, st);                      \
+    else k3_go(k3_flat<KK, WW, SS, EPI, false>, op, WW * 32, a, 0, st);                          \
   }
   IPI_K3U_SHAPES(IPI_K3U_GO)
   IPI_K3F_SHAPES(IPI_K3F_GO)
@@ -494,13 +525,13 @@ static bool k3_launch_epi(const ipi_op* op, const K3Args& a, cudaStream_t st) {
 
 // y = epi(P x) over the operator's rows; generic rows use spmv.cu's kernel.
 int op_launch(const ipi_op* op, const double* x_full, const double* b, int epi, double* y,
-              cudaStream_t st, const double* y_partial, const int* active) {
+              cudaStream_t st, const double* y_partial, const int* active, int pdl) {
   if (op->n_local <= 0) return IPI_OK;
   if (op->variant == IPI_K3_GENERIC || epi >= 4)  // split halves: generic rows
     return launch_spmv(op->rp, op->col, op->val, op->n_local, x_full, b, op->gamma, epi, y,
                        op->lanes, st, op->state0, y_partial);
   K3Args a{op->col, op->val, op->n_local, op->state0, op->n_global, x_full, b, op->gamma, y, op->halo,
-            op->pf, op->trace, op->interleave, active};
+            op->pf, op->trace, op->interleave, active, pdl};
   bool ok = false;
   switch (epi) {
     case 0: ok = k3_launch_epi<0>(op, a, st); break;
