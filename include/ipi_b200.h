@@ -323,7 +323,9 @@ int ipi_solve_sharded(ipi_mdp* h, const ipi_comm* comm, const ipi_opts* opts, do
                       void* stream);
 
 /* Solve (I - gamma P_pi) x = b from x (in/out) to the floored 2-norm target
- * or max_it iterations, one persistent cooperative kernel per call.
+ * or max_it iterations, device-resident: one persistent cooperative kernel
+ * per call, or (GMRES/MGS on large uniform K = 64-class rows) the stepped
+ * solver of krylov_step.cu, two launches per Arnoldi step.
  * inv_diag == NULL: pc = identity; else left Jacobi preconditioning.
  * ortho: IPI_ORTHO_* (GMRES only).  The Krylov workspace is one arena per
  * (device, stream): concurrent calls must use different streams. */
