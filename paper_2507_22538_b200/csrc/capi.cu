@@ -904,6 +904,8 @@ int ipi_solve(ipi_mdp* h, const ipi_opts* o, double* v, int32_t* policy, double*
   double* vcur = v;
   double* vnext = h->xbuf;
   bool pending_report = false;
+  // IPI_R0_FROM_TV=0: every inner solve recomputes its initial residual by an SpMV
+  static const bool r0_from_tv = !(getenv("IPI_R0_FROM_TV") && getenv("IPI_R0_FROM_TV")[0] == '0');
   while (true) {
     cudaEventRecord(g0, st);
     IPI_CUDA_TRY(cudaMemsetAsync(h->res_bits, 0, sizeof(unsigned long long), st));
@@ -974,7 +976,9 @@ int ipi_solve(ipi_mdp* h, const ipi_opts* o, double* v, int32_t* policy, double*
                      h->plan.uniform_rows ? h->plan.row_len_max : 0, h->d_report, st, h->kry,
                      h->kry_len, o->pc_type == IPI_PC_JACOBI ? h->invd : nullptr,
                      (12.0 * h->plan.row_len_mean + 8.0) * (double)n,  // P_pi size estimate
-                     o->gmres_ortho, h->op_pi, h->plan.contiguous_rows);
+                     o->gmres_ortho, h->op_pi, h->plan.contiguous_rows,
+                     // K1 has just produced TV = g_pi + gamma P_pi V for this policy and this V
+                     r0_from_tv ? h->applied : nullptr);
     if (rc) return rc;
     if (o->ksp_type == IPI_KSP_TFQMR || o->ksp_type == IPI_KSP_BICGSTAB) {
       // these kinds can break down: read the report now (driver.py:189-193)

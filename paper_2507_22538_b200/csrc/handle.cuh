@@ -144,13 +144,15 @@ int inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_p
                 double pi_bytes = 0.0,   // bytes of P_pi (L2-residency choice; <= 0: read nnz)
                 int ortho = IPI_ORTHO_AUTO,
                 const ipi_op* op = nullptr,   // planned K3 operator of P_pi: stepped GMRES
-                int contig = 0);              // P_pi rows have consecutive columns
+                int contig = 0,               // P_pi rows have consecutive columns
+                const double* tv = nullptr);  // b + gamma P_pi x0 when the caller already has it
+                                              // (K1's TV in the outer loop): r0 = tv - x0
 // krylov_step.cu
 bool stepped_gmres_fits(int64_t n, int sms);
 int64_t stepped_gmres_workspace(int64_t n, int blocks);
 int stepped_gmres(const ipi_op* op, int64_t n, const double* b, double* x, double target,
                   int32_t max_it, const double* inv_diag, ipi_inner_report* d_report,
-                  double* ws, int64_t ws_doubles, cudaStream_t st);
+                  double* ws, int64_t ws_doubles, cudaStream_t st, const double* tv = nullptr);
 // Jacobi: inv_diag[s] = 1 / (1 - gamma * P_pi[s, s])  (inner.py:115-118)
 int jacobi_inv_diag(const int64_t* rp_pi, const int32_t* col_pi, const double* val_pi, int64_t n,
                     double gamma, double* inv_diag, cudaStream_t st, int64_t state0 = 0);

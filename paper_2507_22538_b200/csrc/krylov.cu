@@ -98,7 +98,7 @@ int inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_p
                 int32_t kind, double scale, int lanes, int halo, int uniform_K,
                 ipi_inner_report* d_report, cudaStream_t st, double* workspace,
                 int64_t workspace_doubles, const double* inv_diag, double pi_bytes, int ortho,
-                const ipi_op* op, int contig) {
+                const ipi_op* op, int contig, const double* tv) {
   if (kind < IPI_KSP_RICHARDSON || kind > IPI_KSP_TFQMR)
     return fail(IPI_EVALIDATION, "unknown inner solver kind " + std::to_string(kind));
   if (max_it < 1) return fail(IPI_EVALIDATION, "iteration cap must be >= 1, got " + std::to_string(max_it));
@@ -182,7 +182,7 @@ int inner_solve(const int64_t* rp_pi, const int32_t* col_pi, const double* val_p
     double* sws = (workspace && workspace_doubles >= sneed) ? workspace : krylov_workspace(sneed, st);
     if (!sws) return fail(IPI_ERESOURCE, "cannot allocate the stepped GMRES workspace");
     return stepped_gmres(op, n, b, x, target, max_it, inv_diag, d_report, sws,
-                         sws == workspace ? workspace_doubles : sneed, st);
+                         sws == workspace ? workspace_doubles : sneed, st, tv);
   }
   // Uniform K = 64-class rows with GMRES/CGS2 or Richardson: the ring kernel
   // (krylov_ring.cu).  IPI_K4_RING=0 keeps the 1024-thread kernel;

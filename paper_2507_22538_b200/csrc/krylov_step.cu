@@ -62,6 +62,7 @@ struct StepArgs {
   StepFlags* hf;  // host-mapped (device pointer)
   int max_it;
   int first;  // step_cycle_start: first call of the solve
+  const double* tv;  // first call: r = tv - x instead of reading a.r (the caller's b + gamma P x), or nullptr
   unsigned long long* trace;  // diagnostics (ipi_k4_trace): step_ortho start / MGS done / end
   int trace_cap;
   unsigned long long* board;  // LL all-reduce mailboxes + result slots (ll_allreduce)
@@ -144,6 +145,20 @@ int64_t ll_board_words(int blocks) { return 2 * ((int64_t)kLLVals * blocks + kLL
 // sh.bc.  (With the loads issued before a blocking barrier the workers only
 // reached it after the load queue had drained: +0.8 us per MGS pass.)
 constexpr int kBarPosted = 1, kBarResult = 2, kBarGo = 3;
+
+// NV warp sums with their shuffle levels interleaved (independent chains: the
+// latency of one level is paid once, not NV times); same xor tree as warp_sum.
+template <int NV>
+__device__ __forceinline__ void warp_sum_n(double (&t)[NV]) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    double o[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) o[k] = __shfl_xor_sync(kFull, t[k], off);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) t[k] = add_rn(t[k], o[k]);
+  }
+}
 __device__ __forceinline__ void bar_arrive(int id, int count) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
@@ -166,7 +181,8 @@ __device__ __forceinline__ void ll_post(const double (&v)[NV], unsigned long lon
     if (warp != 0) {
       double t[NV];
 #pragma unroll
-      for (int k = 0; k < NV; ++k) t[k] = warp_sum(v[k]);
+      for (int k = 0; k < NV; ++k) t[k] = v[k];
+      warp_sum_n<NV>(t);
       if (lane == 0) {
 #pragma unroll
         for (int k = 0; k < NV; ++k) sh.red[k * 32 + warp] = t[k];
@@ -178,11 +194,14 @@ __device__ __forceinline__ void ll_post(const double (&v)[NV], unsigned long lon
     } else {
       bar_sync(kBarPosted, nthr);
       const int nw = nthr >> 5;
+      double t[NV];
 #pragma unroll
-      for (int k = 0; k < NV; ++k) {  // warp 0 holds no elements: lanes 1.. carry the workers
-        const double tk = warp_sum(lane >= 1 && lane < nw ? sh.red[k * 32 + lane] : 0.0);
-        if (lane == k) ll_store(board + 2 * ((int64_t)k * nb + blockIdx.x), tk, call);
-      }
+      for (int k = 0; k < NV; ++k)  // warp 0 holds no elements: lanes 1.. carry the workers
+        t[k] = lane >= 1 && lane < nw ? sh.red[k * 32 + lane] : 0.0;
+      warp_sum_n<NV>(t);
+#pragma unroll
+      for (int k = 0; k < NV; ++k)
+        if (lane == k) ll_store(board + 2 * ((int64_t)k * nb + blockIdx.x), t[k], call);
       bar_arrive(kBarGo, nthr);
     }
   } else {
@@ -247,7 +266,8 @@ __device__ __forceinline__ void publish_flags(const StepArgs& a, const StepState
   f->it = s.it;
   f->done = s.done;
   f->rn = s.rn;
-  __threadfence_system();
+  // no system fence: the host reads the mirror only after synchronising on an
+  // event recorded behind this launch, which makes the kernel's writes visible
 }
 
 // Givens update of the new Hessenberg column (inner.py:256-270), run by
@@ -395,9 +415,11 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_ortho(StepArgs a) {
   ll_allreduce<1>(p, a.board, call, sh);
   const double hnorm = sqrt(p[0]);
   k4_mark_raw(a.trace, a.trace_cap);
-  step_givens(a, st, j, hnorm, hcol, cs_s, sn_s, gj_s, est_s, brk_s);
-  __syncthreads();
-  if (brk_s == 0) {  // V_{j+1} = w / hnorm: the next K3 launch's input, keep it in L2
+  // V_{j+1} = w / hnorm (the next K3 launch's input: keep it in L2) goes out
+  // while thread 0 runs the Givens update; when that update ends the cycle the
+  // vector is simply not used (slot j + 1 <= R exists).  hnorm == 0 is the
+  // breakdown case (inner.py:268-270): nothing is written.
+  if (hnorm != 0.0) {
     double* Vnew = a.V + (int64_t)(j + 1) * ldv + s_lo;
 #pragma unroll
     for (int k = 0; k < kStepE; ++k) {
@@ -405,6 +427,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_ortho(StepArgs a) {
       if (e < own) st_hint(Vnew + e, wv[k] / hnorm, pol_keep);
     }
   }
+  step_givens(a, st, j, hnorm, hcol, cs_s, sn_s, gj_s, est_s, brk_s);
   k4_mark_raw(a.trace, a.trace_cap);
 }
 
@@ -446,7 +469,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_ortho_pair(StepArgs a) {
   const int64_t n = a.n, ldv = a.ldv;
   int64_t s_lo, s_hi;
   ortho_slice(n, s_lo, s_hi);
-  const int64_t own = s_hi - s_lo;
+  const int own = (int)(s_hi - s_lo);  // <= kStepWorkers * kStepE: 32-bit slice indices
   const uint64_t pol_keep = policy_evict_last(), pol_first = policy_evict_first();
   if (tid == 0) {
     for (int l = 0; l < j; ++l) {
@@ -456,10 +479,10 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_ortho_pair(StepArgs a) {
     gj_s = st->g[j];
     est_s = st->est_target;
   }
-  const int64_t wt = tid - 32;  // worker index (< 0: the control warp owns nothing)
+  const int wt = tid - 32;  // worker index (< 0: the control warp owns nothing)
   // element k of this thread: chunk k/2 (16 bytes), half k%2
-  auto elem = [&](int k) -> int64_t {
-    return wt < 0 ? own : 2 * (wt + (int64_t)(k >> 1) * kStepWorkers) + (k & 1);
+  auto elem = [&](int k) -> int {
+    return wt < 0 ? own : 2 * (wt + (k >> 1) * kStepWorkers) + (k & 1);
   };
   const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(stage_raw);
   auto slot = [&](int v, int c) -> uint32_t {  // byte offset of chunk c of staged vector v
@@ -474,7 +497,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_ortho_pair(StepArgs a) {
         const uint64_t pol = l + v < j ? pol_keep : pol_first;
 #pragma unroll
         for (int c = 0; c < kPairChunks; ++c) {
-          const int64_t e = elem(2 * c);
+          const int e = elem(2 * c);
           if (e < own) cp_async16(stage_s + slot(v, c), Vl + e, e + 1 < own ? 16u : 8u, pol);
         }
       }
@@ -490,7 +513,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_ortho_pair(StepArgs a) {
   double wv[kStepE], va[kStepE], vb[kStepE];
 #pragma unroll
   for (int k = 0; k < kStepE; ++k) {
-    const int64_t e = elem(k);
+    const int e = elem(k);
     double v0 = 0.0, v1 = 0.0;
     if (e < own) {
       v0 = ld_hint(a.V + s_lo + e, j > 0 ? pol_keep : pol_first);
@@ -503,7 +526,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_ortho_pair(StepArgs a) {
   if (a.pdl) griddep_wait();
 #pragma unroll
   for (int k = 0; k < kStepE; ++k) {
-    const int64_t e = elem(k);
+    const int e = elem(k);
     double wi = 0.0;
     if (e < own) {
       wi = a.w[s_lo + e];
@@ -577,16 +600,19 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_ortho_pair(StepArgs a) {
   ll_allreduce<1>(pn, a.board, call, sh);
   const double hnorm = sqrt(pn[0]);
   k4_mark_raw(a.trace, a.trace_cap);
-  step_givens(a, st, j, hnorm, hcol, cs_s, sn_s, gj_s, est_s, brk_s);
-  __syncthreads();
-  if (brk_s == 0) {  // V_{j+1} = w / hnorm: the next K3 launch's input, keep it in L2
+  // V_{j+1} = w / hnorm (the next K3 launch's input: keep it in L2) goes out
+  // while thread 0 runs the Givens update; when that update ends the cycle the
+  // vector is simply not used (slot j + 1 <= R exists).  hnorm == 0 is the
+  // breakdown case (inner.py:268-270): nothing is written.
+  if (hnorm != 0.0) {
     double* Vnew = a.V + (int64_t)(j + 1) * ldv + s_lo;
 #pragma unroll
     for (int k = 0; k < kStepE; ++k) {
-      const int64_t e = elem(k);
+      const int e = elem(k);
       if (e < own) st_hint(Vnew + e, wv[k] / hnorm, pol_keep);
     }
   }
+  step_givens(a, st, j, hnorm, hcol, cs_s, sn_s, gj_s, est_s, brk_s);
   k4_mark_raw(a.trace, a.trace_cap);
 }
 
@@ -635,9 +661,14 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_cycle_start(StepArgs a) 
   const int first = a.first, it = first ? 0 : st->it, jprev = first ? 0 : st->j;
   const double gj = first ? 0.0 : fabs(st->g[jprev]);
   double eff = first ? 0.0 : st->eff, est_target = first ? 0.0 : st->est_target;
+  // r0 = (b + gamma P x0) - x0 when the caller already holds b + gamma P x0 (the
+  // outer loop's TV): the same residual as b - (x0 - gamma P x0) up to the
+  // rounding of the last two operations, and one SpMV less per inner solve
+  const bool from_tv = first && a.tv != nullptr;
+  auto resid = [&](int64_t i) -> double { return from_tv ? sub_rn(a.tv[i], a.x[i]) : a.r[i]; };
   double q[2] = {0.0, 0.0};
   for (int64_t i = s_lo + tid; i < s_hi; i += nthr) {
-    const double ri = a.r[i];
+    const double ri = resid(i);
     q[0] = add_rn(q[0], mul_rn(ri, ri));
     if (first) q[1] = add_rn(q[1], mul_rn(a.b[i], a.b[i]));
   }
@@ -656,7 +687,8 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_cycle_start(StepArgs a) 
   if (!done) {
     double z2[1] = {0.0};
     for (int64_t i = s_lo + tid; i < s_hi; i += nthr) {
-      const double z = a.invd ? mul_rn(a.r[i], a.invd[i]) : a.r[i];
+      const double ri = resid(i);
+      const double z = a.invd ? mul_rn(ri, a.invd[i]) : ri;
       a.V[i] = z;
       z2[0] = add_rn(z2[0], mul_rn(z, z));
     }
@@ -702,7 +734,7 @@ int64_t stepped_gmres_workspace(int64_t n, int blocks) {
 // Host loop (inner.py:229-283).  `op` is the planned K3 operator of P_pi.
 int stepped_gmres(const ipi_op* op, int64_t n, const double* b, double* x, double target,
                   int32_t max_it, const double* inv_diag, ipi_inner_report* d_report,
-                  double* ws, int64_t ws_doubles, cudaStream_t st) {
+                  double* ws, int64_t ws_doubles, cudaStream_t st, const double* tv) {
   int dev = 0, sms = 148;
   IPI_CUDA_TRY(cudaGetDevice(&dev));
   IPI_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -784,19 +816,15 @@ int stepped_gmres(const ipi_op* op, int64_t n, const double* b, double* x, doubl
     a.parity ^= 1;
     return IPI_OK;
   };
-  cudaEvent_t ev[2];
-  IPI_CUDA_TRY(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
-  if (cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming) != cudaSuccess) {
-    cudaEventDestroy(ev[0]);
-    return fail(IPI_ECUDA, "event create");
-  }
+  cudaEvent_t ev[3] = {};  // two step events (alternating) and the cycle-start event
   struct Guard {
     cudaEvent_t* e;
     ~Guard() {
-      cudaEventDestroy(e[0]);
-      cudaEventDestroy(e[1]);
+      for (int i = 0; i < 3; ++i)
+        if (e[i]) cudaEventDestroy(e[i]);
     }
   } guard{ev};
+  for (int i = 0; i < 3; ++i) IPI_CUDA_TRY(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
   auto read_flags = [&](StepFlags& f) {
     f.active = hf->active;
     f.j = hf->j;
@@ -805,28 +833,36 @@ int stepped_gmres(const ipi_op* op, int64_t n, const double* b, double* x, doubl
     f.rn = hf->rn;
   };
   int rc;
-  // r = b - A x, then ||r||, ||b||, eff, the first cycle's start
-  if ((rc = op_launch(op, x, b, 2, a.r, st))) return rc;
+  // r = b - A x (or tv - x), then ||r||, ||b||, eff, the first cycle's start
+  a.tv = tv;
+  if (!tv && (rc = op_launch(op, x, b, 2, a.r, st))) return rc;
   a.first = 1;
   if ((rc = coop((const void*)step_cycle_start))) return rc;
   a.first = 0;
-  IPI_CUDA_TRY(cudaStreamSynchronize(st));
+  a.tv = nullptr;
+  IPI_CUDA_TRY(cudaEventRecord(ev[2], st));
+  // Arnoldi steps, one enqueued ahead of the one the host waits for.  The first
+  // step of a cycle is enqueued right behind step_cycle_start, before the host
+  // knows whether the solve is done: a launched step skips itself when the
+  // device state says so, and the GPU has work while the host wakes up.
+  int issued = 0, waited = 0;
+  auto issue = [&]() -> int {
+    int e;
+    if ((e = op_launch(op, a.V + (int64_t)issued * a.ldv, nullptr, 1, a.w, st, nullptr, active, pdl_ok))) return e;
+    if ((e = pair ? coop((const void*)step_ortho_pair, kPairSmem, true) : coop((const void*)step_ortho, 0, true)))
+      return e;
+    a.call_base += R + 2;  // a launch makes at most R + 1 calls
+    IPI_CUDA_TRY(cudaEventRecord(ev[issued & 1], st));
+    ++issued;
+    return IPI_OK;
+  };
+  if ((rc = issue())) return rc;
+  IPI_CUDA_TRY(cudaEventSynchronize(ev[2]));  // step_cycle_start's flags; the speculative step runs on
   StepFlags f{};
   read_flags(f);
+  // f.done is set only by step_cycle_start (steps republish it unchanged); when
+  // it is set the speculative step is a no-op
   while (!f.done) {
-    // Arnoldi steps, one enqueued ahead of the one the host waits for
-    int issued = 0, waited = 0;
-    auto issue = [&]() -> int {
-      int e;
-      if ((e = op_launch(op, a.V + (int64_t)issued * a.ldv, nullptr, 1, a.w, st, nullptr, active, pdl_ok))) return e;
-      if ((e = pair ? coop((const void*)step_ortho_pair, kPairSmem, true) : coop((const void*)step_ortho, 0, true)))
-        return e;
-      a.call_base += R + 2;  // a launch makes at most R + 1 calls
-      IPI_CUDA_TRY(cudaEventRecord(ev[issued & 1], st));
-      ++issued;
-      return IPI_OK;
-    };
-    if ((rc = issue())) return rc;
     while (true) {
       // the host's view of the cycle: steps beyond j + 1 are launched only
       // while the device says the cycle is active
@@ -837,15 +873,18 @@ int stepped_gmres(const ipi_op* op, int64_t n, const double* b, double* x, doubl
       if (!f.active) break;  // steps already issued beyond it skip themselves
       if (waited >= issued) break;  // R steps issued and all done
     }
-    IPI_CUDA_TRY(cudaStreamSynchronize(st));  // the no-op tail step (if any) retired
-    read_flags(f);
+    // a no-op tail step (if any) changes nothing: the flags read above are the
+    // cycle's last, and the launches below follow it in stream order
     if (f.j == 0) break;  // inner.py:271-272
     // x += V y, r = b - A x, est_target / loop test / next cycle start
     step_cycle_end<<<blocks * 2, kStepThreads, 0, st>>>(a);
     IPI_LAUNCH_CHECK();
     if ((rc = op_launch(op, x, b, 2, a.r, st))) return rc;
     if ((rc = coop((const void*)step_cycle_start))) return rc;
-    IPI_CUDA_TRY(cudaStreamSynchronize(st));
+    IPI_CUDA_TRY(cudaEventRecord(ev[2], st));
+    issued = waited = 0;
+    if ((rc = issue())) return rc;  // speculative first step of the next cycle
+    IPI_CUDA_TRY(cudaEventSynchronize(ev[2]));
     read_flags(f);
   }
   ipi_inner_report rep{};
