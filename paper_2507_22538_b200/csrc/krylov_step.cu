@@ -447,9 +447,9 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_ortho(StepArgs a) {
 // Data movement: the pair in use lives in registers (va, vb); the next pair is
 // copied into shared memory with cp.async (16-byte chunks, every thread copies
 // exactly the elements it owns, so it waits only on its own groups) while the
-// exchange of the current pair is in flight.  The dots of the next pair read
-// shared memory directly (the LDS traffic hides under the FP64 pipe); the
-// register copy of that pair happens during its own exchange.
+// exchange of the current pair is in flight.  After the w update has released
+// va / vb, the dots of the next pair read the stage once and leave that pair
+// in the registers, so the stage is free again at the next exchange.
 constexpr int kPairChunks = kStepE / 2;                          // 16-byte chunks per thread and vector
 constexpr int kPairSmem = 2 * kPairChunks * kStepWorkers * 16;   // two vectors staged
 
@@ -544,21 +544,9 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_ortho_pair(StepArgs a) {
   for (int l = 0; l <= j; l += 2) {
     const bool two = l + 1 <= j, more = l + 2 <= j;
     ll_post<3>(p, a.board, call, sh);
-    if (l > 0) {
-      // the pair being exchanged moves from the stage to registers (its dots
-      // were taken from the stage), then the stage takes the next pair
-#pragma unroll
-      for (int c = 0; c < kPairChunks; ++c) {
-        const bool ok = elem(2 * c) < own;  // chunks past the slice were never staged
-        const double2 x = ok ? staged(0, c) : make_double2(0.0, 0.0);
-        const double2 y = ok && two ? staged(1, c) : make_double2(0.0, 0.0);
-        va[2 * c] = x.x;
-        va[2 * c + 1] = x.y;
-        vb[2 * c] = y.x;
-        vb[2 * c + 1] = y.y;
-      }
-      if (more) stage_pair(l + 2);
-    }
+    // the pair being exchanged is already in va / vb (the dots below left it
+    // there), so the stage is free: it takes the next pair during the exchange
+    if (l > 0 && more) stage_pair(l + 2);
     ll_wait_result<3>(p, a.board, call, sh);
     const double h0 = p[0];
     const double h1 = two ? sub_rn(p[1], mul_rn(h0, p[2])) : 0.0;
@@ -575,12 +563,18 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_ortho_pair(StepArgs a) {
     if (more) {
       const bool two_n = l + 3 <= j;
       cp_async_wait<0>();  // this thread's chunks of the next pair
+      // the update above released va / vb: the next pair moves into them here
 #pragma unroll
       for (int c = 0; c < kPairChunks; ++c) {
+        // chunks past the slice were never staged; a chunk's second half is
+        // zero-filled past the slice end (8-byte copy)
         const bool ok = elem(2 * c) < own;
         const double2 x = ok ? staged(0, c) : make_double2(0.0, 0.0);
         const double2 y = ok && two_n ? staged(1, c) : make_double2(0.0, 0.0);
-        // a chunk's second half is zero-filled past the slice end (8-byte copy)
+        va[2 * c] = x.x;
+        va[2 * c + 1] = x.y;
+        vb[2 * c] = y.x;
+        vb[2 * c + 1] = y.y;
         q0 = fma(x.x, wv[2 * c], q0);
         q0 = fma(x.y, wv[2 * c + 1], q0);
         q1 = fma(y.x, wv[2 * c], q1);
