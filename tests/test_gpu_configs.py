@@ -359,17 +359,19 @@ def test_c3_full_size_backup_and_evaluation():
 
 
 @pytest.mark.slow
-def test_c5_rank_block_backup_vs_c_oracle():
-    """BASELINE C5 (16.7M states, sharded-only): rank 0's row block at R = 8
+@pytest.mark.parametrize("rank", [0, 5, 7])
+def test_c5_rank_block_backup_vs_c_oracle(rank):
+    """BASELINE C5 (16.7M states, sharded-only): a rank's row block at R = 8
     (2,097,152 states x 16 actions x 64 nnz = 2^31 nnz, full-length V) — the
     per-rank Bellman backup against the C restatement of greedy_policy on the
-    same block (state0 = 0)."""
+    same block: rank 0 (state0 = 0), an interior rank (state0 = 10,485,760) and
+    the last rank (locality windows clipped at the upper end of the state space)."""
     import os
     from oracle import c_oracle as co
     from paper_2507_22538_b200.model import make_partition
     from paper_2507_22538_b200.parallel import MdpShard
     spec = gen.CONFIGS[5]
-    lo, hi = make_partition(spec.n, 8).block(0)
+    lo, hi = make_partition(spec.n, 8).block(rank)
     rp, col, val, cost = devgen.locality(spec.n, spec.m, spec.K, spec.window, 0, lo, hi - lo)
     sh = MdpShard(spec.n, spec.m, spec.gamma, lo, cost,
                   ipi.CsrMatrix((hi - lo) * spec.m, spec.n, rp, col, val))
