@@ -529,16 +529,26 @@ def run_ours(args):
                   "what": "policy-evaluation SpMV y = x - gamma*P_pi x (PolicyOperator.apply) on "
                           "P_pi of the greedy policy, x all-gathered"}
 
+    # The extra blocks of the N > 1 line never cost the headline: a failure in
+    # one of them (it would hit every rank alike: same code, same sizes) is
+    # reported in its place.
     ipi_sharded = None
     if world > 1 and not args.no_ipi:
-        from paper_2507_22538_b200.parallel import solve_sharded_native
-        opts = ipi.SolveOptions(alpha=spec.alpha, tol=spec.atol)
-        ipi_sharded = sharded_ipi(solve_sharded_native, shard, ctx, opts, dev, dist)
+        try:
+            from paper_2507_22538_b200.parallel import solve_sharded_native
+            opts = ipi.SolveOptions(alpha=spec.alpha, tol=spec.atol)
+            ipi_sharded = sharded_ipi(solve_sharded_native, shard, ctx, opts, dev, dist)
+        except Exception as exc:  # noqa: BLE001
+            ipi_sharded = {"error": f"{type(exc).__name__}: {exc}"[:400]}
     c5 = None
     if world > 1 and not args.no_c5:
         del shard
         torch.cuda.empty_cache()
-        c5 = run_c5(args, ipi, dev, dist, world, local)
+        try:
+            c5 = run_c5(args, ipi, dev, dist, world, local)
+        except Exception as exc:  # noqa: BLE001
+            c5 = {"error": f"{type(exc).__name__}: {exc}"[:400]}
+            torch.cuda.empty_cache()
     out = None
     if rank == 0:
         cpu = None
