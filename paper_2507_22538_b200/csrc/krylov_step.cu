@@ -27,7 +27,11 @@
 // are two-level deterministic (fixed intra-CTA trees, CTA partials added in
 // CTA order), so reruns are bit-identical.
 #include <algorithm>
+#include <atomic>
+#include <map>
+#include <mutex>
 #include <string>
+#include <utility>
 
 #include "krylov.cuh"
 
@@ -735,13 +739,20 @@ int stepped_gmres(const ipi_op* op, int64_t n, const double* b, double* x, doubl
   const int blocks = sms;
   if (ws_doubles < stepped_gmres_workspace(n, blocks))
     return fail(IPI_ERESOURCE, "stepped GMRES: workspace too small");
-  // mapped host flags, one block per device (pinned allocations are slow to make)
-  static StepFlags* h_flags[64] = {};
-  if (dev < 0 || dev >= 64) return fail(IPI_ECUDA, "device index out of range");
-  if (!h_flags[dev]) IPI_CUDA_TRY(cudaHostAlloc(&h_flags[dev], sizeof(StepFlags), cudaHostAllocMapped));
-  volatile StepFlags* hf = h_flags[dev];
+  // mapped host flags, one block per (device, stream): pinned allocations are
+  // slow to make, and two solves on two streams must not share a mirror
+  static std::mutex flags_mu;
+  static std::map<std::pair<int, cudaStream_t>, StepFlags*> flags_of;
+  StepFlags* h_flags = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(flags_mu);
+    StepFlags*& slot = flags_of[{dev, st}];
+    if (!slot) IPI_CUDA_TRY(cudaHostAlloc(&slot, sizeof(StepFlags), cudaHostAllocMapped));
+    h_flags = slot;
+  }
+  volatile StepFlags* hf = h_flags;
   StepFlags* hf_dev = nullptr;
-  IPI_CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&hf_dev), h_flags[dev], 0));
+  IPI_CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&hf_dev), h_flags, 0));
   StepArgs a{};
   a.n = n;
   a.b = b;
@@ -780,7 +791,7 @@ int stepped_gmres(const ipi_op* op, int64_t n, const double* b, double* x, doubl
     if (per_sm < 1) return fail(IPI_ECUDA, "step_ortho cannot be resident");
   }
   // IPI_STEP_PDL=0: plain stream order between the K3 and step_ortho launches
-  static int pdl_ok = getenv("IPI_STEP_PDL") ? atoi(getenv("IPI_STEP_PDL")) : 1;
+  static std::atomic<int> pdl_ok{getenv("IPI_STEP_PDL") ? atoi(getenv("IPI_STEP_PDL")) : 1};
   auto coop = [&](const void* fn, int smem = 0, bool pdl = false) -> int {
     void* args[] = {(void*)&a};
     a.pdl = pdl && pdl_ok ? 1 : 0;
@@ -842,7 +853,7 @@ int stepped_gmres(const ipi_op* op, int64_t n, const double* b, double* x, doubl
   int issued = 0, waited = 0;
   auto issue = [&]() -> int {
     int e;
-    if ((e = op_launch(op, a.V + (int64_t)issued * a.ldv, nullptr, 1, a.w, st, nullptr, active, pdl_ok))) return e;
+    if ((e = op_launch(op, a.V + (int64_t)issued * a.ldv, nullptr, 1, a.w, st, nullptr, active, pdl_ok.load()))) return e;
     if ((e = pair ? coop((const void*)step_ortho_pair, kPairSmem, true) : coop((const void*)step_ortho, 0, true)))
       return e;
     a.call_base += R + 2;  // a launch makes at most R + 1 calls
