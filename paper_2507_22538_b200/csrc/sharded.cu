@@ -14,15 +14,22 @@
 // Arnoldi orthogonalisation is CGS2 (classical Gram-Schmidt with one full
 // re-orthogonalisation): 3 all-gathers of partials per step whatever j,
 // against MGS's j+2 (inner.py:251-253), the choice SURVEY §8(e) names for
-// multi-GPU runs.  The host synchronises once per Arnoldi step (mapped flags:
-// the break decision) and once per outer iteration (the Bellman residual);
-// all vector work runs in the kernels below and the K1/K2/K3 kernels of the
-// single-GPU path on the rank's rows.
+// multi-GPU runs.  The host stays one Arnoldi step ahead of the device: it
+// enqueues step j+1 (kernels and collectives) and only then waits for step
+// j's event and reads the break decision from mapped flags; a step the
+// previous one ended skips itself on the device (every kernel reads
+// state.active; the collectives still run, on every rank alike, and move stale
+// partials nobody reads).  One more synchronisation per outer iteration (the
+// Bellman residual).  All vector work runs in the kernels below and the
+// K1/K2/K3 kernels of the single-GPU path on the rank's rows.
 #include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "krylov.cuh"
@@ -115,26 +122,52 @@ __device__ __forceinline__ bool sh_finish(const double* bs, int cnt, double* blk
   return true;
 }
 
+// The sweeps below take two consecutive elements per thread and step (16-byte
+// loads: ldv is even and every vector starts 16-byte aligned); an odd last
+// element is handled by the grid's first thread.  sh_elems(a, f) calls
+// f(i, pair) for this thread's elements in a fixed order.
+template <class F>
+__device__ __forceinline__ void sh_elems(const ShArgs& a, F&& f) {
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t n2 = a.n >> 1;
+  for (int64_t p = gtid; p < n2; p += stride) f(2 * p, true);
+  if ((a.n & 1) && gtid == 0) f(a.n - 1, false);
+}
+__device__ __forceinline__ double2 sh_ld2(const double* p, bool pair) {
+  return pair ? *reinterpret_cast<const double2*>(p) : make_double2(*p, 0.0);
+}
+__device__ __forceinline__ void sh_st2(double* p, double2 v, bool pair) {
+  if (pair) *reinterpret_cast<double2*>(p) = v;
+  else *p = v.x;
+}
+
 // Pass 1 of a CGS2 step: (optionally w <- pc(w)), partials <V_l, w> (l <= j), <w, w>.
 __global__ void __launch_bounds__(kShT) sh_dots1(ShArgs a, int j, int apply_pc) {
   __shared__ double red[8 * 32], bs[kPartStride];
+  if (!a.s->active) return;  // uniform: the previous step ended the cycle
   const int cnt = j + 2;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int l0 = 0; l0 < cnt; l0 += 8) {
     double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride) {
-      double wi = a.w[i];
+    sh_elems(a, [&](int64_t i, bool pair) {
+      double2 wi = sh_ld2(a.w + i, pair);
       if (l0 == 0 && apply_pc && a.invd) {  // w = pc(A v_j) (inner.py:249), once
-        wi = mul_rn(wi, a.invd[i]);
-        a.w[i] = wi;
+        const double2 d = sh_ld2(a.invd + i, pair);
+        wi.x = mul_rn(wi.x, d.x);
+        wi.y = mul_rn(wi.y, d.y);
+        sh_st2(a.w + i, wi, pair);
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int l = l0 + u;
-        if (l <= j) acc[u] = add_rn(acc[u], mul_rn(a.V[(int64_t)l * a.ldv + i], wi));
-        else if (l == j + 1) acc[u] = add_rn(acc[u], mul_rn(wi, wi));
+        if (l <= j) {
+          const double2 v = sh_ld2(a.V + (int64_t)l * a.ldv + i, pair);
+          acc[u] = add_rn(add_rn(acc[u], mul_rn(v.x, wi.x)), mul_rn(v.y, wi.y));
+        } else if (l == j + 1) {
+          acc[u] = add_rn(add_rn(acc[u], mul_rn(wi.x, wi.x)), mul_rn(wi.y, wi.y));
+        }
       }
-    }
+    });
     sh_block8(acc, l0, cnt, bs, red);
   }
   sh_finish(bs, cnt, a.blk, a.ticket, a.part_out);
@@ -146,36 +179,41 @@ __global__ void __launch_bounds__(kShT) sh_dots1(ShArgs a, int j, int apply_pc) 
 // re-orthogonalisation pass); mode 2 only <w, w>.
 __global__ void __launch_bounds__(kShT) sh_update(ShArgs a, int j, int cnt_in, int mode) {
   __shared__ double red[8 * 32], bs[kPartStride], coef[kPartStride];
+  if (!a.s->active) return;  // uniform: the previous step ended the cycle
   if ((int)threadIdx.x <= j) coef[threadIdx.x] = rank_sum(a.parts, a.world, cnt_in, threadIdx.x);
   __syncthreads();
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     for (int l = 0; l <= j; ++l)
       a.s->H[l * R + j] = mode == 1 ? coef[l] : add_rn(a.s->H[l * R + j], coef[l]);
   }
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int cnt = mode == 1 ? j + 2 : 1;
   for (int l0 = 0; l0 < cnt; l0 += 8) {
     double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride) {
-      double wi;
+    sh_elems(a, [&](int64_t i, bool pair) {
+      double2 wi = sh_ld2(a.w + i, pair);
       if (l0 == 0) {  // the update, once per element (l ascending, separate roundings)
-        wi = a.w[i];
-        for (int l = 0; l <= j; ++l) wi = sub_rn(wi, mul_rn(coef[l], a.V[(int64_t)l * a.ldv + i]));
-        a.w[i] = wi;
-      } else {
-        wi = a.w[i];
+        for (int l = 0; l <= j; ++l) {
+          const double2 v = sh_ld2(a.V + (int64_t)l * a.ldv + i, pair);
+          wi.x = sub_rn(wi.x, mul_rn(coef[l], v.x));
+          wi.y = sub_rn(wi.y, mul_rn(coef[l], v.y));
+        }
+        sh_st2(a.w + i, wi, pair);
       }
       if (mode == 1) {
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int l = l0 + u;
-          if (l <= j) acc[u] = add_rn(acc[u], mul_rn(a.V[(int64_t)l * a.ldv + i], wi));
-          else if (l == j + 1) acc[u] = add_rn(acc[u], mul_rn(wi, wi));
+          if (l <= j) {
+            const double2 v = sh_ld2(a.V + (int64_t)l * a.ldv + i, pair);
+            acc[u] = add_rn(add_rn(acc[u], mul_rn(v.x, wi.x)), mul_rn(v.y, wi.y));
+          } else if (l == j + 1) {
+            acc[u] = add_rn(add_rn(acc[u], mul_rn(wi.x, wi.x)), mul_rn(wi.y, wi.y));
+          }
         }
       } else {
-        acc[0] = add_rn(acc[0], mul_rn(wi, wi));
+        acc[0] = add_rn(add_rn(acc[0], mul_rn(wi.x, wi.x)), mul_rn(wi.y, wi.y));
       }
-    }
+    });
     sh_block8(acc, l0, cnt, bs, red);
   }
   sh_finish(bs, cnt, a.blk, a.ticket, a.part_out);
@@ -189,13 +227,18 @@ __device__ __forceinline__ void sh_publish(const ShArgs& a, const ShState& s) {
   f->done = s.done;
   f->brk = s.brk;
   f->rn = s.rn;
-  __threadfence_system();
+  // no system fence: the host reads the mirror only after synchronising on an
+  // event (or the stream) behind this launch
 }
 
 // Givens update and break test (inner.py:255-270) on the completed column j.
 __global__ void sh_givens(ShArgs a, int j) {
   if (threadIdx.x != 0) return;
   ShState* st = a.s;
+  if (!st->active) {  // a step enqueued past the cycle's end: nothing to normalise either
+    st->brk = 3;
+    return;
+  }
   const double hnorm = sqrt(rank_sum(a.parts, a.world, 1, 0));
   double* H = st->H;
   H[(j + 1) * R + j] = hnorm;
@@ -226,7 +269,7 @@ __global__ void sh_givens(ShArgs a, int j) {
   sh_publish(a, *st);
 }
 
-// V_{j+1} = w / hnorm (only when the step did not break)
+// V_{j+1} = w / hnorm (only when the step ran and did not break)
 __global__ void __launch_bounds__(kShT) sh_normalize(ShArgs a) {
   const ShState* st = a.s;
   if (st->brk != 0) return;
@@ -417,7 +460,10 @@ int ipi_solve_sharded(ipi_mdp* h, const ipi_comm* comm, const ipi_opts* o, doubl
   int dev = 0, sms = 148;
   IPI_CUDA_TRY(cudaGetDevice(&dev));
   IPI_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const int nblk = 2 * sms;
+  static const int nblk_mult = getenv("IPI_SH_NBLK") ? atoi(getenv("IPI_SH_NBLK")) : 4;  // blocks per SM of the vector sweeps: 4 measured best (C2, world 1: 51.7 / 41.1 / 43.9 ms of inner
+  // time at 2 / 4 / 6; occupancy, not per-thread loads in flight, is what these sweeps need: a
+  // register-resident single-sweep variant of the re-orthogonalisation pass measured 42.8-47.3 ms)
+  const int nblk = nblk_mult * sms;
   const auto t_start = std::chrono::steady_clock::now();
   // ---- workspace (stream-ordered) -----------------------------------------
   ShWork W;
@@ -446,12 +492,28 @@ int ipi_solve_sharded(ipi_mdp* h, const ipi_comm* comm, const ipi_opts* o, doubl
   W.res = p; p += 2;
   W.s = reinterpret_cast<ShState*>(p);
   IPI_CUDA_TRY(cudaMemsetAsync(W.ticket, 0, 64, st));
-  static ShFlags* h_flags[64] = {};
-  if (dev < 0 || dev >= 64) return fail(IPI_ECUDA, "device index out of range");
-  if (!h_flags[dev]) IPI_CUDA_TRY(cudaHostAlloc(&h_flags[dev], sizeof(ShFlags), cudaHostAllocMapped));
-  volatile ShFlags* hf = h_flags[dev];
+  // mapped host flags, one block per (device, stream)
+  static std::mutex flags_mu;
+  static std::map<std::pair<int, cudaStream_t>, ShFlags*> flags_of;
+  ShFlags* h_flags = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(flags_mu);
+    ShFlags*& slot = flags_of[{dev, st}];
+    if (!slot) IPI_CUDA_TRY(cudaHostAlloc(&slot, sizeof(ShFlags), cudaHostAllocMapped));
+    h_flags = slot;
+  }
+  volatile ShFlags* hf = h_flags;
   ShFlags* hf_dev = nullptr;
-  IPI_CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&hf_dev), h_flags[dev], 0));
+  IPI_CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&hf_dev), h_flags, 0));
+  cudaEvent_t step_ev[2] = {};
+  struct EvGuard {
+    cudaEvent_t* e;
+    ~EvGuard() {
+      for (int i = 0; i < 2; ++i)
+        if (e[i]) cudaEventDestroy(e[i]);
+    }
+  } ev_guard{step_ev};
+  for (int i = 0; i < 2; ++i) IPI_CUDA_TRY(cudaEventCreateWithFlags(&step_ev[i], cudaEventDisableTiming));
   ShArgs a{};
   a.n = n;
   a.ldv = ldv;
@@ -580,26 +642,38 @@ int ipi_solve_sharded(ipi_mdp* h, const ipi_comm* comm, const ipi_opts* o, doubl
       sh_cycle_begin<<<nblk, kShT, 0, st>>>(a);
       IPI_LAUNCH_CHECK();
       if ((rc = sync())) return rc;
+      const int* active = &W.s->active;
       while (!hf->done) {
-        int j = 0;
-        while (true) {
+        // Arnoldi steps, one enqueued ahead of the one the host waits for
+        int issued = 0, waited = 0;
+        auto issue = [&]() -> int {
+          const int j = issued;
+          int e;
           // w = A V_j on the rank's rows (the Krylov vector assembled first)
-          if ((rc = gather_vec(W.V + (int64_t)j * ldv))) return rc;
-          if ((rc = op_launch(h->op_pi, W.xfull, nullptr, 1, W.w, st))) return rc;
+          if ((e = gather_vec(W.V + (int64_t)j * ldv))) return e;
+          if ((e = op_launch(h->op_pi, W.xfull, nullptr, 1, W.w, st, nullptr, active))) return e;
           sh_dots1<<<nblk, kShT, 0, st>>>(a, j, 1);
-          if ((rc = gather_parts(j + 2))) return rc;
+          if ((e = gather_parts(j + 2))) return e;
           sh_update<<<nblk, kShT, 0, st>>>(a, j, j + 2, 1);
-          if ((rc = gather_parts(j + 2))) return rc;
+          if ((e = gather_parts(j + 2))) return e;
           sh_update<<<nblk, kShT, 0, st>>>(a, j, j + 2, 2);
-          if ((rc = gather_parts(1))) return rc;
+          if ((e = gather_parts(1))) return e;
           sh_givens<<<1, 32, 0, st>>>(a, j);
           sh_normalize<<<nblk, kShT, 0, st>>>(a);
           IPI_LAUNCH_CHECK();
-          if ((rc = sync())) return rc;
-          its = hf->it;
-          j = hf->j;
-          if (!hf->active) break;
+          IPI_CUDA_TRY(cudaEventRecord(step_ev[issued & 1], st));
+          ++issued;
+          return IPI_OK;
+        };
+        if ((rc = issue())) return rc;
+        while (true) {
+          if (issued < R && issued == waited + 1 && (rc = issue())) return rc;
+          IPI_CUDA_TRY(cudaEventSynchronize(step_ev[waited & 1]));
+          ++waited;
+          if (!hf->active) break;       // steps enqueued beyond it skip themselves
+          if (waited >= issued) break;  // R steps issued and all done
         }
+        its = hf->it;
         if (hf->j == 0) break;  // inner.py:271-272
         sh_cycle_end<<<nblk, kShT, 0, st>>>(a);
         if ((rc = gather_vec(W.x))) return rc;
