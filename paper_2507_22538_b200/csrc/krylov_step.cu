@@ -444,9 +444,12 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_ortho(StepArgs a) {
 // correction for a basis that has lost orthogonality (G is the measured
 // inner product, ~1e-16 here, not assumed zero).  w is then updated as MGS
 // does, (w - h_l V_l) - h_{l+1} V_{l+1}.  h_l is bitwise MGS's; h_{l+1}
-// differs from it by rounding of order eps |w|.  The inner products use fused
-// multiply-adds (the reference's are BLAS dots, whose rounding order is not
-// specified either); the w updates keep numpy's separate mul / sub roundings.
+// differs from it by rounding of order eps |w|.  Inner products and updates use
+// fused multiply-adds: the reference's dots are BLAS dots, whose rounding order
+// is not specified, so the h_l are not bitwise the reference's in any case, and
+// the FP64 pipe is what the compute phase of a pass waits for (7 -> 5
+// instructions per element and pair).  IPI_STEP_PAIR=0 keeps numpy's separate
+// mul / add roundings throughout.
 //
 // Data movement: the pair in use lives in registers (va, vb); the next pair is
 // copied into shared memory with cp.async (16-byte chunks, every thread copies
@@ -559,9 +562,9 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_ortho_pair(StepArgs a) {
       if (two) hcol[l + 1] = h1;
     }
 #pragma unroll
-    for (int k = 0; k < kStepE; ++k) {
-      wv[k] = sub_rn(wv[k], mul_rn(h0, va[k]));
-      if (two) wv[k] = sub_rn(wv[k], mul_rn(h1, vb[k]));
+    for (int k = 0; k < kStepE; ++k) {  // (w - h_l V_l) - h_{l+1} V_{l+1}, one rounding per term
+      wv[k] = fma(-h0, va[k], wv[k]);
+      if (two) wv[k] = fma(-h1, vb[k], wv[k]);
     }
     double q0 = 0.0, q1 = 0.0, q2 = 0.0;
     if (more) {

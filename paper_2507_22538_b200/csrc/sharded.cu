@@ -232,41 +232,56 @@ __device__ __forceinline__ void sh_publish(const ShArgs& a, const ShState& s) {
 }
 
 // Givens update and break test (inner.py:255-270) on the completed column j.
+// One warp: the column and the rotations are loaded and stored by 32 lanes
+// (thread 0 alone paid one dependent global round trip per operand: ~10 us per
+// step), the recurrence itself runs in thread 0 on shared memory.
 __global__ void sh_givens(ShArgs a, int j) {
-  if (threadIdx.x != 0) return;
+  __shared__ double hc[R + 2], cs_s[R], sn_s[R];
   ShState* st = a.s;
+  const int t = threadIdx.x;
   if (!st->active) {  // a step enqueued past the cycle's end: nothing to normalise either
-    st->brk = 3;
+    if (t == 0) st->brk = 3;
     return;
   }
-  const double hnorm = sqrt(rank_sum(a.parts, a.world, 1, 0));
-  double* H = st->H;
-  H[(j + 1) * R + j] = hnorm;
-  for (int l = 0; l < j; ++l) {
-    const double hl = H[l * R + j], hl1 = H[(l + 1) * R + j];
-    const double t = add_rn(mul_rn(st->cs[l], hl), mul_rn(st->sn[l], hl1));
-    H[(l + 1) * R + j] = add_rn(mul_rn(-st->sn[l], hl), mul_rn(st->cs[l], hl1));
-    H[l * R + j] = t;
+  if (t <= j) hc[t] = st->H[t * R + j];
+  if (t < j) {
+    cs_s[t] = st->cs[t];
+    sn_s[t] = st->sn[t];
   }
-  const double denom = hypot(H[j * R + j], H[(j + 1) * R + j]);
-  int brk = 0;
-  if (denom == 0.0) {
-    brk = 1;
-  } else {
-    st->cs[j] = H[j * R + j] / denom;
-    st->sn[j] = H[(j + 1) * R + j] / denom;
-    H[j * R + j] = denom;
-    H[(j + 1) * R + j] = 0.0;
-    st->g[j + 1] = mul_rn(-st->sn[j], st->g[j]);
-    st->g[j] = mul_rn(st->cs[j], st->g[j]);
-    if (fabs(st->g[j + 1]) <= st->est_target || hnorm == 0.0) brk = 2;
+  __syncwarp();
+  if (t == 0) {
+    const double hnorm = sqrt(rank_sum(a.parts, a.world, 1, 0));
+    hc[j + 1] = hnorm;
+    for (int l = 0; l < j; ++l) {
+      const double hl = hc[l], hl1 = hc[l + 1];
+      hc[l] = add_rn(mul_rn(cs_s[l], hl), mul_rn(sn_s[l], hl1));
+      hc[l + 1] = add_rn(mul_rn(-sn_s[l], hl), mul_rn(cs_s[l], hl1));
+    }
+    const double denom = hypot(hc[j], hc[j + 1]);
+    int brk = 0;
+    if (denom == 0.0) {
+      brk = 1;
+    } else {
+      const double csj = hc[j] / denom, snj = hc[j + 1] / denom;
+      st->cs[j] = csj;
+      st->sn[j] = snj;
+      hc[j] = denom;
+      hc[j + 1] = 0.0;
+      const double gj = st->g[j];
+      const double gj1 = mul_rn(-snj, gj);
+      st->g[j + 1] = gj1;
+      st->g[j] = mul_rn(csj, gj);
+      if (fabs(gj1) <= st->est_target || hnorm == 0.0) brk = 2;
+    }
+    st->hnorm = hnorm;
+    st->brk = brk;
+    st->it += 1;
+    st->j = brk == 1 ? j : j + 1;
+    st->active = (brk == 0 && st->j < R && st->it < a.max_it) ? 1 : 0;
+    sh_publish(a, *st);
   }
-  st->hnorm = hnorm;
-  st->brk = brk;
-  st->it += 1;
-  st->j = brk == 1 ? j : j + 1;
-  st->active = (brk == 0 && st->j < R && st->it < a.max_it) ? 1 : 0;
-  sh_publish(a, *st);
+  __syncwarp();
+  if (t <= j + 1) st->H[t * R + j] = hc[t];
 }
 
 // V_{j+1} = w / hnorm (only when the step ran and did not break)
