@@ -666,7 +666,7 @@ int ipi_op_create(const int64_t* rp, const int32_t* col, const double* val, int6
                       cudaMemsetAsync(tx, 0, sizeof(double) * n_global, st) == cudaSuccess;
       best = !ok ? -1 : autotune_pick(
           nc, [&](int i) { const int* c = shape(i); return install(c[0], c[1], c[2], c[3] != 0, c[4]); },
-          [&] { return op_launch(op, tx, nullptr, 1, ty, st); }, st, 3);
+          [&] { return op_launch(op, tx, nullptr, 1, ty, st); }, st, 3, 3, 10);
       cudaFree(tx);
       cudaFree(ty);
       cudaGetLastError();

@@ -414,7 +414,7 @@ static int plan_uniform_ring(PlanCtx& c) {
       const int best = !tmp.ok ? -1 : autotune_pick(
           8, [&](int i) { return install(12, 3, cand[i], 1); },
           [&] { return launch_bellman(h, tmp.v, IPI_MODE_MIN, tmp.policy, tmp.applied, nullptr,
-                                      nullptr, nullptr, st); }, st);
+                                      nullptr, nullptr, st); }, st, 1, 3, 2);
       if (best >= 0) install(12, 3, cand[best], 1);
       else install(shapes[0][0], shapes[0][1], shapes[0][2], shapes[0][3]);
     }

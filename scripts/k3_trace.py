@@ -68,6 +68,18 @@ def main():
                          "start_spread_us": (t0.max() - base) / 1e3,
                          "end_spread_us": (t1.max() - t1.min()) / 1e3,
                          "cta_us_min": dur.min(), "cta_us_median": float(np.median(dur)), "cta_us_max": dur.max()})
+        if os.environ.get("K3_TRACE_DETAIL"):
+            # last repetition: per-CTA duration by block index and by SM id
+            sm = tr[:, 0]
+            order = np.argsort(dur)
+            print("slowest 12 (block, sm, us):", [(int(b), int(sm[b]), round(float(dur[b]), 1)) for b in order[-12:]])
+            print("fastest 12 (block, sm, us):", [(int(b), int(sm[b]), round(float(dur[b]), 1)) for b in order[:12]])
+            print("by block decile (mean us):", [round(float(dur[k * nb // 10:(k + 1) * nb // 10].mean()), 1) for k in range(10)])
+            prev = getattr(main, "_prev", None)
+            if prev is not None and len(prev) == len(dur):
+                print("corr with previous shape's per-block durations:", round(float(np.corrcoef(prev, dur)[0, 1]), 3))
+            main._prev = dur.copy()
+            main._runs = getattr(main, "_runs", []) + [dur.copy()]
         med = {k: float(np.median([r[k] for r in recs])) for k in recs[0]}
         print(json.dumps({"shape": sh, "blocks": nb, **{k: round(v_, 2) for k, v_ in med.items()}}), flush=True)
         del op
