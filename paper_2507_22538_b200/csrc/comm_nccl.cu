@@ -12,6 +12,8 @@
 // single-GPU path never touches it.
 #include <dlfcn.h>
 
+#include <cstdlib>
+
 #include <mutex>
 #include <string>
 #include <vector>
@@ -54,6 +56,7 @@ struct NcclCtx {
   int rank, world;
   std::vector<int64_t> start;
   bool equal;
+  bool local;  // one rank and no communicator (or not forced): plain device copies
 };
 
 int nccl_fail(nccl_result r, const char* what) {
@@ -65,7 +68,7 @@ int nccl_allgather_blocks(void* ctx, const double* local, double* full, void* st
   auto* c = static_cast<NcclCtx*>(ctx);
   NcclApi& api = nccl();
   cudaStream_t st = (cudaStream_t)stream;
-  if (c->world == 1) {
+  if (c->local) {
     if (full != local) {
       const cudaError_t e = cudaMemcpyAsync(full, local, sizeof(double) * (c->start[1] - c->start[0]),
                                             cudaMemcpyDeviceToDevice, st);
@@ -91,7 +94,7 @@ int nccl_allgather_blocks(void* ctx, const double* local, double* full, void* st
 
 int nccl_allgather(void* ctx, const double* send, double* out, int64_t count, void* stream) {
   auto* c = static_cast<NcclCtx*>(ctx);
-  if (c->world == 1) {
+  if (c->local) {
     const cudaError_t e = cudaMemcpyAsync(out, send, sizeof(double) * count, cudaMemcpyDeviceToDevice,
                                           (cudaStream_t)stream);
     return e != cudaSuccess ? ipi::fail(IPI_ECUDA, cudaGetErrorString(e)) : IPI_OK;
@@ -110,10 +113,16 @@ int ipi_comm_nccl(void* nccl_comm, int32_t rank, int32_t world, const int64_t* b
   if (!out || !block_start) return ipi::fail(IPI_EVALIDATION, "null argument");
   if (world < 1 || rank < 0 || rank >= world) return ipi::fail(IPI_EVALIDATION, "bad rank / world");
   if (world > 1 && !nccl_comm) return ipi::fail(IPI_EVALIDATION, "null NCCL communicator");
-  if (world > 1 && !nccl().ok)
+  // One rank normally needs no NCCL at all; IPI_COMM_FORCE_NCCL=1 sends a
+  // one-rank communicator's exchanges through ncclAllGather / ncclBroadcast
+  // anyway (how the binding is exercised on a single-GPU box).
+  const bool force = nccl_comm && getenv("IPI_COMM_FORCE_NCCL") && atoi(getenv("IPI_COMM_FORCE_NCCL")) != 0;
+  const bool use_nccl = world > 1 || force;
+  if (use_nccl && !nccl().ok)
     return ipi::fail(IPI_ECUDA, "libnccl.so.2 not found (load torch.distributed's NCCL first)");
   auto* c = new NcclCtx{nccl_comm, rank, world, std::vector<int64_t>(block_start, block_start + world + 1),
-                        true};
+                        true, !use_nccl};
+  if (force && world == 1 && getenv("IPI_COMM_FORCE_NCCL")[0] == '2') c->equal = false;  // the broadcast path
   for (int q = 1; q < world; ++q)
     if (c->start[q + 1] - c->start[q] != c->start[1] - c->start[0]) c->equal = false;
   out->ctx = c;

@@ -708,7 +708,9 @@ class NativeComm:
         self._starts = starts
         L = _lib.lib()
         self.kind = "local"
-        if R > 1 and dist.get_backend() == "nccl":
+        import os
+        force = bool(int(os.environ.get("IPI_COMM_FORCE_NCCL", "0") or 0))
+        if (R > 1 or force) and dist.is_initialized() and dist.get_backend() == "nccl":
             # the communicator exists once a collective ran (eager init otherwise)
             dist.barrier()
             pg = dist.distributed_c10d._get_default_group()

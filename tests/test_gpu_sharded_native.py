@@ -235,3 +235,54 @@ def test_per_rank_callback_construction_solves_like_one_process():
     assert status == ref.status.value and outer == ref.outer_iterations
     np.testing.assert_allclose(values, ref.values, rtol=1e-8, atol=1e-8)
     np.testing.assert_array_equal(policy, ref.policy)
+
+
+def _nccl_world1_worker(q, force):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()), RANK="0", WORLD_SIZE="1",
+                      IPI_COMM_FORCE_NCCL=force)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        from paper_2507_22538_b200.parallel import MdpShard, NativeComm, RankContext, solve_sharded_native
+        n = 8191  # odd: the last 16-byte chunk of every vector is half-filled
+        ctx = RankContext.from_env(n)
+        lo, hi = ctx.block
+        rp, col, val, cost = devgen.locality(n, M, K, W, 0, lo, hi - lo)
+        shard = MdpShard(n, M, GAMMA, lo, cost, ipi.CsrMatrix((hi - lo) * M, n, rp, col, val))
+        comm = NativeComm(ctx)
+        res = solve_sharded_native(shard, ctx, ipi.SolveOptions(alpha=1e-4, tol=1e-8, max_outer=300),
+                                   comm=comm)
+        q.put((comm.kind, res.status.value, res.outer_iterations, res.inner_iterations_total,
+               res.values.tolist(), res.policy.tolist()))
+    except Exception as exc:  # pragma: no cover - reported by the parent
+        q.put(("error", repr(exc), None, None, None, None))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_binding_on_a_one_rank_communicator():
+    """The NCCL path of ipi_comm (comm_nccl.cu: dlopen'd ncclAllGather and the
+    grouped ncclBroadcast all-gather-v, torch's own communicator through
+    ProcessGroupNCCL._comm_ptr) exercised on the one GPU there is: a one-rank
+    communicator, with IPI_COMM_FORCE_NCCL sending the driver's exchanges
+    through NCCL instead of the one-rank device copies.  Results must be
+    bitwise those of the copy path (a one-rank all-gather / broadcast is a
+    copy): this checks symbol resolution, argument order, the dtype enum and
+    stream ordering, not multi-GPU behaviour."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    outs = {}
+    for force in ("0", "1", "2"):  # copies / ncclAllGather / grouped ncclBroadcast
+        q = ctx.Queue()
+        p = ctx.Process(target=_nccl_world1_worker, args=(q, force))
+        p.start()
+        outs[force] = q.get(timeout=600)
+        p.join(timeout=120)
+        assert outs[force][0] != "error", outs[force]
+        assert p.exitcode == 0
+    assert outs["0"][0] == "local" and outs["1"][0] == "nccl" and outs["2"][0] == "nccl"
+    assert outs["1"][1:] == outs["0"][1:]
+    assert outs["2"][1:] == outs["0"][1:]
+    assert outs["0"][1] == "converged"
