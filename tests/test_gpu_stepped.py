@@ -46,19 +46,20 @@ from paper_2507_22538_b200 import devgen
 n, m, K, W, gamma = {n}, {m}, {k}, {w}, {gamma}
 rp, col, val, cost = devgen.locality(n, m, K, W, 0, 0, n)
 mdp = ipi.MdpInstance(n, m, gamma, cost, ipi.CsrMatrix(n * m, n, rp, col, val))
-res = ipi.solve(mdp, ipi.SolveOptions(alpha=1e-4, tol=1e-8, gmres_ortho="mgs"))
+pc = ipi.Preconditioner.from_name(sys.argv[2] if len(sys.argv) > 2 else "none")
+res = ipi.solve(mdp, ipi.SolveOptions(alpha=1e-4, tol=1e-8, gmres_ortho="mgs", pc=pc))
 np.save(sys.argv[1], res.values)
 print(json.dumps({{"status": res.status.value, "outer": res.outer_iterations,
                   "inner": res.inner_iterations_total, "hist": res.residual_history}}))
 """
 
 
-def _child(tmp_path, tag, env):
+def _child(tmp_path, tag, env, pc="none"):
     out = tmp_path / f"v_{tag}.npy"
     code = _CHILD.format(repo=str(REPO), n=N, m=M, k=K, w=W, gamma=GAMMA)
     e = dict(os.environ)
     e.update(env)
-    r = subprocess.run([sys.executable, "-c", code, str(out)], capture_output=True, text=True, env=e,
+    r = subprocess.run([sys.executable, "-c", code, str(out), pc], capture_output=True, text=True, env=e,
                        timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     info = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
@@ -88,3 +89,24 @@ def test_stepped_default_matches_c_oracle_and_switches_agree(tmp_path):
     # programmatic dependent launch changes no arithmetic: bitwise equal results
     _, v_nopdl = _child(tmp_path, "nopdl2", {"IPI_STEP_PDL": "0"})
     assert np.array_equal(v_nopdl, v)
+
+
+def test_stepped_with_jacobi_agrees_with_the_persistent_kernel(tmp_path):
+    """Left Jacobi preconditioning (inner.py:113-118) through the stepped
+    solver (w = pc(A v_j) in step_ortho, z = pc(r) in step_cycle_start) against
+    the persistent kernel on the same instance, and the fixed point against
+    the unpreconditioned C oracle solve."""
+    from oracle import c_oracle as co
+    from paper_2507_22538_b200 import devgen
+
+    a, va = _child(tmp_path, "jac_stepped", {}, pc="jacobi")
+    b, vb = _child(tmp_path, "jac_persistent", {"IPI_K4_STEPPED": "0"}, pc="jacobi")
+    assert a["status"] == b["status"] == "converged"
+    assert a["outer"] == b["outer"]
+    scale = max(1.0, np.abs(vb).max())
+    np.testing.assert_allclose(va, vb, rtol=1e-10, atol=1e-10 * scale)
+    rp, col, val, cost = (t.cpu().numpy() for t in devgen.locality(N, M, K, W, 0, 0, N))
+    ref = co.solve(rp, col, val, cost, GAMMA, tol=1e-8, alpha=1e-4, kind="gmres")
+    np.testing.assert_allclose(va, ref.values, rtol=1e-8, atol=1e-8 * scale)
+    _, _, r = co.greedy(rp, col, val, cost, GAMMA, va)
+    assert r <= 1e-8 * 1.0001
