@@ -47,20 +47,23 @@ n, m, K, W, gamma = {n}, {m}, {k}, {w}, {gamma}
 rp, col, val, cost = devgen.locality(n, m, K, W, 0, 0, n)
 mdp = ipi.MdpInstance(n, m, gamma, cost, ipi.CsrMatrix(n * m, n, rp, col, val))
 pc = ipi.Preconditioner.from_name(sys.argv[2] if len(sys.argv) > 2 else "none")
-res = ipi.solve(mdp, ipi.SolveOptions(alpha=1e-4, tol=1e-8, gmres_ortho="mgs", pc=pc))
+cap = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+mode = ipi.Mode.from_name(sys.argv[4] if len(sys.argv) > 4 else "min")
+res = ipi.solve(mdp, ipi.SolveOptions(alpha=1e-4, tol=1e-8, gmres_ortho="mgs", pc=pc, mode=mode,
+                                      ksp_max_it=cap or None))
 np.save(sys.argv[1], res.values)
 print(json.dumps({{"status": res.status.value, "outer": res.outer_iterations,
                   "inner": res.inner_iterations_total, "hist": res.residual_history}}))
 """
 
 
-def _child(tmp_path, tag, env, pc="none"):
+def _child(tmp_path, tag, env, pc="none", cap=0, mode="min"):
     out = tmp_path / f"v_{tag}.npy"
     code = _CHILD.format(repo=str(REPO), n=N, m=M, k=K, w=W, gamma=GAMMA)
     e = dict(os.environ)
     e.update(env)
-    r = subprocess.run([sys.executable, "-c", code, str(out), pc], capture_output=True, text=True, env=e,
-                       timeout=600)
+    r = subprocess.run([sys.executable, "-c", code, str(out), pc, str(cap), mode], capture_output=True,
+                       text=True, env=e, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     info = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
     return info, np.load(out)
@@ -110,3 +113,36 @@ def test_stepped_with_jacobi_agrees_with_the_persistent_kernel(tmp_path):
     np.testing.assert_allclose(va, ref.values, rtol=1e-8, atol=1e-8 * scale)
     _, _, r = co.greedy(rp, col, val, cost, GAMMA, va)
     assert r <= 1e-8 * 1.0001
+
+
+@pytest.mark.parametrize("cap", [7, 37])
+def test_stepped_fixed_inner_iterations(tmp_path, cap):
+    """Optimistic-PI style runs (driver.py:170-175: target 0, exactly ksp_max_it
+    inner iterations per outer step): the cap falls inside a cycle (7) and
+    across a restart (37 = 30 + 7); the stepped solver must stop on the same
+    iteration as the persistent kernel."""
+    a, va = _child(tmp_path, f"cap{cap}_stepped", {}, cap=cap)
+    b, vb = _child(tmp_path, f"cap{cap}_persistent", {"IPI_K4_STEPPED": "0"}, cap=cap)
+    assert a["status"] == b["status"]
+    assert a["outer"] == b["outer"]
+    assert a["inner"] == b["inner"] == cap * a["outer"]
+    scale = max(1.0, np.abs(vb).max())
+    np.testing.assert_allclose(va, vb, rtol=1e-9, atol=1e-9 * scale)
+
+
+def test_stepped_max_mode(tmp_path):
+    """MAX mode: K1's TV is the per-state maximum, and r0 = TV - V holds all the
+    same; the stepped solve against the persistent kernel and the C oracle."""
+    from oracle import c_oracle as co
+    from paper_2507_22538_b200 import devgen
+
+    a, va = _child(tmp_path, "max_stepped", {}, mode="max")
+    b, vb = _child(tmp_path, "max_persistent", {"IPI_K4_STEPPED": "0"}, mode="max")
+    assert a["status"] == b["status"] == "converged"
+    assert a["outer"] == b["outer"]
+    scale = max(1.0, np.abs(vb).max())
+    np.testing.assert_allclose(va, vb, rtol=1e-10, atol=1e-10 * scale)
+    rp, col, val, cost = (t.cpu().numpy() for t in devgen.locality(N, M, K, W, 0, 0, N))
+    ref = co.solve(rp, col, val, cost, GAMMA, maximize=True, tol=1e-8, alpha=1e-4, kind="gmres")
+    assert a["status"] == ref.status and a["outer"] == ref.outer_iterations
+    np.testing.assert_allclose(va, ref.values, rtol=1e-8, atol=1e-8 * scale)
