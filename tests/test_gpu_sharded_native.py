@@ -43,7 +43,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, q, n, kind, mode, pc, v0_seed):
+def _worker(rank, world, port, q, n, kind, mode, pc, v0_seed, ksp=None):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
                       WORLD_SIZE=str(world))
@@ -58,7 +58,7 @@ def _worker(rank, world, port, q, n, kind, mode, pc, v0_seed):
         v0 = None if v0_seed is None else np.random.default_rng(v0_seed).random(n) * 100
         opts = ipi.SolveOptions(alpha=1e-4, tol=1e-8, inner=ipi.InnerSolver.from_name(kind),
                                 pc=ipi.Preconditioner.from_name(pc),
-                                mode=ipi.Mode.from_name(mode), max_outer=300, v0=v0)
+                                mode=ipi.Mode.from_name(mode), max_outer=300, v0=v0, ksp_max_it=ksp)
         res = solve_sharded_native(shard, ctx, opts)
         q.put((rank, res.status.value, res.outer_iterations, res.values.tolist(),
                res.policy.tolist(), res.residual_history, res.inner_iterations_total))
@@ -69,12 +69,12 @@ def _worker(rank, world, port, q, n, kind, mode, pc, v0_seed):
         dist.destroy_process_group()
 
 
-def _run(world, n=N, kind="gmres", mode="min", pc="none", v0_seed=None):
+def _run(world, n=N, kind="gmres", mode="min", pc="none", v0_seed=None, ksp=None):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q, n, kind, mode, pc, v0_seed))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, n, kind, mode, pc, v0_seed, ksp))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -165,6 +165,26 @@ def test_gmres_jacobi_two_ranks():
     _, _, r = co.greedy(rp, col, val, cost, GAMMA, np.asarray(values))
     assert r <= 1e-8 * 1.0001
     assert np.max(np.abs(np.asarray(values) - ref.values)) <= 2e-8 / (1 - GAMMA)
+
+
+@pytest.mark.parametrize("ksp", [5, 33])
+def test_fixed_inner_iterations_two_ranks(ksp):
+    """ksp_max_it (driver.py:170-175): exactly that many GMRES iterations per
+    outer step, the cap falling inside a cycle (5) or after a restart (33) —
+    with the host enqueueing one step ahead, the device must stop on the cap
+    and the step enqueued past it must be a no-op."""
+    from oracle import c_oracle as co
+    n = 2 * 4096
+    got = _run(2, n=n, ksp=ksp)
+    rp, col, val, cost = (t.cpu().numpy() for t in devgen.locality(n, M, K, W, 0, 0, n))
+    ref = co.solve(rp, col, val, cost, GAMMA, tol=1e-8, alpha=1e-4, kind="gmres", max_outer=300,
+                   ksp_max_it=ksp)
+    _, status, outer, values, _, history, inner = got
+    assert status == ref.status
+    assert outer == ref.outer_iterations
+    assert inner == ksp * outer == ref.inner_iterations_total
+    scale = max(1.0, np.abs(ref.values).max())
+    np.testing.assert_allclose(np.asarray(values), ref.values, rtol=1e-8, atol=1e-8 * scale)
 
 
 def test_unsupported_kinds_raise():
