@@ -123,6 +123,9 @@ def ncu_traffic(name: str = "k1_c2_ncu.json", alg: float | None = None):
     """DRAM bytes per launch from the committed ncu summary, only when that
     capture is of the same launch (its algorithmic bytes match this one's)."""
     p = REPO / "profiles" / name
+    r2 = REPO / "profiles" / ("r02_" + name)  # this round's capture of the same kernel, when committed
+    if r2.exists():
+        p = r2
     if p.exists():
         d = json.loads(p.read_text())
         ref = d.get("algorithmic_bytes_per_launch")
@@ -521,7 +524,9 @@ def run_ours(args):
         dist.all_reduce(k3_t, op=dist.ReduceOp.MAX)
     k3_ms = float(k3_t[0])
     k3_ach = k3_alg / (k3_ms * 1e-3) / 1e9
-    k3_traffic, _ = ncu_traffic("k3_c2_ncu.json", k3_alg)
+    k3_traffic, _ = ncu_traffic("k3_c2_insolve_ncu.json", k3_alg)
+    if k3_traffic is None:
+        k3_traffic, _ = ncu_traffic("k3_c2_ncu.json", k3_alg)
     roof_inner = {"bound": "hbm", "achieved": k3_ach, "peak": peak, "unit": "GB/s",
                   "frac": k3_ach / peak, "traffic": k3_traffic,
                   "kernel": {1: "k3_uring", 2: "k3_flat"}.get(k3_plan["variant"], "spmv_kernel"),
